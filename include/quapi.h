@@ -1,0 +1,143 @@
+/*
+ * quapi.h -- C ABI of the B200-native QUAPI tensor-propagator library (libquapi.so).
+ *
+ * What it computes: the reduced density matrix rho(t_k) of an open quantum system in the
+ * Feynman-Vernon model (N. S. Dattani, arXiv 1205.6872, PAPER.md = P:<line>):
+ *   rho(t_N) = Eq. 8: sum over forward/backward paths of the bare propagator pair
+ *              <s+_{k+1}|e^{-iH dt}|s+_k><s-_k|e^{+iH dt}|s-_{k+1}>, rho(0), and the discretised
+ *              influence functional Eq. 9 with eta coefficients Eqs. 10-16
+ *              of the bath response Eq. 4 for spectral density J(w) (Eq. 3, Eq. 21) at T.
+ *   Memory truncation: pairs with lag k-k' <= Delta k_max (= dkmax, "L") are kept.
+ *   Evaluation: the iterative tensor-propagator scheme (Makri-Makarov): the augmented
+ *   reduced density matrix (ARDM) of N^L complex FP64 entries (N = M^2 path-pair states) is
+ *   propagated in place on the GPU, one launch per time step, with the rho(t) readout of
+ *   P:384-390 / P:415-418 fused into the same pass.  Readings of the paper (windows, limits,
+ *   conventions) are listed in DESIGN.md §3.
+ *
+ * The problem statement follows the paper's abstract and §II: system
+ * coordinate vector s, Hamiltonian H, spectral density + temperature (or G/alpha given directly),
+ * rho(0), time grid {k dt}, Delta k_max; output rho at the requested time indices
+ * ("allPointsOrJustFinalPoint", generalised to a list).
+ *
+ * Conventions
+ *   - hbar = k_B = 1.  Complex numbers are qp_c64 {re, im} (binary-compatible with double2 and
+ *     std::complex<double>).  Matrices are row-major [M][M].
+ *   - Pair state sigma = (a, b) has flat index a*M + b; s+(sigma) = s[a], s-(sigma) = s[b].
+ *   - Every function returns a qp_status; none aborts or throws.  On failure qp_last_error()
+ *     returns a thread-local message naming the violated invariant (e.g. "config: H not
+ *     Hermitian (max |H - H^+| = ...)", "capacity: need 4294967296 B ...").
+ *   - Ownership: the caller owns every host array passed in or out and every device buffer
+ *     (the Python layer allocates them with PyTorch).  The library owns only the opaque plan.
+ *   - Streams are the caller's cudaStream_t passed as void*; all device work is enqueued on it.
+ *     Functions marked [sync] synchronise that stream before returning.
+ *   - Thread-compatible: distinct plans may be used concurrently from different threads.
+ */
+#ifndef QUAPI_H
+#define QUAPI_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } qp_c64;
+
+typedef enum {
+    QP_OK = 0,
+    QP_ERR_ARG = 1,        /* NULL pointer / bad argument to an API call                      */
+    QP_ERR_CONFIG = 2,     /* invalid physics input (Hermiticity, trace, dt, M, L, out_steps)  */
+    QP_ERR_CAPACITY = 3,   /* ARDM + workspace do not fit (message carries the byte count)     */
+    QP_ERR_QUADRATURE = 4, /* eta quadrature did not converge (message names class and lag)    */
+    QP_ERR_CUDA = 6,       /* CUDA runtime error (message carries cudaGetErrorString)          */
+    QP_ERR_COMM = 7        /* reserved for the sharded path                                    */
+} qp_status;
+
+typedef enum {
+    QP_J_ZERO = 0,             /* J = 0 (closed system)                                        */
+    QP_J_OHMIC_EXP = 1,        /* J = (pi/2) xi w exp(-w/wc)                 (reading C.3-9)   */
+    QP_J_DEBYE = 2,            /* J = (pi/2) xi w wc^2/(w^2+wc^2)            (reading C.3-9)   */
+    QP_J_SUPEROHMIC_GAUSS = 3, /* J = A w^3 exp(-(w/wc)^2)   Eq. 21, P:291   (reading C.3-5)   */
+    QP_J_CALLBACK = 4,         /* J(w) from a caller function, integrated on (0, J_cutoff]     */
+    QP_J_G_TABLE = 5           /* bath given directly as G(m dt/2), m = 0..2L+2, where
+                                  G(tau) = int_0^tau int_0^t' alpha(t'-t'') dt'' dt'  -- the
+                                  paper's "or the bath response function alpha(t)"     */
+} qp_bath_kind;
+
+typedef struct {
+    int32_t M;               /* OQS Hilbert-space dimension; 2 <= M <= 4 on the GPU path       */
+    const double *s;         /* [M] coupling-coordinate eigenvalues (basis of H and rho0)      */
+    const qp_c64 *H;         /* [M*M] Hermitian (|H - H^+| <= 1e-12)                           */
+    const qp_c64 *rho0;      /* [M*M] Hermitian, trace 1 (<= 1e-12)                            */
+    int32_t kind;            /* qp_bath_kind                                                    */
+    double coupling;         /* xi (Ohmic, Debye) or A (super-Ohmic Gaussian)                   */
+    double omega_c;          /* cutoff frequency wc > 0 (unused for ZERO / CALLBACK / G_TABLE)  */
+    double kT;               /* k_B T >= 0 (0 => coth = 1)                                       */
+    double (*J)(double w, void *user); /* QP_J_CALLBACK only: J(w) for w > 0; must be thread-safe */
+    void *J_user;            /* passed back to J                                                 */
+    double J_cutoff;         /* QP_J_CALLBACK only: upper integration limit (J ~ 0 beyond)      */
+    const qp_c64 *G_in;      /* QP_J_G_TABLE only: [2*dkmax+3] values G(m dt/2)                 */
+    double dt;               /* time step > 0                                                    */
+    int64_t n_steps;         /* N_t >= 0: last time index; t = n_steps * dt                     */
+    int32_t dkmax;           /* L = Delta k_max >= 1                                             */
+    const int64_t *out_steps;/* sorted unique step indices in [0, n_steps]; NULL => all         */
+    int64_t n_out;           /* length of out_steps (ignored when out_steps == NULL)            */
+    int64_t max_bytes;       /* capacity budget for ARDM + workspace; 0 => no budget check      */
+} qp_problem;
+
+typedef struct qp_plan qp_plan;
+
+typedef struct {
+    int32_t M, N, L;         /* N = M^2                                                          */
+    int64_t ardm_entries;    /* N^L                                                              */
+    int64_t ardm_bytes;      /* 16 N^L: the single in-place ARDM buffer the caller allocates     */
+    int64_t work_bytes;      /* device workspace the caller allocates (tables, partials, rho)    */
+    double pmc_bytes;        /* the paper's PMC = 64 M^(2(L+1)) (Eqs. 18-19) -- reported only  */
+    int64_t n_out;           /* number of rho outputs                                            */
+    int64_t n_steps;
+    int64_t bytes_per_step;  /* algorithmic HBM bytes of one slide step: 2 * 16 * N^L            */
+    int32_t lattice;         /* 1 if s is an arithmetic progression (fewer Delta-s classes)      */
+    int32_t n_classes;       /* D: number of nonzero Delta-s classes used by the kernels         */
+    int32_t grid, block;     /* slide-kernel launch configuration                                */
+    int32_t tile_fibres;     /* fibres per tile                                                  */
+    double setup_seconds;    /* host time spent in qp_plan_create (validation, U, eta, tables)  */
+} qp_sizes;
+
+/* Host only (no GPU needed): validate (a1), U = e^{-iH dt} and the pair propagator K (a2),
+   eta by omega-quadrature (a3), factor tables and launch schedule (a4).  *out owned by caller,
+   free with qp_plan_destroy.  Errors: QP_ERR_ARG, QP_ERR_CONFIG, QP_ERR_QUADRATURE,
+   QP_ERR_CAPACITY (only when max_bytes > 0). */
+qp_status qp_plan_create(const qp_problem *prob, qp_plan **out);
+qp_status qp_plan_query(const qp_plan *plan, qp_sizes *out);
+
+/* eta classes used by the plan (units: the eta of Eqs. 10-16), written as
+   [self_interior (Eq. 11), self_end (Eqs. 13/14), eta_1..eta_L (Eq. 10), E_1..E_L (Eqs. 15/16),
+    TI_1..TI_L (Eq. 12)]  = 3L+2 values.  cap = capacity of out in elements. */
+qp_status qp_plan_eta(const qp_plan *plan, qp_c64 *out, int64_t cap);
+/* U = e^{-iH dt} [M*M] as used by the plan. */
+qp_status qp_plan_propagator(const qp_plan *plan, qp_c64 *U_out);
+
+/* Enqueue: copy the plan's tables into d_work (H2D) and write A_0 into d_ardm.
+   d_ardm: >= ardm_bytes, 16-byte aligned; d_work: >= work_bytes, 256-byte aligned. */
+qp_status qp_init(qp_plan *plan, void *d_ardm, void *d_work, void *stream);
+/* Enqueue time steps k = k_begin .. k_end-1 (1 <= k_begin <= k_end <= n_steps+1): step k turns
+   A_{k-1} into A_k in place (growth for k < L, slide for k >= L) and, when k is an output step,
+   reduces rho(t_k) from A_{k-1} in the same pass (fused readout).  One kernel launch per step.
+   Steps must be enqueued in order after qp_init.  Returns the number of kernels launched in
+   *n_launch (may be NULL). */
+qp_status qp_steps(qp_plan *plan, int64_t k_begin, int64_t k_end, void *d_ardm, void *d_work, void *stream,
+                   int64_t *n_launch);
+/* [sync] Copy every requested rho(t_k) to the host: rho_out[n_out][M][M].  Outputs whose step
+   has not been enqueued yet are undefined. */
+qp_status qp_read_rho(const qp_plan *plan, const void *d_work, qp_c64 *rho_out, void *stream);
+/* [sync] Whole run: qp_init + qp_steps(1, n_steps+1) + qp_read_rho. */
+qp_status qp_run(qp_plan *plan, void *d_ardm, void *d_work, void *stream, qp_c64 *rho_out);
+
+const char *qp_last_error(void);
+void qp_plan_destroy(qp_plan *plan);
+/* Library build identification, e.g. "quapi 0.1 sm_100a". */
+const char *qp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

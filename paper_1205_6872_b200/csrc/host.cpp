@@ -1,0 +1,741 @@
+// host.cpp -- host setup and C ABI of libquapi.so (include/quapi.h).
+//
+// Setup (all on the host, once per plan):
+//   a1 validate     : H, rho0 Hermitian, tr rho0 = 1, dt > 0, 2 <= M <= 4, 2 <= L, out_steps
+//   a2 propagator   : U = exp(-i H dt) by scaling-and-squaring Taylor (no eigensolver);
+//                     K(sig', sig) = U[a',a] conj(U[b',b])  (Eq. 8)
+//   a3 eta          : each eta class of Eqs. 10-16 on the Strang windows (DESIGN §3,
+//                     reading C.3-1) integrated DIRECTLY in omega with its window kernel
+//                       pair  : (1/pi) int J(w) [4 sin(w wa/2) sin(w wb/2)/w^2][coth cos(w dc) - i sin(w dc)]
+//                       self  : (1/pi) int J(w)/w^2 [coth (1 - cos w w0) - i (w w0 - sin w w0)]
+//                     (adaptive Gauss-Kronrod 10/21; Debye: complex partial-fraction asymptotic tail)
+//   a4 tables       : Eq. 9 exponents psi, per-digit-group factor tables, K', beta, offsets
+// The CPU oracle (oracle/) computes the same quantities with different formulations and shares
+// no code with this file.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/quapi.h"
+#include "qp_internal.h"
+
+using cd = std::complex<double>;
+
+namespace {
+
+thread_local std::string g_err;
+
+qp_status err(qp_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define QP_CUDA(call)                                                                           \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess) return err(QP_ERR_CUDA, "cuda: %s at %s:%d", cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+inline double2 d2(cd z) { return make_double2(z.real(), z.imag()); }
+inline int64_t ipow(int64_t b, int e) {
+    int64_t r = 1;
+    while (e-- > 0) r *= b;
+    return r;
+}
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ------------------------------------------------------------------------------------- a2: U
+// exp(X), X = -i H dt, by scaling and squaring with a degree-20 Taylor polynomial.
+std::vector<cd> expm_taylor(const std::vector<cd> &X, int M) {
+    double nrm = 0.0;  // 1-norm
+    for (int j = 0; j < M; ++j) {
+        double c = 0.0;
+        for (int i = 0; i < M; ++i) c += std::abs(X[i * M + j]);
+        nrm = std::max(nrm, c);
+    }
+    int s = 0;
+    while (nrm > 0.125) { nrm *= 0.5; ++s; }
+    const double scale = std::ldexp(1.0, -s);
+    std::vector<cd> Y(M * M), R(M * M, 0.0), T(M * M), tmp(M * M);
+    for (int i = 0; i < M * M; ++i) Y[i] = X[i] * scale;
+    for (int i = 0; i < M; ++i) R[i * M + i] = 1.0;
+    T = R;
+    for (int n = 1; n <= 20; ++n) {  // T = Y^n / n!
+        for (int i = 0; i < M; ++i)
+            for (int j = 0; j < M; ++j) {
+                cd acc = 0.0;
+                for (int k = 0; k < M; ++k) acc += T[i * M + k] * Y[k * M + j];
+                tmp[i * M + j] = acc / double(n);
+            }
+        T = tmp;
+        for (int i = 0; i < M * M; ++i) R[i] += T[i];
+    }
+    for (int q = 0; q < s; ++q) {
+        for (int i = 0; i < M; ++i)
+            for (int j = 0; j < M; ++j) {
+                cd acc = 0.0;
+                for (int k = 0; k < M; ++k) acc += R[i * M + k] * R[k * M + j];
+                tmp[i * M + j] = acc;
+            }
+        R = tmp;
+    }
+    return R;
+}
+
+// ------------------------------------------------------------------------------------- a3: eta
+// QK21 (Gauss-Kronrod 10/21) nodes and weights.
+const double kXgk[11] = {0.995657163025808080735527280689003, 0.973906528517171720077964012084452,
+                         0.930157491355708226001207180059508, 0.865063366688984510732096688423493,
+                         0.780817726586416897063717578345042, 0.679409568299024406234327365114874,
+                         0.562757134668604683339000099272694, 0.433395394129247190799265943165784,
+                         0.294392862701460198131126603103866, 0.148874338981631210884826001129720,
+                         0.000000000000000000000000000000000};
+const double kWgk[11] = {0.011694638867371874278064396062192, 0.032558162307964727478818972459390,
+                         0.054755896574351996031381300244580, 0.075039674810919952767043140916190,
+                         0.093125454583697605535065465083366, 0.109387158802297641899210590325805,
+                         0.123491976262065851077208980725525, 0.134709217311473325928054001771707,
+                         0.142775938577060080797094273138717, 0.147739104901338491374841515972068,
+                         0.149445554002916905664936468389821};
+const double kWg[5] = {0.066671344308688137593568809893332, 0.149451349150580593145776339657697,
+                       0.219086362515982043995534934228163, 0.269266719309996355091226921569469,
+                       0.295524224714752870173892994651338};
+
+struct Bath {
+    int kind;
+    double xi, wc, kT;
+    double (*J)(double, void *);
+    void *user;
+    double cutoff;
+    double spectral(double w) const {
+        switch (kind) {
+        case QP_J_OHMIC_EXP: return 0.5 * M_PI * xi * w * std::exp(-w / wc);
+        case QP_J_DEBYE: return 0.5 * M_PI * xi * w * (wc * wc / (w * w + wc * wc));
+        case QP_J_SUPEROHMIC_GAUSS: { double r = w / wc; return xi * w * w * w * std::exp(-r * r); }
+        case QP_J_CALLBACK: return J(w, user);
+        default: return 0.0;
+        }
+    }
+    double coth_half_beta(double w) const {  // coth(w / 2kT)
+        if (kT <= 0.0) return 1.0;
+        double y = w / (2.0 * kT);
+        if (y > 36.0) return 1.0;
+        double e = std::exp(-2.0 * y);
+        return (1.0 + e) / (1.0 - e);
+    }
+};
+
+// A window class: "self" triangle of width w0, or a disjoint pair (later width wa, earlier wb,
+// centre distance dc).  Units: time (already multiplied by dt).
+struct WinClass {
+    bool self;
+    double w0, wa, wb, dc;
+};
+
+// w - sin(w) for the self kernel: x^3 sum_m (-1)^m x^(2m)/(2m+3)!  (Horner in x^2) below 0.75
+double wms(double x) {
+    if (std::fabs(x) >= 0.75) return x - std::sin(x);
+    static const std::array<double, 13> c = [] {  // 1/(2m+3)!
+        std::array<double, 13> t{};
+        for (int m = 0; m < 13; ++m) {
+            double f = 1.0;
+            for (int q = 2; q <= 2 * m + 3; ++q) f *= q;
+            t[m] = 1.0 / f;
+        }
+        return t;
+    }();
+    const double y = x * x;
+    double t = c[12];
+    for (int m = 11; m >= 0; --m) t = c[m] - y * t;
+    return x * y * t;
+}
+
+cd kernel(const Bath &b, const WinClass &c, double w) {
+    const double j = b.spectral(w) / M_PI;
+    const double ct = b.coth_half_beta(w);
+    if (c.self) {
+        const double h = std::sin(0.5 * w * c.w0);
+        return cd(j * ct * 2.0 * h * h / (w * w), -j * wms(w * c.w0) / (w * w));
+    }
+    const double P = 4.0 * std::sin(0.5 * w * c.wa) * std::sin(0.5 * w * c.wb) / (w * w);
+    return cd(j * P * ct * std::cos(w * c.dc), -j * P * std::sin(w * c.dc));
+}
+
+struct QK {
+    cd val;
+    double err, roundoff;
+};
+
+QK qk21(const Bath &b, const WinClass &c, double lo, double hi) {
+    const double m = 0.5 * (lo + hi), h = 0.5 * (hi - lo);
+    cd f[21];
+    double wk[21];
+    f[0] = kernel(b, c, m);
+    wk[0] = kWgk[10];
+    for (int i = 0; i < 10; ++i) {
+        f[1 + 2 * i] = kernel(b, c, m - h * kXgk[i]);
+        f[2 + 2 * i] = kernel(b, c, m + h * kXgk[i]);
+        wk[1 + 2 * i] = wk[2 + 2 * i] = kWgk[i];
+    }
+    cd K = 0.0, Gs = 0.0;
+    double absr = 0.0, absi = 0.0;
+    for (int q = 0; q < 21; ++q) {
+        K += wk[q] * f[q];
+        absr += wk[q] * std::fabs(f[q].real());
+        absi += wk[q] * std::fabs(f[q].imag());
+    }
+    for (int i = 1; i < 10; i += 2) Gs += kWg[i / 2] * (f[1 + 2 * i] + f[2 + 2 * i]);
+    const cd mean = 0.5 * K;
+    double ascr = 0.0, asci = 0.0;
+    for (int q = 0; q < 21; ++q) {
+        ascr += wk[q] * std::fabs(f[q].real() - mean.real());
+        asci += wk[q] * std::fabs(f[q].imag() - mean.imag());
+    }
+    auto est = [](double d, double asc, double abs_) {
+        double e = std::fabs(d);
+        if (asc != 0.0 && e != 0.0) e = asc * std::min(1.0, std::pow(200.0 * e / asc, 1.5));
+        return std::max(e, 50.0 * 2.2204460492503131e-16 * abs_);
+    };
+    QK r;
+    r.val = K * h;
+    r.err = (est((K - Gs).real() * h, ascr * h, absr * h) + est((K - Gs).imag() * h, asci * h, absi * h));
+    r.roundoff = 100.0 * 2.2204460492503131e-16 * (absr + absi) * h;
+    return r;
+}
+
+// adaptive bisection; accumulates into (s, comp) with compensated summation
+bool adapt(const Bath &b, const WinClass &c, double lo, double hi, double tol, int depth, cd &s, cd &comp) {
+    QK r = qk21(b, c, lo, hi);
+    if (r.err <= tol || r.err <= 1.01 * r.roundoff || depth >= 30) {
+        cd y = r.val - comp;  // Kahan
+        cd t = s + y;
+        comp = (t - s) - y;
+        s = t;
+        return r.err <= tol || r.err <= 1.01 * r.roundoff;
+    }
+    const double mid = 0.5 * (lo + hi);
+    bool ok = adapt(b, c, lo, mid, 0.5 * tol, depth + 1, s, comp);
+    ok &= adapt(b, c, mid, hi, 0.5 * tol, depth + 1, s, comp);
+    return ok;
+}
+
+// Debye tail  int_Om^inf (1/pi) J/w^2 (1 - i w tau - e^{-i w tau}) dw  with coth = 1 (beta Om > 40):
+//   J/(pi w^2) = (xi/2) c^2 / (w (w^2 + c^2)) = (xi/2) [1/w - Re 1/(w - ic)]   (partial fractions)
+//   non-oscillatory part: (xi/2)[ (1/2) log(1 + c^2/Om^2) - i c tau atan(c/Om) ]
+//   oscillatory part: e^{-i Om tau} sum_n g^(n)(Om)/(i tau)^(n+1),  g = 1/w - Re 1/(w - ic).
+cd debye_Gtail(const Bath &b, double tau, double Om) {
+    if (tau == 0.0) return 0.0;
+    const double c = b.wc;
+    const cd non = cd(0.5 * std::log1p((c / Om) * (c / Om)), -c * tau * std::atan(c / Om));
+    cd sum = 0.0, denom = cd(0.0, tau);  // (i tau)^(n+1)
+    const cd z = cd(Om, -c);
+    double fact = 1.0, prev = 1e300;
+    cd zinv = 1.0 / z, zpow = zinv;  // z^-(n+1)
+    double ompow = 1.0 / Om;
+    for (int n = 0; n < 60; ++n) {
+        if (n > 0) { fact *= n; zpow *= zinv; ompow /= Om; }
+        const double gn = ((n % 2) ? -1.0 : 1.0) * fact * (ompow - zpow.real());
+        const cd term = gn / denom;
+        const double mag = std::abs(term);
+        if (mag > prev) break;
+        sum += term;
+        prev = mag;
+        if (mag < 1e-24 * std::abs(sum)) break;
+        denom *= cd(0.0, tau);
+    }
+    const cd osc = std::exp(cd(0.0, -Om * tau)) * sum;
+    return 0.5 * b.xi * (non - osc);
+}
+
+qp_status eta_class(const Bath &b, const WinClass &c, cd *out, const char *name, int lag) {
+    *out = 0.0;
+    if (b.kind == QP_J_ZERO) return QP_OK;
+    double Om;
+    switch (b.kind) {
+    case QP_J_OHMIC_EXP: Om = 64.0 * b.wc; break;
+    case QP_J_SUPEROHMIC_GAUSS: Om = 13.0 * b.wc; break;
+    case QP_J_DEBYE: Om = std::max(256.0 * b.wc, 80.0 * b.kT); break;
+    default: Om = b.cutoff; break;
+    }
+    const double span = c.self ? c.w0 : c.dc + 0.5 * (c.wa + c.wb);
+    double h = 0.25 * (b.kind == QP_J_CALLBACK ? Om / 64.0 : b.wc);
+    h = std::min(h, 0.5 * M_PI / span);
+    const long np = std::max(1L, (long)std::ceil(Om / h));
+    cd s = 0.0, comp = 0.0;
+    bool ok = true;
+    for (long i = 0; i < np; ++i) {
+        const double lo = Om * double(i) / double(np), hi = Om * double(i + 1) / double(np);
+        ok &= adapt(b, c, lo, hi, 1e-17 / double(np), 0, s, comp);
+    }
+    if (b.kind == QP_J_DEBYE) {
+        cd t;
+        if (c.self) {
+            t = debye_Gtail(b, c.w0, Om);
+        } else {  // four corners of the window pair (later [a1,a2], earlier [b1,b2])
+            const double t1 = c.dc + 0.5 * (c.wa + c.wb), t2 = c.dc - 0.5 * (c.wa + c.wb);
+            const double t3 = c.dc - 0.5 * c.wa + 0.5 * c.wb, t4 = c.dc + 0.5 * c.wa - 0.5 * c.wb;
+            t = debye_Gtail(b, t1, Om) + debye_Gtail(b, t2, Om) - debye_Gtail(b, t3, Om) - debye_Gtail(b, t4, Om);
+        }
+        s += t;
+    }
+    *out = s - comp;
+    if (!ok) return err(QP_ERR_QUADRATURE, "quadrature: eta class %s lag %d did not converge", name, lag);
+    return QP_OK;
+}
+
+}  // namespace
+
+// ===================================================================================== plan
+struct qp_plan {
+    int M = 0, N = 0, L = 0, D = 0;
+    bool lattice = false;        // class map used by the kernels
+    double dt = 0.0;
+    int64_t n_steps = 0;
+    std::vector<int64_t> out_steps;
+    std::vector<double> s;
+    std::vector<cd> H, rho0, U, K;     // K[new*N + old]
+    std::vector<double> delta;         // [D]
+    // eta classes (Strang windows): self interior, self end, eta_j, E_j, TI_j (j = 1..L)
+    cd self_int, self_end;
+    std::vector<cd> eta, E, TI;        // index j (0 unused)
+    std::vector<cd> A0;                // [N]
+    // device image
+    std::vector<double2> small;        // SmallLayout
+    int v = 0, T = 1, G = 1, X = 1, n_tiles = 1, block = 256, fib = 1, wgrp = 1;
+    std::vector<double2> Etab;         // [L][2][G][D][X]
+    std::vector<int2> lofs;            // [L][T]
+    std::vector<qp::SlideArgs> sargs;  // per p, pointers filled at init
+    size_t off_small = 0, off_E = 0, off_lofs = 0, off_part = 0, off_rho = 0, off_cnt = 0, work_bytes = 0;
+    int64_t ardm_entries = 0;
+    int grid = 0, sms = 0;
+    int64_t next_k = 1;
+    bool inited = false;
+    double setup_seconds = 0.0;
+    int64_t slot_of(int64_t k) const {
+        auto it = std::lower_bound(out_steps.begin(), out_steps.end(), k);
+        return (it != out_steps.end() && *it == k) ? int64_t(it - out_steps.begin()) : -1;
+    }
+};
+
+namespace {
+
+// psi(sigma'; eta) = -(eta s+(sigma') - conj(eta) s-(sigma'))  -- Eq. 9 summand without Delta s(later)
+cd psi(const qp_plan &P, int sg, cd e) {
+    const double sp = P.s[sg / P.M], sm = P.s[sg % P.M];
+    return -(e * sp - std::conj(e) * sm);
+}
+double dsig(const qp_plan &P, int sg) { return P.s[sg / P.M] - P.s[sg % P.M]; }
+
+void build_classes(qp_plan &P) {
+    const int M = P.M;
+    bool lat = false;
+    if (M > 2) {
+        const double u = P.s[1] - P.s[0];
+        lat = (u != 0.0);
+        for (int a = 0; a < M && lat; ++a)
+            if (std::fabs(P.s[a] - (P.s[0] + a * u)) > 1e-15 * std::max(1.0, std::fabs(P.s[a]))) lat = false;
+    }
+    P.lattice = lat;
+    P.D = qp::n_classes(M, lat);
+    P.delta.assign(P.D, 0.0);
+    for (int a = 0; a < M; ++a)
+        for (int b = 0; b < M; ++b) {
+            const int c = qp::class_of(M, lat, a, b);
+            if (c > 0) P.delta[c - 1] = P.s[a] - P.s[b];  // same value for every (a,b) of a lattice class
+        }
+}
+
+qp_status compute_eta(qp_plan &P, const qp_problem &pr) {
+    const int L = P.L;
+    const double dt = P.dt;
+    P.eta.assign(L + 1, 0.0);
+    P.E.assign(L + 1, 0.0);
+    P.TI.assign(L + 1, 0.0);
+    if (pr.kind == QP_J_G_TABLE) {  // alpha given as G(m dt/2): four-corner rule, G'' = alpha
+        auto G = [&](int m) { return cd(pr.G_in[m].re, pr.G_in[m].im); };  // m = 2 x
+        P.self_int = G(2);
+        P.self_end = G(1);
+        for (int j = 1; j <= L; ++j) {
+            P.eta[j] = G(2 * j + 2) + G(2 * j - 2) - 2.0 * G(2 * j);
+            P.E[j] = G(2 * j + 1) + G(2 * j - 2) - G(2 * j - 1) - G(2 * j);
+            P.TI[j] = G(2 * j) + G(2 * j - 2) - 2.0 * G(2 * j - 1);
+        }
+        return QP_OK;
+    }
+    Bath b{pr.kind, pr.coupling, pr.omega_c, pr.kT, pr.J, pr.J_user, pr.J_cutoff};
+    qp_status st;
+    if ((st = eta_class(b, WinClass{true, dt, 0, 0, 0}, &P.self_int, "self_interior", 0))) return st;
+    if ((st = eta_class(b, WinClass{true, 0.5 * dt, 0, 0, 0}, &P.self_end, "self_end", 0))) return st;
+    for (int j = 1; j <= L; ++j) {
+        if ((st = eta_class(b, WinClass{false, 0, dt, dt, j * dt}, &P.eta[j], "eta", j))) return st;
+        if ((st = eta_class(b, WinClass{false, 0, dt, 0.5 * dt, (j - 0.25) * dt}, &P.E[j], "edge", j))) return st;
+        if ((st = eta_class(b, WinClass{false, 0, 0.5 * dt, 0.5 * dt, (j - 0.5) * dt}, &P.TI[j], "terminal_initial", j)))
+            return st;
+    }
+    return QP_OK;
+}
+
+void build_tables(qp_plan &P) {
+    const int N = P.N, M = P.M, L = P.L, D = P.D;
+    // ---- K and self-factor-weighted K'
+    P.K.assign(N * N, 0.0);
+    for (int a1 = 0; a1 < M; ++a1)
+        for (int b1 = 0; b1 < M; ++b1)
+            for (int a = 0; a < M; ++a)
+                for (int b = 0; b < M; ++b)
+                    P.K[(a1 * M + b1) * N + (a * M + b)] = P.U[a1 * M + a] * std::conj(P.U[b1 * M + b]);
+    const qp::SmallLayout lay{N, D, L};
+    P.small.assign(lay.total(), make_double2(0, 0));
+    const cd selfc[2] = {P.self_int, P.self_end};
+    for (int kap = 0; kap < 2; ++kap)
+        for (int nw = 0; nw < N; ++nw) {
+            const cd c = std::exp(dsig(P, nw) * psi(P, nw, selfc[kap]));  // I(new,new; eta_self)
+            for (int last = 0; last < N; ++last) P.small[lay.kp(kap) + nw * N + last] = d2(c * P.K[nw * N + last]);
+        }
+    // ---- beta_d(old) = exp(delta_d psi_L(old)) : variant 0 (k > L), 1 (k == L, partner sigma_0)
+    const cd lagL[2][2] = {{P.eta[L], P.E[L]}, {P.E[L], P.TI[L]}};
+    for (int var = 0; var < 2; ++var)
+        for (int kap = 0; kap < 2; ++kap)
+            for (int d = 0; d < D; ++d)
+                for (int old = 0; old < N; ++old)
+                    P.small[lay.beta(var, kap) + d * N + old] = d2(std::exp(P.delta[d] * psi(P, old, lagL[var][kap])));
+    // ---- growth exponent rows psi_{k,j}(sigma), k = 1..L-1, j = 1..k
+    for (int k = 1; k < L; ++k)
+        for (int j = 1; j <= k; ++j) {
+            const cd ep = (j < k) ? P.eta[j] : P.E[k];
+            const cd et = (j < k) ? P.E[j] : P.TI[k];
+            for (int sg = 0; sg < N; ++sg) {
+                P.small[lay.psi(0) + ((size_t)k * L + j) * N + sg] = d2(psi(P, sg, ep));
+                P.small[lay.psi(1) + ((size_t)k * L + j) * N + sg] = d2(psi(P, sg, et));
+            }
+        }
+    // ---- slide tiles and digit-group factor tables
+    int block, F, v, w;
+    qp::slide_shape(M, &block, &F, &v, &w);
+    const int nmid = L - 1;
+    P.v = std::min(v, nmid);
+    P.T = (int)ipow(N, P.v);
+    P.n_tiles = (int)ipow(N, nmid - P.v);
+    P.block = block;
+    P.fib = F;
+    P.wgrp = w;
+    const int hi = nmid - P.v;
+    P.G = 1 + (hi + w - 1) / w;
+    P.X = P.T;
+    for (int g = 1; g < P.G; ++g) P.X = std::max<int>(P.X, (int)ipow(N, std::min(w, hi - (g - 1) * w)));
+    P.Etab.assign((size_t)L * 2 * P.G * D * P.X, make_double2(1.0, 0.0));
+    P.lofs.assign((size_t)L * P.T, make_int2(0, -1));
+    P.sargs.assign(L, qp::SlideArgs{});
+    for (int p = 0; p < L; ++p) {
+        auto pos_of = [&](int i) { return i < p ? i : i + 1; };  // mid digit i -> ARDM digit
+        auto lag_of = [&](int i) { return ((p - pos_of(i)) % L + L) % L; };
+        // group tables
+        for (int g = 0; g < P.G; ++g) {
+            const int i0 = (g == 0) ? 0 : P.v + (g - 1) * w;
+            const int nd = (g == 0) ? P.v : std::min(w, hi - (g - 1) * w);
+            const int cnt = (int)ipow(N, nd);
+            for (int x = 0; x < cnt; ++x) {
+                cd Ps[2] = {0.0, 0.0};
+                int r = x;
+                for (int t = 0; t < nd; ++t) {
+                    const int dig = r % N;
+                    r /= N;
+                    const int lag = lag_of(i0 + t);
+                    Ps[0] += psi(P, dig, P.eta[lag]);
+                    Ps[1] += psi(P, dig, P.E[lag]);
+                }
+                for (int kap = 0; kap < 2; ++kap)
+                    for (int d = 0; d < D; ++d)
+                        P.Etab[((((size_t)p * 2 + kap) * P.G + g) * D + d) * P.X + x] = d2(std::exp(P.delta[d] * Ps[kap]));
+            }
+        }
+        // in-tile offsets and lo 'last' digit
+        const int qlast = (p - 1 + L) % L;
+        const int ilast = qlast < p ? qlast : qlast - 1;
+        for (int fl = 0; fl < P.T; ++fl) {
+            int64_t off;
+            if (p >= P.v) off = fl;
+            else off = (fl % ipow(N, p)) + (fl / ipow(N, p)) * ipow(N, p + 1);
+            int lastd = -1;
+            if (ilast < P.v) lastd = (int)((fl / ipow(N, ilast)) % N);
+            P.lofs[(size_t)p * P.T + fl] = make_int2((int)off, lastd);
+        }
+        qp::SlideArgs &a = P.sargs[p];
+        a.pw_p = ipow(N, p);
+        a.pw_p1 = ipow(N, p + 1);
+        a.tile_stride = ipow(N, P.v + 1);
+        a.n_tiles = P.n_tiles;
+        a.T = P.T;
+        a.p_ge_v = p >= P.v;
+        a.Qlo = p >= P.v ? (int)ipow(N, p - P.v) : 1;
+        a.G = P.G;
+        a.X = P.X;
+        for (int g = 1; g < P.G; ++g) {
+            a.gdiv[g] = (int)ipow(N, (g - 1) * w);
+            a.gmod[g] = (int)ipow(N, std::min(w, hi - (g - 1) * w));
+        }
+        a.last_div = ilast >= P.v ? (int)ipow(N, ilast - P.v) : -1;
+    }
+    // ---- A_0(sigma_0) = rho0(sigma_0) I(sigma_0, sigma_0; eta_00 = G(1/2))   (Eq. 13, reading C.3-2)
+    P.A0.assign(N, 0.0);
+    for (int sg = 0; sg < N; ++sg) P.A0[sg] = P.rho0[sg] * std::exp(dsig(P, sg) * psi(P, sg, P.self_end));
+    // ---- workspace layout
+    size_t off = 0;
+    P.off_small = off; off = align256(off + P.small.size() * sizeof(double2));
+    P.off_E = off;     off = align256(off + P.Etab.size() * sizeof(double2));
+    P.off_lofs = off;  off = align256(off + P.lofs.size() * sizeof(int2));
+    P.off_part = off;  off = align256(off + (size_t)qp::kPartialsMax * N * sizeof(double2));
+    P.off_rho = off;   off = align256(off + std::max<size_t>(1, P.out_steps.size()) * N * sizeof(double2));
+    P.off_cnt = off;   off = align256(off + 256);
+    P.work_bytes = off;
+}
+
+qp_status validate(const qp_problem *pr) {
+    if (!pr) return err(QP_ERR_ARG, "arg: problem is NULL");
+    const int M = pr->M;
+    if (M < 2 || M > qp::kMaxM) return err(QP_ERR_CONFIG, "config: GPU path supports 2 <= M <= %d (got %d)", qp::kMaxM, M);
+    if (!pr->s || !pr->H || !pr->rho0) return err(QP_ERR_ARG, "arg: s, H and rho0 are required");
+    if (pr->dkmax < 2 || pr->dkmax > qp::kMaxL) return err(QP_ERR_CONFIG, "config: dkmax must be in [2, %d] (got %d)", qp::kMaxL, pr->dkmax);
+    if (!(pr->dt > 0.0) || !std::isfinite(pr->dt)) return err(QP_ERR_CONFIG, "config: dt must be finite and > 0");
+    if (pr->n_steps < 0) return err(QP_ERR_CONFIG, "config: n_steps must be >= 0");
+    double hmax = 0.0, rmax = 0.0;
+    cd tr = 0.0;
+    for (int i = 0; i < M; ++i) {
+        if (!std::isfinite(pr->s[i])) return err(QP_ERR_CONFIG, "config: s[%d] not finite", i);
+        for (int j = 0; j < M; ++j) {
+            const cd h = {pr->H[i * M + j].re, pr->H[i * M + j].im}, hT = {pr->H[j * M + i].re, pr->H[j * M + i].im};
+            const cd r = {pr->rho0[i * M + j].re, pr->rho0[i * M + j].im}, rT = {pr->rho0[j * M + i].re, pr->rho0[j * M + i].im};
+            hmax = std::max(hmax, std::abs(h - std::conj(hT)));
+            rmax = std::max(rmax, std::abs(r - std::conj(rT)));
+        }
+        tr += cd(pr->rho0[i * M + i].re, pr->rho0[i * M + i].im);
+    }
+    if (!(hmax <= 1e-12)) return err(QP_ERR_CONFIG, "config: H not Hermitian (max |H - H^+| = %.3g)", hmax);
+    if (!(rmax <= 1e-12)) return err(QP_ERR_CONFIG, "config: rho0 not Hermitian (max |rho0 - rho0^+| = %.3g)", rmax);
+    if (!(std::abs(tr - 1.0) <= 1e-12)) return err(QP_ERR_CONFIG, "config: trace(rho0) = %.17g%+.3gi, must be 1", tr.real(), tr.imag());
+    switch (pr->kind) {
+    case QP_J_ZERO: break;
+    case QP_J_OHMIC_EXP: case QP_J_DEBYE: case QP_J_SUPEROHMIC_GAUSS:
+        if (!(pr->omega_c > 0.0)) return err(QP_ERR_CONFIG, "config: omega_c must be > 0");
+        if (!(pr->kT >= 0.0)) return err(QP_ERR_CONFIG, "config: kT must be >= 0");
+        break;
+    case QP_J_CALLBACK:
+        if (!pr->J || !(pr->J_cutoff > 0.0)) return err(QP_ERR_CONFIG, "config: callback bath needs J and J_cutoff > 0");
+        if (!(pr->kT >= 0.0)) return err(QP_ERR_CONFIG, "config: kT must be >= 0");
+        break;
+    case QP_J_G_TABLE:
+        if (!pr->G_in) return err(QP_ERR_CONFIG, "config: G_TABLE bath needs G_in[2*dkmax+3]");
+        break;
+    default: return err(QP_ERR_CONFIG, "config: unknown bath kind %d", pr->kind);
+    }
+    if (pr->out_steps) {
+        for (int64_t o = 0; o < pr->n_out; ++o) {
+            const int64_t k = pr->out_steps[o];
+            if (k < 0 || k > pr->n_steps || (o > 0 && k <= pr->out_steps[o - 1]))
+                return err(QP_ERR_CONFIG, "config: out_steps must be sorted, unique and within [0, n_steps]");
+        }
+    }
+    // N^L must fit comfortably in int64 and the 32-bit tile indices
+    const double ent = std::pow(double(M * M), double(pr->dkmax));
+    if (ent > 4.0e12) return err(QP_ERR_CAPACITY, "capacity: need %.4g B for the ARDM (N^L = %.4g entries)", 16.0 * ent, ent);
+    return QP_OK;
+}
+
+}  // namespace
+
+// ===================================================================================== C ABI
+extern "C" {
+
+const char *qp_last_error(void) { return g_err.c_str(); }
+const char *qp_version(void) { return "quapi 0.1 sm_100a"; }
+
+qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
+    if (!out) return err(QP_ERR_ARG, "arg: out is NULL");
+    *out = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    qp_status st = validate(pr);
+    if (st) return st;
+    qp_plan *P = new (std::nothrow) qp_plan();
+    if (!P) return err(QP_ERR_CAPACITY, "capacity: host allocation failed");
+    P->M = pr->M;
+    P->N = pr->M * pr->M;
+    P->L = pr->dkmax;
+    P->dt = pr->dt;
+    P->n_steps = pr->n_steps;
+    if (pr->out_steps) P->out_steps.assign(pr->out_steps, pr->out_steps + pr->n_out);
+    else for (int64_t k = 0; k <= pr->n_steps; ++k) P->out_steps.push_back(k);
+    P->s.assign(pr->s, pr->s + P->M);
+    P->H.resize(P->M * P->M);
+    P->rho0.resize(P->M * P->M);
+    for (int i = 0; i < P->M * P->M; ++i) {
+        P->H[i] = cd(pr->H[i].re, pr->H[i].im);
+        P->rho0[i] = cd(pr->rho0[i].re, pr->rho0[i].im);
+    }
+    std::vector<cd> X(P->M * P->M);
+    for (int i = 0; i < P->M * P->M; ++i) X[i] = cd(0.0, -P->dt) * P->H[i];
+    P->U = expm_taylor(X, P->M);
+    build_classes(*P);
+    if ((st = compute_eta(*P, *pr))) { delete P; return st; }
+    build_tables(*P);
+    P->ardm_entries = ipow(P->N, P->L);
+    const double need = 16.0 * double(P->ardm_entries) + double(P->work_bytes);
+    if (pr->max_bytes > 0 && need > double(pr->max_bytes)) {
+        delete P;
+        return err(QP_ERR_CAPACITY, "capacity: need %.0f B (ARDM %.0f B + workspace) > budget %lld B", need,
+                   16.0 * std::pow(double(pr->M * pr->M), pr->dkmax), (long long)pr->max_bytes);
+    }
+    P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = P;
+    return QP_OK;
+}
+
+void qp_plan_destroy(qp_plan *P) { delete P; }
+
+qp_status qp_plan_query(const qp_plan *P, qp_sizes *o) {
+    if (!P || !o) return err(QP_ERR_ARG, "arg: NULL plan or out");
+    o->M = P->M; o->N = P->N; o->L = P->L;
+    o->ardm_entries = P->ardm_entries;
+    o->ardm_bytes = 16 * P->ardm_entries;
+    o->work_bytes = (int64_t)P->work_bytes;
+    o->pmc_bytes = 64.0 * std::pow(double(P->M), 2.0 * (P->L + 1));
+    o->n_out = (int64_t)P->out_steps.size();
+    o->n_steps = P->n_steps;
+    o->bytes_per_step = 32 * P->ardm_entries;
+    o->lattice = P->lattice;
+    o->n_classes = P->D;
+    o->grid = P->grid;
+    o->block = P->block;
+    o->tile_fibres = P->T;
+    o->setup_seconds = P->setup_seconds;
+    return QP_OK;
+}
+
+qp_status qp_plan_eta(const qp_plan *P, qp_c64 *out, int64_t cap) {
+    if (!P || !out) return err(QP_ERR_ARG, "arg: NULL plan or out");
+    if (cap < 3 * P->L + 2) return err(QP_ERR_ARG, "arg: eta output needs %d entries", 3 * P->L + 2);
+    auto put = [&](int i, cd z) { out[i].re = z.real(); out[i].im = z.imag(); };
+    put(0, P->self_int);
+    put(1, P->self_end);
+    for (int j = 1; j <= P->L; ++j) {
+        put(1 + j, P->eta[j]);
+        put(1 + P->L + j, P->E[j]);
+        put(1 + 2 * P->L + j, P->TI[j]);
+    }
+    return QP_OK;
+}
+
+qp_status qp_plan_propagator(const qp_plan *P, qp_c64 *U) {
+    if (!P || !U) return err(QP_ERR_ARG, "arg: NULL plan or out");
+    for (int i = 0; i < P->M * P->M; ++i) { U[i].re = P->U[i].real(); U[i].im = P->U[i].imag(); }
+    return QP_OK;
+}
+
+qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
+    if (!P || !d_ardm || !d_work) return err(QP_ERR_ARG, "arg: NULL plan or device buffer");
+    if ((uintptr_t)d_ardm % 16 || (uintptr_t)d_work % 256) return err(QP_ERR_ARG, "arg: misaligned device buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    QP_CUDA(cudaGetDevice(&dev));
+    QP_CUDA(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
+    char *w = (char *)d_work;
+    QP_CUDA(cudaMemcpyAsync(w + P->off_small, P->small.data(), P->small.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+    QP_CUDA(cudaMemcpyAsync(w + P->off_E, P->Etab.data(), P->Etab.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+    QP_CUDA(cudaMemcpyAsync(w + P->off_lofs, P->lofs.data(), P->lofs.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    QP_CUDA(cudaMemsetAsync(w + P->off_cnt, 0, 256, s));
+    std::vector<double2> a0(P->N);
+    for (int i = 0; i < P->N; ++i) a0[i] = d2(P->A0[i]);
+    QP_CUDA(cudaMemcpyAsync(d_ardm, a0.data(), P->N * sizeof(double2), cudaMemcpyHostToDevice, s));
+    const int64_t slot0 = P->slot_of(0);
+    if (slot0 >= 0) {  // rho(t_0) = rho0 exactly (reading C.3-8)
+        std::vector<double2> r0(P->N);
+        for (int i = 0; i < P->N; ++i) r0[i] = d2(P->rho0[i]);
+        QP_CUDA(cudaMemcpyAsync(w + P->off_rho + slot0 * P->N * sizeof(double2), r0.data(), P->N * sizeof(double2),
+                                cudaMemcpyHostToDevice, s));
+    }
+    // the host vectors above are pageable: cudaMemcpyAsync from pageable memory returns after the
+    // source has been staged, so they may go out of scope.
+    // persistent slide grid: fixed per (plan, device type) => deterministic readout order
+    const int occ = 2;  // design point: 2 resident CTAs per SM (register budget)
+    P->grid = std::max(1, std::min<int>({P->n_tiles, P->sms * occ, qp::kPartialsMax}));
+    P->next_k = 1;
+    P->inited = true;
+    return QP_OK;
+}
+
+qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, void *d_work, void *stream,
+                   int64_t *n_launch) {
+    if (n_launch) *n_launch = 0;
+    if (!P || !d_ardm || !d_work) return err(QP_ERR_ARG, "arg: NULL plan or device buffer");
+    if (!P->inited) return err(QP_ERR_ARG, "arg: qp_init must be called before qp_steps");
+    if (k_begin != P->next_k || k_end < k_begin || k_end > P->n_steps + 1)
+        return err(QP_ERR_ARG, "arg: steps must be enqueued in order: expected k_begin = %lld, k_end <= %lld",
+                   (long long)P->next_k, (long long)P->n_steps + 1);
+    cudaStream_t s = (cudaStream_t)stream;
+    char *w = (char *)d_work;
+    double2 *A = (double2 *)d_ardm;
+    const double2 *small = (const double2 *)(w + P->off_small);
+    double2 *part = (double2 *)(w + P->off_part);
+    unsigned *cnt = (unsigned *)(w + P->off_cnt);
+    int64_t launched = 0;
+    for (int64_t k = k_begin; k < k_end; ++k) {
+        const int64_t slot = P->slot_of(k);
+        double2 *rho = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * P->N : nullptr;
+        cudaError_t e;
+        if (k < P->L) {
+            qp::GrowArgs g{};
+            g.A = A; g.small = small; g.partials = part; g.rho = rho; g.counter = cnt;
+            g.n_in = ipow(P->N, (int)k);
+            g.k = (int)k;
+            g.L = P->L;
+            for (int d = 0; d < P->D; ++d) g.delta[d] = P->delta[d];
+            const int grid = (int)std::min<int64_t>({(g.n_in + 255) / 256, (int64_t)P->sms * 8, (int64_t)qp::kPartialsMax});
+            e = qp::launch_grow(P->M, P->lattice, g, std::max(1, grid), s);
+        } else {
+            const int p = (int)(k % P->L);
+            qp::SlideArgs a = P->sargs[p];
+            a.A = A; a.small = small;
+            a.Etab = (const double2 *)(w + P->off_E) + (size_t)p * 2 * P->G * P->D * P->X;
+            a.lofs = (const int2 *)(w + P->off_lofs) + (size_t)p * P->T;
+            a.partials = part; a.rho = rho; a.counter = cnt;
+            a.variant = (k == P->L) ? 1 : 0;
+            e = qp::launch_slide(P->M, P->lattice, a, P->grid, s);
+        }
+        if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
+        ++launched;
+        P->next_k = k + 1;
+    }
+    if (n_launch) *n_launch = launched;
+    return QP_OK;
+}
+
+qp_status qp_read_rho(const qp_plan *P, const void *d_work, qp_c64 *rho_out, void *stream) {
+    if (!P || !d_work || !rho_out) return err(QP_ERR_ARG, "arg: NULL plan, workspace or output");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n = P->out_steps.size() * P->N;
+    if (n == 0) return QP_OK;
+    QP_CUDA(cudaMemcpyAsync(rho_out, (const char *)d_work + P->off_rho, n * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    QP_CUDA(cudaStreamSynchronize(s));
+    return QP_OK;
+}
+
+qp_status qp_run(qp_plan *P, void *d_ardm, void *d_work, void *stream, qp_c64 *rho_out) {
+    qp_status st;
+    if ((st = qp_init(P, d_ardm, d_work, stream))) return st;
+    if ((st = qp_steps(P, 1, P->n_steps + 1, d_ardm, d_work, stream, nullptr))) return st;
+    return qp_read_rho(P, d_work, rho_out, stream);
+}
+
+}  // extern "C"

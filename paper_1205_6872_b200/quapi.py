@@ -1,0 +1,264 @@
+"""Thin Python binding of libquapi.so (include/quapi.h): argument marshalling only.
+
+Every step of the hot path runs inside the library's CUDA kernels; this module only
+builds the ``qp_problem`` struct, allocates the caller-owned device buffers with PyTorch
+(device memory and streams are the only things PyTorch is used for) and forwards calls.
+There is no CPU fallback: if ``libquapi.so`` is missing or no CUDA device is present the
+GPU entry points raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import workloads as W
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "lib", "libquapi.so")
+
+QP_OK, QP_ERR_ARG, QP_ERR_CONFIG, QP_ERR_CAPACITY, QP_ERR_QUADRATURE, QP_ERR_CUDA, QP_ERR_COMM = 0, 1, 2, 3, 4, 6, 7
+QP_J_CALLBACK, QP_J_G_TABLE = 4, 5
+
+_JFUNC = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
+
+
+class qp_c64(ctypes.Structure):
+    _fields_ = [("re", ctypes.c_double), ("im", ctypes.c_double)]
+
+
+class qp_problem(ctypes.Structure):
+    _fields_ = [
+        ("M", ctypes.c_int32),
+        ("s", ctypes.POINTER(ctypes.c_double)),
+        ("H", ctypes.POINTER(qp_c64)),
+        ("rho0", ctypes.POINTER(qp_c64)),
+        ("kind", ctypes.c_int32),
+        ("coupling", ctypes.c_double),
+        ("omega_c", ctypes.c_double),
+        ("kT", ctypes.c_double),
+        ("J", _JFUNC),
+        ("J_user", ctypes.c_void_p),
+        ("J_cutoff", ctypes.c_double),
+        ("G_in", ctypes.POINTER(qp_c64)),
+        ("dt", ctypes.c_double),
+        ("n_steps", ctypes.c_int64),
+        ("dkmax", ctypes.c_int32),
+        ("out_steps", ctypes.POINTER(ctypes.c_int64)),
+        ("n_out", ctypes.c_int64),
+        ("max_bytes", ctypes.c_int64),
+    ]
+
+
+class qp_sizes(ctypes.Structure):
+    _fields_ = [
+        ("M", ctypes.c_int32), ("N", ctypes.c_int32), ("L", ctypes.c_int32),
+        ("ardm_entries", ctypes.c_int64), ("ardm_bytes", ctypes.c_int64), ("work_bytes", ctypes.c_int64),
+        ("pmc_bytes", ctypes.c_double), ("n_out", ctypes.c_int64), ("n_steps", ctypes.c_int64),
+        ("bytes_per_step", ctypes.c_int64), ("lattice", ctypes.c_int32), ("n_classes", ctypes.c_int32),
+        ("grid", ctypes.c_int32), ("block", ctypes.c_int32), ("tile_fibres", ctypes.c_int32),
+        ("setup_seconds", ctypes.c_double),
+    ]
+
+
+# Every symbol include/quapi.h declares (tests check the library exports all of them).
+EXPORTS = ("qp_plan_create", "qp_plan_query", "qp_plan_eta", "qp_plan_propagator", "qp_init", "qp_steps",
+           "qp_read_rho", "qp_run", "qp_last_error", "qp_plan_destroy", "qp_version")
+
+_lib = None
+
+
+class QuapiError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[qp_status {status}] {msg}")
+        self.status = status
+
+
+def lib() -> ctypes.CDLL:
+    """Load libquapi.so (built in-tree by paper_1205_6872_b200/build.py).  Fails loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise RuntimeError(f"libquapi.so not built ({SO_PATH}); run `python -m paper_1205_6872_b200.build` "
+                               "or __graft_entry__.build() -- there is no CPU fallback")
+        L = ctypes.CDLL(SO_PATH)
+        PP = ctypes.POINTER(ctypes.c_void_p)
+        L.qp_plan_create.argtypes = [ctypes.POINTER(qp_problem), PP]
+        L.qp_plan_query.argtypes = [ctypes.c_void_p, ctypes.POINTER(qp_sizes)]
+        L.qp_plan_eta.argtypes = [ctypes.c_void_p, ctypes.POINTER(qp_c64), ctypes.c_int64]
+        L.qp_plan_propagator.argtypes = [ctypes.c_void_p, ctypes.POINTER(qp_c64)]
+        L.qp_init.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.qp_steps.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
+        L.qp_read_rho.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(qp_c64), ctypes.c_void_p]
+        L.qp_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(qp_c64)]
+        L.qp_last_error.restype = ctypes.c_char_p
+        L.qp_version.restype = ctypes.c_char_p
+        L.qp_plan_destroy.argtypes = [ctypes.c_void_p]
+        L.qp_plan_destroy.restype = None
+        for f in ("qp_plan_create", "qp_plan_query", "qp_plan_eta", "qp_plan_propagator", "qp_init", "qp_steps",
+                  "qp_read_rho", "qp_run"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != QP_OK:
+        raise QuapiError(st, lib().qp_last_error().decode())
+
+
+def _c64_array(a) -> ctypes.Array:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.complex128).ravel())
+    arr = (qp_c64 * len(a))()
+    ctypes.memmove(arr, a.ctypes.data, a.nbytes)
+    return arr
+
+
+def _to_numpy(arr, shape) -> np.ndarray:
+    out = np.empty(int(np.prod(shape)), dtype=np.complex128)
+    ctypes.memmove(out.ctypes.data, arr, out.nbytes)
+    return out.reshape(shape)
+
+
+@dataclass
+class Sizes:
+    M: int
+    N: int
+    L: int
+    ardm_entries: int
+    ardm_bytes: int
+    work_bytes: int
+    pmc_bytes: float
+    n_out: int
+    n_steps: int
+    bytes_per_step: int
+    lattice: int
+    n_classes: int
+    grid: int
+    block: int
+    tile_fibres: int
+    setup_seconds: float
+
+
+class Plan:
+    """An opaque ``qp_plan`` (host setup done at construction: validation, U, eta, tables)."""
+
+    def __init__(self, w: W.Workload, out_steps: Optional[Sequence[int]] = None,
+                 J: Optional[Callable[[float], float]] = None, J_cutoff: float = 0.0,
+                 G_in: Optional[np.ndarray] = None, max_bytes: int = 0):
+        L = lib()
+        self.w = w
+        self._keep = []
+        s = np.ascontiguousarray(w.s, dtype=np.float64)
+        H, rho0 = _c64_array(w.H), _c64_array(w.rho0)
+        self._keep += [s, H, rho0]
+        pr = qp_problem()
+        pr.M = w.M
+        pr.s = s.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        pr.H, pr.rho0 = H, rho0
+        pr.kind = int(w.kind)
+        pr.coupling, pr.omega_c, pr.kT = float(w.coupling), float(w.omega_c), float(w.kT)
+        if J is not None:
+            cb = _JFUNC(lambda x, _u: float(J(x)))
+            self._keep.append(cb)
+            pr.kind, pr.J, pr.J_cutoff = QP_J_CALLBACK, cb, float(J_cutoff)
+        if G_in is not None:
+            g = _c64_array(G_in)
+            self._keep.append(g)
+            pr.kind, pr.G_in = QP_J_G_TABLE, g
+        pr.dt, pr.n_steps, pr.dkmax = float(w.dt), int(w.n_steps), int(w.L)
+        if out_steps is not None:
+            o = np.ascontiguousarray(np.asarray(out_steps, dtype=np.int64))
+            self._keep.append(o)
+            pr.out_steps = o.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+            pr.n_out = len(o)
+        pr.max_bytes = int(max_bytes)
+        h = ctypes.c_void_p()
+        _check(L.qp_plan_create(ctypes.byref(pr), ctypes.byref(h)))
+        self._h = h
+        self.out_steps = (np.arange(w.n_steps + 1) if out_steps is None else np.asarray(out_steps, dtype=np.int64))
+        self.launches = 0
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.qp_plan_destroy(h)
+            self._h = None
+
+    @property
+    def sizes(self) -> Sizes:
+        o = qp_sizes()
+        _check(lib().qp_plan_query(self._h, ctypes.byref(o)))
+        return Sizes(*(getattr(o, f) for f, _ in qp_sizes._fields_))
+
+    def eta(self) -> dict:
+        Lm = self.w.L
+        buf = (qp_c64 * (3 * Lm + 2))()
+        _check(lib().qp_plan_eta(self._h, buf, len(buf)))
+        v = _to_numpy(buf, (3 * Lm + 2,))
+        return {"self_interior": v[0], "self_end": v[1], "eta": v[2:2 + Lm], "E": v[2 + Lm:2 + 2 * Lm],
+                "TI": v[2 + 2 * Lm:2 + 3 * Lm]}
+
+    def propagator(self) -> np.ndarray:
+        buf = (qp_c64 * (self.w.M ** 2))()
+        _check(lib().qp_plan_propagator(self._h, buf))
+        return _to_numpy(buf, (self.w.M, self.w.M))
+
+    # ---- device-side calls (PyTorch tensors own the memory; the caller's stream is passed through)
+    def alloc(self, device="cuda"):
+        import torch
+        sz = self.sizes
+        ardm = torch.empty(sz.ardm_entries * 2, dtype=torch.float64, device=device)
+        work = torch.empty((sz.work_bytes + 7) // 8, dtype=torch.float64, device=device)
+        return ardm, work
+
+    @staticmethod
+    def _stream_ptr(stream) -> int:
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        return int(s.cuda_stream)
+
+    def init(self, ardm, work, stream=None):
+        _check(lib().qp_init(self._h, ctypes.c_void_p(ardm.data_ptr()), ctypes.c_void_p(work.data_ptr()),
+                             ctypes.c_void_p(self._stream_ptr(stream))))
+
+    def steps(self, k_begin: int, k_end: int, ardm, work, stream=None) -> int:
+        n = ctypes.c_int64(0)
+        _check(lib().qp_steps(self._h, int(k_begin), int(k_end), ctypes.c_void_p(ardm.data_ptr()),
+                              ctypes.c_void_p(work.data_ptr()), ctypes.c_void_p(self._stream_ptr(stream)),
+                              ctypes.byref(n)))
+        self.launches += n.value
+        return n.value
+
+    def read_rho(self, work, stream=None) -> np.ndarray:
+        n = len(self.out_steps)
+        buf = (qp_c64 * max(1, n * self.w.N))()
+        _check(lib().qp_read_rho(self._h, ctypes.c_void_p(work.data_ptr()), buf,
+                                 ctypes.c_void_p(self._stream_ptr(stream))))
+        return _to_numpy(buf, (n, self.w.M, self.w.M))[:n]
+
+    def run(self, ardm, work, stream=None) -> np.ndarray:
+        n = len(self.out_steps)
+        buf = (qp_c64 * max(1, n * self.w.N))()
+        _check(lib().qp_run(self._h, ctypes.c_void_p(ardm.data_ptr()), ctypes.c_void_p(work.data_ptr()),
+                            ctypes.c_void_p(self._stream_ptr(stream)), buf))
+        self.launches += self.w.n_steps
+        return _to_numpy(buf, (n, self.w.M, self.w.M))[:n]
+
+
+def solve(w: W.Workload, out_steps: Optional[Sequence[int]] = None, device: str = "cuda", **kw) -> np.ndarray:
+    """Public one-call API: rho(t_k) [n_out, M, M] for the workload (host in, host out)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("quapi.solve needs a CUDA device (no CPU fallback)")
+    plan = Plan(w, out_steps=out_steps, **kw)
+    ardm, work = plan.alloc(device)
+    return plan.run(ardm, work)
+
+
+def version() -> str:
+    return lib().qp_version().decode()
