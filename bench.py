@@ -1,0 +1,256 @@
+#!/usr/bin/env python
+"""bench.py -- QUAPI tensor-propagator step on B200 (BASELINE.json metric, config 3 at N=1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--cfg 3]
+
+A "step" is one QUAPI time step k >= L of the BASELINE workload (config 3: spin-boson M=2,
+Debye bath, Delta k_max = 14, ARDM of 4^14 complex FP64 entries = 4.3 GB, larger than L2):
+the in-place slide of the ARDM with the rho(t_k) readout fused (allPoints mode).  Our arm
+times K such steps after W warm-up steps with CUDA events on the launching stream (barrier +
+synchronize on both sides, max over ranks).  N > 1: independent replicas, one per GPU (weak
+scaling; the sharded config-5 path is DESIGN.md's next step).
+
+--impl reference: the CPU oracle (oracle/liboracle.so) on the host cores, same config/metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QUAPI steps/s & achieved HBM GB/s, spin-boson Δkmax=14 FP64, 1/2/4/8 B200"
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _ncu_traffic():
+    """Per-launch DRAM bytes of the slide kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_slide_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = []
+        for ln in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_baseline(cfg: int, max_slide: int = 3):
+    """The oracle as it stands on the host cores, on a bounded sample of the workload:
+    init + growth + `max_slide` slide steps with readout; value = slide steps / slide seconds."""
+    import numpy as np
+
+    import oracle as O
+    from paper_1205_6872_b200 import workloads as W
+    w = W.CONFIGS[cfg]
+    n = w.L + max_slide - 1
+    p = O.Problem(s=w.s, H=w.H, rho0=w.rho0, kind=w.kind, coupling=w.coupling, omega_c=w.omega_c,
+                  kT=w.kT, dt=w.dt, n_steps=n, L=w.L)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    _, tm = O.run(p, out_steps=np.arange(n + 1), nthreads=cores, timings=True)
+    wall = time.perf_counter() - t0
+    v = tm["n_slide"] / tm["slide_s"] if tm["slide_s"] > 0 else None
+    return {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
+            "sample": (f"{w.name}: init + {w.L - 1} growth + {tm['n_slide']} slide steps with readout "
+                       f"(allPoints), {cores} OpenMP threads; slide {tm['slide_s']:.2f} s of {wall:.1f} s wall")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cb = cpu_baseline(args.cfg, max_slide=max(1, min(args.steps, 3)))
+    from paper_1205_6872_b200 import workloads as W
+    w = W.CONFIGS[args.cfg]
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / cb["value"] if cb["value"] else None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "ardm_entries": w.ardm_entries},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cfg", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1205_6872_b200 import build as B
+    from paper_1205_6872_b200 import quapi as Q
+    from paper_1205_6872_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    B.build()
+
+    base = W.CONFIGS[args.cfg]
+    K, Wm, L = args.steps, max(args.warmup, 3), base.L
+    n_total = L - 1 + Wm + K  # growth steps, then W warm-up and K timed slide steps
+    w = base.with_(n_steps=n_total)
+    plan = Q.Plan(w)  # allPoints readout: every step reduces rho(t_k)
+    sz = plan.sizes
+    ardm, work = plan.alloc()
+    stream = torch.cuda.current_stream()
+    plan.init(ardm, work, stream)
+    plan.steps(1, L, ardm, work, stream)                 # growth (untimed)
+    plan.steps(L, L + Wm, ardm, work, stream)            # warm-up slide steps
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)  # let the sampler start
+        ev0.record(stream)
+        launches = plan.steps(L + Wm, L + Wm + K, ardm, work, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    rho = plan.read_rho(work, stream)
+    tr_err = float(np.abs(np.einsum("kii->k", rho) - 1).max())
+    del ardm, work
+    torch.cuda.empty_cache()
+
+    # e2e: the whole public-API call from host inputs to host rho (plan setup, H2D tables,
+    # growth, all steps of the workload with readout, D2H) for the BASELINE config itself
+    e2e = None
+    if not args.no_e2e:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pe = Q.Plan(base)
+        a2, w2 = pe.alloc()
+        rho_e = pe.run(a2, w2, stream)
+        el = time.perf_counter() - t0
+        se = pe.sizes
+        h2d = se.init_h2d_bytes  # tables + A_0 + rho(0)
+        d2h = se.n_out * se.N * 16
+        tt = torch.tensor([el], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * base.n_steps / float(tt.item()), "unit": "steps/s",
+               "h2d_bytes_per_step": int(h2d // base.n_steps), "d2h_bytes_per_step": int(d2h // base.n_steps),
+               "seconds": float(tt.item()), "steps": base.n_steps, "setup_seconds": se.setup_seconds,
+               "max_abs_trace_err": float(np.abs(np.einsum("kii->k", rho_e) - 1).max())}
+        del a2, w2
+
+    if rank == 0:
+        steps_per_s = world * K / (ms_max / 1e3)
+        bytes_step = 32 * sz.ardm_entries
+        per_kernel_s = (ms / 1e3) / K                      # rank-0 average slide-kernel duration
+        achieved = bytes_step / per_kernel_s / 1e9
+        peak, peak_kind = _peaks()
+        line = {
+            "metric": METRIC, "value": steps_per_s, "unit": "steps/s", "n_gpus": world, "steps": K,
+            "warmup": Wm, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": base.name, "ardm_entries": sz.ardm_entries, "ardm_bytes": sz.ardm_bytes,
+                       "readout": "every step (allPoints), fused", "l2": "inputs larger than L2 (4.3 GB ARDM)",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "grid": plan.sizes.grid, "block": sz.block, "tile_fibres": sz.tile_fibres},
+            "achieved_gbs": achieved,
+            "element_updates_per_s": steps_per_s * sz.ardm_entries,
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "frac_of_8TBs": achieved / 8000.0,
+                         "traffic": _ncu_traffic(), "algorithmic_bytes_per_launch": bytes_step},
+            "clocks": clk.summary(),
+            "max_abs_trace_err": tr_err,
+            "e2e": e2e,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args.cfg)
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

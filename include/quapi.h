@@ -100,6 +100,7 @@ typedef struct {
     int32_t grid, block;     /* slide-kernel launch configuration                                */
     int32_t tile_fibres;     /* fibres per tile                                                  */
     double setup_seconds;    /* host time spent in qp_plan_create (validation, U, eta, tables)  */
+    int64_t init_h2d_bytes;  /* bytes qp_init copies host->device (tables, A_0, rho(0))         */
 } qp_sizes;
 
 /* Host only (no GPU needed): validate (a1), U = e^{-iH dt} and the pair propagator K (a2),

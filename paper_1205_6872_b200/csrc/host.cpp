@@ -21,6 +21,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -314,7 +315,7 @@ struct qp_plan {
     std::vector<cd> A0;                // [N]
     // device image
     std::vector<double2> small;        // SmallLayout
-    int v = 0, T = 1, G = 1, X = 1, n_tiles = 1, block = 256, fib = 1, wgrp = 1;
+    int variant = 0, v = 0, T = 1, G = 1, X = 1, n_tiles = 1, block = 256, fib = 1, wgrp = 1;
     std::vector<double2> Etab;         // [L][2][G][D][X]
     std::vector<int2> lofs;            // [L][T]
     std::vector<qp::SlideArgs> sargs;  // per p, pointers filled at init
@@ -423,8 +424,8 @@ void build_tables(qp_plan &P) {
             }
         }
     // ---- slide tiles and digit-group factor tables
-    int block, F, v, w;
-    qp::slide_shape(M, &block, &F, &v, &w);
+    const qp::SlideVariant *var = qp::find_variant(P.variant);
+    const int block = var->block, F = var->F, v = var->v, w = var->w;
     const int nmid = L - 1;
     P.v = std::min(v, nmid);
     P.T = (int)ipow(N, P.v);
@@ -588,6 +589,11 @@ qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
     for (int i = 0; i < P->M * P->M; ++i) X[i] = cd(0.0, -P->dt) * P->H[i];
     P->U = expm_taylor(X, P->M);
     build_classes(*P);
+    P->variant = qp::default_variant(P->M);
+    if (const char *ev = std::getenv("QUAPI_SLIDE_VARIANT")) {  // tuning override
+        const qp::SlideVariant *var = qp::find_variant(std::atoi(ev));
+        if (var && var->M == P->M) P->variant = var->id;
+    }
     if ((st = compute_eta(*P, *pr))) { delete P; return st; }
     build_tables(*P);
     P->ardm_entries = ipow(P->N, P->L);
@@ -620,6 +626,7 @@ qp_status qp_plan_query(const qp_plan *P, qp_sizes *o) {
     o->block = P->block;
     o->tile_fibres = P->T;
     o->setup_seconds = P->setup_seconds;
+    o->init_h2d_bytes = (int64_t)((P->small.size() + P->Etab.size() + 2 * P->N) * sizeof(double2) + P->lofs.size() * sizeof(int2));
     return QP_OK;
 }
 
@@ -668,7 +675,7 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
     // the host vectors above are pageable: cudaMemcpyAsync from pageable memory returns after the
     // source has been staged, so they may go out of scope.
     // persistent slide grid: fixed per (plan, device type) => deterministic readout order
-    const int occ = 2;  // design point: 2 resident CTAs per SM (register budget)
+    const int occ = std::max(1, qp::slide_occupancy(P->variant, P->lattice, P->T));
     P->grid = std::max(1, std::min<int>({P->n_tiles, P->sms * occ, qp::kPartialsMax}));
     P->next_k = 1;
     P->inited = true;
@@ -711,7 +718,7 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             a.lofs = (const int2 *)(w + P->off_lofs) + (size_t)p * P->T;
             a.partials = part; a.rho = rho; a.counter = cnt;
             a.variant = (k == P->L) ? 1 : 0;
-            e = qp::launch_slide(P->M, P->lattice, a, P->grid, s);
+            e = qp::launch_slide(P->variant, P->lattice, a, P->grid, s);
         }
         if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
         ++launched;

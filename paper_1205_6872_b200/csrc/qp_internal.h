@@ -74,10 +74,15 @@ struct GrowArgs {
     double delta[kMaxD];     // Delta s of each class (index d-1)
 };
 
+// Slide-kernel variant: launch shape and pipelining (kernels.cu registry).
+struct SlideVariant {
+    int id, M, block, F, v, w, minb, prefetch, stages;  // stages > 0 => TMA-staged kernel
+};
+const SlideVariant *find_variant(int id);
+int default_variant(int M);
 // Launchers (kernels.cu).  Return cudaError_t of the launch.
-cudaError_t launch_slide(int M, bool lattice, const SlideArgs &a, int grid, cudaStream_t s);
+cudaError_t launch_slide(int variant, bool lattice, const SlideArgs &a, int grid, cudaStream_t s);
+int slide_occupancy(int variant, bool lattice, int T);  // resident CTAs per SM (needs a device)
 cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaStream_t s);
-// Slide-kernel block size and fibres per thread for this M (must match the kernel templates).
-void slide_shape(int M, int *block, int *fibres_per_thread, int *tile_digits, int *group_digits);
 
 }  // namespace qp

@@ -176,3 +176,16 @@ def test_sigma_x_symmetry_full_size():
     a, _, _ = gpu_run(w.with_(rho0=rho0))
     b, _, _ = gpu_run(w.with_(rho0=X @ rho0 @ X))
     assert np.abs(b - X @ a @ X).max() < 1e-12
+
+
+@pytest.mark.parametrize("variant,M,L,n", [(0, 2, 7, 20), (1, 2, 7, 20), (2, 2, 7, 20), (3, 2, 7, 20),
+                                           (2, 2, 3, 9), (5, 2, 7, 20), (6, 2, 8, 21), (7, 2, 8, 21), (8, 2, 7, 20),
+                                           (5, 2, 3, 9), (7, 2, 3, 9), (10, 3, 5, 12), (11, 3, 5, 12), (12, 3, 5, 12),
+                                           (13, 3, 5, 12), (14, 3, 5, 12), (20, 4, 4, 8)])
+def test_every_slide_variant(variant, M, L, n, monkeypatch):
+    """Each tile shape / pipelining variant of k_slide against the oracle."""
+    monkeypatch.setenv("QUAPI_SLIDE_VARIANT", str(variant))
+    for lat in (True, False) if M > 2 else (True,):
+        w = W.random_problem(300 + variant, M, L, n, kind=W.J_DEBYE, lattice_s=lat)
+        rg, plan, _ = gpu_run(w)
+        check(rg, O.run(P(w)))
