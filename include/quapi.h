@@ -101,6 +101,7 @@ typedef struct {
     int32_t tile_fibres;     /* fibres per tile                                                  */
     double setup_seconds;    /* host time spent in qp_plan_create (validation, U, eta, tables)  */
     int64_t init_h2d_bytes;  /* bytes qp_init copies host->device (tables, A_0, rho(0))         */
+    int32_t fuse_steps;      /* time steps fused into one pass over the ARDM (slide kernel)      */
 } qp_sizes;
 
 /* Host only (no GPU needed): validate (a1), U = e^{-iH dt} and the pair propagator K (a2),
@@ -122,7 +123,8 @@ qp_status qp_plan_propagator(const qp_plan *plan, qp_c64 *U_out);
 qp_status qp_init(qp_plan *plan, void *d_ardm, void *d_work, void *stream);
 /* Enqueue time steps k = k_begin .. k_end-1 (1 <= k_begin <= k_end <= n_steps+1): step k turns
    A_{k-1} into A_k in place (growth for k < L, slide for k >= L) and, when k is an output step,
-   reduces rho(t_k) from A_{k-1} in the same pass (fused readout).  One kernel launch per step.
+   reduces rho(t_k) from A_{k-1} in the same pass (fused readout).  Slide steps are fused in
+   groups of fuse_steps (aligned on k - L) into one kernel launch, i.e. one pass over the ARDM.
    Steps must be enqueued in order after qp_init.  Returns the number of kernels launched in
    *n_launch (may be NULL). */
 qp_status qp_steps(qp_plan *plan, int64_t k_begin, int64_t k_end, void *d_ardm, void *d_work, void *stream,

@@ -303,6 +303,8 @@ qp_status eta_class(const Bath &b, const WinClass &c, cd *out, const char *name,
 struct qp_plan {
     int M = 0, N = 0, L = 0, D = 0;
     bool lattice = false;        // class map used by the kernels
+    bool sym = false;            // M = 2 with s = (+s, -s): symmetric-moment kernel
+    int kind = 1;                // fused kernel variant: 1 = register super-fibre where available, 0 = warp-mapped
     double dt = 0.0;
     int64_t n_steps = 0;
     std::vector<int64_t> out_steps;
@@ -315,13 +317,22 @@ struct qp_plan {
     std::vector<cd> A0;                // [N]
     // device image
     std::vector<double2> small;        // SmallLayout
-    int variant = 0, v = 0, T = 1, G = 1, X = 1, n_tiles = 1, block = 256, fib = 1, wgrp = 1;
-    std::vector<double2> Etab;         // [L][2][G][D][X]
-    std::vector<int2> lofs;            // [L][T]
-    std::vector<qp::SlideArgs> sargs;  // per p, pointers filled at init
-    size_t off_small = 0, off_E = 0, off_lofs = 0, off_part = 0, off_rho = 0, off_cnt = 0, work_bytes = 0;
+    struct LaunchSet {                 // fused launch over inner slots p0..p0+S-1 (mod L)
+        int p0 = 0, S = 1;
+        std::vector<double2> inner;    // [S][S][2][D][N]
+        std::vector<double2> Etab;     // [S][2][G][D][X]
+        std::vector<long long> goff;   // [G][X]
+        std::vector<int2> lofs;        // [T]
+        size_t off_inner = 0, off_E = 0, off_goff = 0, off_lofs = 0;
+        qp::FusedArgs args{};          // table pointers filled in qp_steps
+    };
+    qp::FusedShape shape{};
+    int Smax = 1;
+    std::vector<LaunchSet> sets;       // index p0 * Smax + (S - 1)
+    size_t off_small = 0, off_part = 0, off_rho = 0, off_cnt = 0, tables_end = 0, work_bytes = 0;
     int64_t ardm_entries = 0;
-    int grid = 0, sms = 0;
+    int grid[qp::kMaxS + 1] = {0};
+    int sms = 0;
     int64_t next_k = 1;
     bool inited = false;
     double setup_seconds = 0.0;
@@ -350,6 +361,7 @@ void build_classes(qp_plan &P) {
             if (std::fabs(P.s[a] - (P.s[0] + a * u)) > 1e-15 * std::max(1.0, std::fabs(P.s[a]))) lat = false;
     }
     P.lattice = lat;
+    P.sym = (M == 2) && P.s[0] == -P.s[1] && P.s[0] != 0.0 && !std::getenv("QUAPI_NO_SYM");
     P.D = qp::n_classes(M, lat);
     P.delta.assign(P.D, 0.0);
     for (int a = 0; a < M; ++a)
@@ -423,82 +435,110 @@ void build_tables(qp_plan &P) {
                 P.small[lay.psi(1) + ((size_t)k * L + j) * N + sg] = d2(psi(P, sg, et));
             }
         }
-    // ---- slide tiles and digit-group factor tables
-    const qp::SlideVariant *var = qp::find_variant(P.variant);
-    const int block = var->block, F = var->F, v = var->v, w = var->w;
-    const int nmid = L - 1;
-    P.v = std::min(v, nmid);
-    P.T = (int)ipow(N, P.v);
-    P.n_tiles = (int)ipow(N, nmid - P.v);
-    P.block = block;
-    P.fib = F;
-    P.wgrp = w;
-    const int hi = nmid - P.v;
-    P.G = 1 + (hi + w - 1) / w;
-    P.X = P.T;
-    for (int g = 1; g < P.G; ++g) P.X = std::max<int>(P.X, (int)ipow(N, std::min(w, hi - (g - 1) * w)));
-    P.Etab.assign((size_t)L * 2 * P.G * D * P.X, make_double2(1.0, 0.0));
-    P.lofs.assign((size_t)L * P.T, make_int2(0, -1));
-    P.sargs.assign(L, qp::SlideArgs{});
-    for (int p = 0; p < L; ++p) {
-        auto pos_of = [&](int i) { return i < p ? i : i + 1; };  // mid digit i -> ARDM digit
-        auto lag_of = [&](int i) { return ((p - pos_of(i)) % L + L) % L; };
-        // group tables
-        for (int g = 0; g < P.G; ++g) {
-            const int i0 = (g == 0) ? 0 : P.v + (g - 1) * w;
-            const int nd = (g == 0) ? P.v : std::min(w, hi - (g - 1) * w);
-            const int cnt = (int)ipow(N, nd);
-            for (int x = 0; x < cnt; ++x) {
-                cd Ps[2] = {0.0, 0.0};
-                int r = x;
-                for (int t = 0; t < nd; ++t) {
-                    const int dig = r % N;
-                    r /= N;
-                    const int lag = lag_of(i0 + t);
-                    Ps[0] += psi(P, dig, P.eta[lag]);
-                    Ps[1] += psi(P, dig, P.E[lag]);
+    // ---- fused launch sets: for every start slot p0 and fusion depth S, the super-fibres of the
+    //      inner slots p0..p0+S-1 and the factor / address tables of the L-S outer slots
+    P.shape = qp::fused_shape(M);
+    P.Smax = std::max(1, std::min(P.shape.S, L - 1));
+    if (const char *ek = std::getenv("QUAPI_FUSED_KIND")) P.kind = (ek[0] == 'w') ? 0 : 1;
+    if (const char *ev = std::getenv("QUAPI_FUSE_S")) P.Smax = std::max(1, std::min(P.Smax, std::atoi(ev)));
+    P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
+    for (int p0 = 0; p0 < L; ++p0)
+        for (int S = 1; S <= P.Smax; ++S) {
+            qp_plan::LaunchSet &ls = P.sets[(size_t)p0 * P.Smax + (S - 1)];
+            ls.p0 = p0;
+            ls.S = S;
+            std::vector<int> inner(S), outer;
+            for (int i = 0; i < S; ++i) inner[i] = (p0 + i) % L;
+            for (int q = 0; q < L; ++q)
+                if (std::find(inner.begin(), inner.end(), q) == inner.end()) outer.push_back(q);  // ascending
+            const int nout = (int)outer.size();
+            const int v = std::min(qp::fused_tile_digits(M, S, P.kind), nout), w = std::max(1, P.shape.w);
+            const int hi = nout - v;
+            const int G = 1 + (hi + w - 1) / w;
+            const int T = (int)ipow(N, v);
+            int X = T;
+            for (int g = 1; g < G; ++g) X = std::max<int>(X, (int)ipow(N, std::min(w, hi - (g - 1) * w)));
+            auto g_first = [&](int g) { return g == 0 ? 0 : v + (g - 1) * w; };
+            auto g_size = [&](int g) { return g == 0 ? v : std::min(w, hi - (g - 1) * w); };
+            // outer digit group tables: per sub-step s, kind kap, exponent over the group's digits
+            ls.Etab.assign((size_t)S * 2 * G * D * X, make_double2(1.0, 0.0));
+            for (int st = 0; st < S; ++st)
+                for (int g = 0; g < G; ++g) {
+                    const int i0 = g_first(g), nd = g_size(g);
+                    for (int x = 0; x < (int)ipow(N, nd); ++x) {
+                        cd Ps[2] = {0.0, 0.0};
+                        int r = x;
+                        for (int t = 0; t < nd; ++t) {
+                            const int dig = r % N;
+                            r /= N;
+                            const int lag = ((p0 + st - outer[i0 + t]) % L + L) % L;  // 1..L-1
+                            Ps[0] += psi(P, dig, P.eta[lag]);  // propagate: partner interior
+                            Ps[1] += psi(P, dig, P.E[lag]);    // terminal (readout) edge class
+                        }
+                        for (int kap = 0; kap < 2; ++kap)
+                            for (int d = 0; d < D; ++d)
+                                ls.Etab[((((size_t)st * 2 + kap) * G + g) * D + d) * X + x] = d2(std::exp(P.delta[d] * Ps[kap]));
+                    }
                 }
-                for (int kap = 0; kap < 2; ++kap)
-                    for (int d = 0; d < D; ++d)
-                        P.Etab[((((size_t)p * 2 + kap) * P.G + g) * D + d) * P.X + x] = d2(std::exp(P.delta[d] * Ps[kap]));
+            // inner-slot factors: sub-step st, inner digit i != st (new value if i < st, old if i > st)
+            ls.inner.assign((size_t)S * S * 2 * D * N, make_double2(1.0, 0.0));
+            for (int st = 0; st < S; ++st)
+                for (int i = 0; i < S; ++i) {
+                    if (i == st) continue;
+                    const int lag = i < st ? st - i : L - (i - st);
+                    for (int kap = 0; kap < 2; ++kap)
+                        for (int d = 0; d < D; ++d)
+                            for (int sg = 0; sg < N; ++sg)
+                                ls.inner[((((size_t)st * S + i) * 2 + kap) * D + d) * N + sg] =
+                                    d2(std::exp(P.delta[d] * psi(P, sg, kap == 0 ? P.eta[lag] : P.E[lag])));
+                }
+            // address offsets of the outer digit groups g >= 1 and of the tile-local fibres
+            ls.goff.assign((size_t)G * X, 0);
+            for (int g = 1; g < G; ++g) {
+                const int i0 = g_first(g), nd = g_size(g);
+                for (int x = 0; x < (int)ipow(N, nd); ++x) {
+                    long long o = 0;
+                    int r = x;
+                    for (int t = 0; t < nd; ++t) { o += (long long)(r % N) * ipow(N, outer[i0 + t]); r /= N; }
+                    ls.goff[(size_t)g * X + x] = o;
+                }
             }
+            const int qlast = (p0 - 1 + L) % L;  // sub-step 0's 'last' point sigma_{k-1}
+            const int ilast = (int)(std::find(outer.begin(), outer.end(), qlast) - outer.begin());
+            ls.lofs.assign(T, make_int2(0, -1));
+            for (int fl = 0; fl < T; ++fl) {
+                long long o = 0;
+                int r = fl;
+                for (int t = 0; t < v; ++t) { o += (long long)(r % N) * ipow(N, outer[t]); r /= N; }
+                const int lastd = ilast < v ? (int)((fl / ipow(N, ilast)) % N) : -1;
+                ls.lofs[fl] = make_int2((int)o, lastd);
+            }
+            qp::FusedArgs &a = ls.args;
+            for (int i = 0; i < S; ++i) a.pw_in[i] = ipow(N, inner[i]);
+            a.n_tiles = (int)ipow(N, hi);
+            a.T = T;
+            a.G = G;
+            a.X = X;
+            for (int g = 1; g < G; ++g) {
+                a.gdiv[g] = (int)ipow(N, (g - 1) * w);
+                a.gmod[g] = (int)ipow(N, g_size(g));
+            }
+            a.last_div = ilast >= v ? (int)ipow(N, ilast - v) : -1;
         }
-        // in-tile offsets and lo 'last' digit
-        const int qlast = (p - 1 + L) % L;
-        const int ilast = qlast < p ? qlast : qlast - 1;
-        for (int fl = 0; fl < P.T; ++fl) {
-            int64_t off;
-            if (p >= P.v) off = fl;
-            else off = (fl % ipow(N, p)) + (fl / ipow(N, p)) * ipow(N, p + 1);
-            int lastd = -1;
-            if (ilast < P.v) lastd = (int)((fl / ipow(N, ilast)) % N);
-            P.lofs[(size_t)p * P.T + fl] = make_int2((int)off, lastd);
-        }
-        qp::SlideArgs &a = P.sargs[p];
-        a.pw_p = ipow(N, p);
-        a.pw_p1 = ipow(N, p + 1);
-        a.tile_stride = ipow(N, P.v + 1);
-        a.n_tiles = P.n_tiles;
-        a.T = P.T;
-        a.p_ge_v = p >= P.v;
-        a.Qlo = p >= P.v ? (int)ipow(N, p - P.v) : 1;
-        a.G = P.G;
-        a.X = P.X;
-        for (int g = 1; g < P.G; ++g) {
-            a.gdiv[g] = (int)ipow(N, (g - 1) * w);
-            a.gmod[g] = (int)ipow(N, std::min(w, hi - (g - 1) * w));
-        }
-        a.last_div = ilast >= P.v ? (int)ipow(N, ilast - P.v) : -1;
-    }
     // ---- A_0(sigma_0) = rho0(sigma_0) I(sigma_0, sigma_0; eta_00 = G(1/2))   (Eq. 13, reading C.3-2)
     P.A0.assign(N, 0.0);
     for (int sg = 0; sg < N; ++sg) P.A0[sg] = P.rho0[sg] * std::exp(dsig(P, sg) * psi(P, sg, P.self_end));
     // ---- workspace layout
     size_t off = 0;
     P.off_small = off; off = align256(off + P.small.size() * sizeof(double2));
-    P.off_E = off;     off = align256(off + P.Etab.size() * sizeof(double2));
-    P.off_lofs = off;  off = align256(off + P.lofs.size() * sizeof(int2));
-    P.off_part = off;  off = align256(off + (size_t)qp::kPartialsMax * N * sizeof(double2));
+    for (auto &ls : P.sets) {
+        ls.off_inner = off; off = align256(off + ls.inner.size() * sizeof(double2));
+        ls.off_E = off;     off = align256(off + ls.Etab.size() * sizeof(double2));
+        ls.off_goff = off;  off = align256(off + ls.goff.size() * sizeof(long long));
+        ls.off_lofs = off;  off = align256(off + ls.lofs.size() * sizeof(int2));
+    }
+    P.tables_end = off;
+    P.off_part = off;  off = align256(off + (size_t)qp::kMaxS * qp::kPartialsMax * N * sizeof(double2));
     P.off_rho = off;   off = align256(off + std::max<size_t>(1, P.out_steps.size()) * N * sizeof(double2));
     P.off_cnt = off;   off = align256(off + 256);
     P.work_bytes = off;
@@ -589,11 +629,6 @@ qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
     for (int i = 0; i < P->M * P->M; ++i) X[i] = cd(0.0, -P->dt) * P->H[i];
     P->U = expm_taylor(X, P->M);
     build_classes(*P);
-    P->variant = qp::default_variant(P->M);
-    if (const char *ev = std::getenv("QUAPI_SLIDE_VARIANT")) {  // tuning override
-        const qp::SlideVariant *var = qp::find_variant(std::atoi(ev));
-        if (var && var->M == P->M) P->variant = var->id;
-    }
     if ((st = compute_eta(*P, *pr))) { delete P; return st; }
     build_tables(*P);
     P->ardm_entries = ipow(P->N, P->L);
@@ -622,11 +657,12 @@ qp_status qp_plan_query(const qp_plan *P, qp_sizes *o) {
     o->bytes_per_step = 32 * P->ardm_entries;
     o->lattice = P->lattice;
     o->n_classes = P->D;
-    o->grid = P->grid;
-    o->block = P->block;
-    o->tile_fibres = P->T;
+    o->grid = P->grid[P->Smax];
+    o->block = qp::fused_block(P->M, P->Smax, P->kind);
+    o->tile_fibres = P->sets.empty() ? 0 : P->sets[(size_t)P->Smax - 1].args.T;
+    o->fuse_steps = P->Smax;
     o->setup_seconds = P->setup_seconds;
-    o->init_h2d_bytes = (int64_t)((P->small.size() + P->Etab.size() + 2 * P->N) * sizeof(double2) + P->lofs.size() * sizeof(int2));
+    o->init_h2d_bytes = (int64_t)(P->tables_end + 2 * P->N * sizeof(double2));
     return QP_OK;
 }
 
@@ -659,8 +695,12 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
     QP_CUDA(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
     char *w = (char *)d_work;
     QP_CUDA(cudaMemcpyAsync(w + P->off_small, P->small.data(), P->small.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
-    QP_CUDA(cudaMemcpyAsync(w + P->off_E, P->Etab.data(), P->Etab.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
-    QP_CUDA(cudaMemcpyAsync(w + P->off_lofs, P->lofs.data(), P->lofs.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    for (const auto &ls : P->sets) {
+        QP_CUDA(cudaMemcpyAsync(w + ls.off_inner, ls.inner.data(), ls.inner.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+        QP_CUDA(cudaMemcpyAsync(w + ls.off_E, ls.Etab.data(), ls.Etab.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+        QP_CUDA(cudaMemcpyAsync(w + ls.off_goff, ls.goff.data(), ls.goff.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
+        QP_CUDA(cudaMemcpyAsync(w + ls.off_lofs, ls.lofs.data(), ls.lofs.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    }
     QP_CUDA(cudaMemsetAsync(w + P->off_cnt, 0, 256, s));
     std::vector<double2> a0(P->N);
     for (int i = 0; i < P->N; ++i) a0[i] = d2(P->A0[i]);
@@ -675,8 +715,11 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
     // the host vectors above are pageable: cudaMemcpyAsync from pageable memory returns after the
     // source has been staged, so they may go out of scope.
     // persistent slide grid: fixed per (plan, device type) => deterministic readout order
-    const int occ = std::max(1, qp::slide_occupancy(P->variant, P->lattice, P->T));
-    P->grid = std::max(1, std::min<int>({P->n_tiles, P->sms * occ, qp::kPartialsMax}));
+    for (int S = 1; S <= P->Smax; ++S) {
+        const int occ = std::max(1, qp::fused_occupancy(P->M, P->lattice, P->sym, P->kind, S));
+        const int nt = P->sets[(size_t)S - 1].args.n_tiles;  // same for every p0
+        P->grid[S] = std::max(1, std::min<int>({nt, P->sms * occ, qp::kPartialsMax}));
+    }
     P->next_k = 1;
     P->inited = true;
     return QP_OK;
@@ -697,13 +740,14 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
     double2 *part = (double2 *)(w + P->off_part);
     unsigned *cnt = (unsigned *)(w + P->off_cnt);
     int64_t launched = 0;
-    for (int64_t k = k_begin; k < k_end; ++k) {
-        const int64_t slot = P->slot_of(k);
-        double2 *rho = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * P->N : nullptr;
+    for (int64_t k = k_begin; k < k_end;) {
         cudaError_t e;
+        int64_t adv = 1;
         if (k < P->L) {
+            const int64_t slot = P->slot_of(k);
             qp::GrowArgs g{};
-            g.A = A; g.small = small; g.partials = part; g.rho = rho; g.counter = cnt;
+            g.A = A; g.small = small; g.partials = part; g.counter = cnt;
+            g.rho = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * P->N : nullptr;
             g.n_in = ipow(P->N, (int)k);
             g.k = (int)k;
             g.L = P->L;
@@ -711,18 +755,50 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             const int grid = (int)std::min<int64_t>({(g.n_in + 255) / 256, (int64_t)P->sms * 8, (int64_t)qp::kPartialsMax});
             e = qp::launch_grow(P->M, P->lattice, g, std::max(1, grid), s);
         } else {
-            const int p = (int)(k % P->L);
-            qp::SlideArgs a = P->sargs[p];
-            a.A = A; a.small = small;
-            a.Etab = (const double2 *)(w + P->off_E) + (size_t)p * 2 * P->G * P->D * P->X;
-            a.lofs = (const int2 *)(w + P->off_lofs) + (size_t)p * P->T;
-            a.partials = part; a.rho = rho; a.counter = cnt;
-            a.variant = (k == P->L) ? 1 : 0;
-            e = qp::launch_slide(P->variant, P->lattice, a, P->grid, s);
+            // fusion groups are aligned on absolute k (k - L multiple of Smax), so the floating-point
+            // grouping of a step does not depend on how the caller segments qp_steps calls
+            const int64_t grp_end = P->L + ((k - P->L) / P->Smax + 1) * P->Smax;
+            const int S = (int)std::min<int64_t>(grp_end, k_end) - (int)k;
+            const int p0 = (int)(k % P->L);
+            const qp_plan::LaunchSet &ls = P->sets[(size_t)p0 * P->Smax + (S - 1)];
+            qp::FusedArgs a = ls.args;
+            a.A = A;
+            a.small = small;
+            a.inner = (const double2 *)(w + ls.off_inner);
+            a.Etab = (const double2 *)(w + ls.off_E);
+            a.goff = (const long long *)(w + ls.off_goff);
+            a.lofs = (const int2 *)(w + ls.off_lofs);
+            a.partials = part;
+            a.counter = cnt;
+            bool ro = false;
+            for (int st = 0; st < S; ++st) {
+                const int64_t slot = P->slot_of(k + st);
+                a.rho[st] = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * P->N : nullptr;
+                ro |= slot >= 0;
+                const int var = (k + st == P->L) ? 1 : 0;
+                const qp::SmallLayout lay{P->N, P->D, P->L};
+                for (int kap = 0; kap < 2; ++kap)
+                    for (int d = 0; d < P->D; ++d)
+                        for (int old = 0; old < P->N; ++old)
+                            a.beta[st][kap][d][old] = P->small[lay.beta(var, kap) + d * P->N + old];
+                if (P->sym) {  // class 1 = (0,1): beta_1 = (c, rho, 1/rho, conj c)
+                    for (int kap = 0; kap < 2; ++kap) {
+                        const double2 c = a.beta[st][kap][0][0];
+                        const double rho = a.beta[st][kap][0][1].x;
+                        a.sym[st][kap][0] = c.x;
+                        a.sym[st][kap][1] = c.y;
+                        a.sym[st][kap][2] = 0.5 * (rho + 1.0 / rho);
+                        a.sym[st][kap][3] = 0.5 * (rho - 1.0 / rho);
+                    }
+                }
+            }
+            e = qp::launch_fused(P->M, P->lattice, P->sym, P->kind, S, a, ro, P->grid[S], s);
+            adv = S;
         }
         if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
         ++launched;
-        P->next_k = k + 1;
+        k += adv;
+        P->next_k = k;
     }
     if (n_launch) *n_launch = launched;
     return QP_OK;

@@ -1,22 +1,29 @@
 // kernels.cu -- sm_100a kernels of the QUAPI tensor-propagator step (arXiv 1205.6872).
 //
-// k_slide : one time step k >= L of the iterative tensor propagator (Makri-Makarov scheme the
-//           paper accelerates, "BSXFUN" lines), in place on a ring-buffer ARDM,
-//           with the rho(t_k) readout ("line 169") fused into the same pass.
+// k_fused : S consecutive time steps k..k+S-1 (k >= L) of the iterative tensor propagator (the
+//           Makri-Makarov scheme the paper accelerates; the "BSXFUN" lines P:384) in ONE
+//           pass over HBM, in place on a ring-buffer ARDM, with the rho(t) readout of every
+//           requested step ("line 169") fused into the same pass.
 // k_grow  : growth steps 1 <= k < L (no contraction; the tensor gains one digit per step).
 //
-// ARDM layout: A has N^L complex FP64 entries, flat index x = sum_q d_q N^q.
-// Time point t lives in digit q = t mod L ("ring slot"), so no data is ever transposed.
-// Step k (k >= L) contracts slot p = k mod L (holding sigma_{k-L}) and writes sigma_k into the
-// same slot.  For one fibre (all digits except p fixed = "mid") with old values a[old]:
+// ARDM layout: N^L complex FP64 entries, flat index x = sum_q d_q N^q; time point
+// t lives in digit ("ring slot") q = t mod L, so nothing is ever transposed.  Step k contracts
+// slot k mod L (holding sigma_{k-L}) and writes sigma_k into the same slot.  For one fibre (all
+// slots except the contracted one fixed) with old values a[old]:
 //   out[new] = K'(new, last) * exp(Ds(new) Psi(mid)) * sum_old exp(Ds(new) psi_L(old)) a[old]
-// where Ds = s+ - s- of the new pair state, K' = self factor * bare propagator pair (Eq. 8),
-// Psi(mid) = sum_j psi_j(digit at lag j) the Eq. 9 exponent of the kept partners and psi_L the
-// lag-L (summed) partner.  Rows with the same Ds share one "moment" S_d = sum_old beta_d(old) a[old]
-// and one factor E_d = exp(delta_d Psi): E_d is a product of per-digit-group tables (host-built),
-// one uniform factor per tile times one per-fibre factor.  No transcendental in the slide kernel.
-// The readout of rho(t_k) uses the same loaded fibre with the terminal classes (E_j, TI) and
-// accumulates sum over all mid of K'_term * E^T_d * S^T_d (diagonal rows: the propagated value).
+// Ds = s+ - s- of the new pair state, K' = self factor x bare propagator pair (Eq. 8),
+// Psi(mid) = sum_j psi_j(partner at lag j) the Eq. 9 exponent of the kept partners.  Rows with the
+// same Ds share one moment S_d = sum_old beta_d(old) a[old] and one factor E_d = exp(delta_d Psi),
+// a product of host-built tables (no transcendental in the kernel).
+//
+// Step fusion: step k only reads/writes slot p = k mod L, and its factors depend on the other
+// slots only through their values.  Steps k..k+S-1 touch slots p..p+S-1 only, so for every fixed
+// value of the other L-S ("outer") slots the N^S entries of the "super-fibre" evolve independently
+// through all S steps.  One thread loads its super-fibre once, applies S steps in registers
+// (reading rho of each step from the pre-step values) and stores it once: HBM traffic per step
+// drops from 32 B to 32/S B per ARDM entry.
+#include <cstdlib>
+
 #include "qp_internal.h"
 
 namespace qp {
@@ -34,6 +41,8 @@ __device__ __forceinline__ double2 cexp_(double2 z) {
     return make_double2(e * c, e * s);
 }
 
+__host__ __device__ constexpr int cpow(int b, int e) { return e == 0 ? 1 : b * cpow(b, e - 1); }
+
 // Fixed-order block reduction of N complex accumulators into partials[blockIdx][N]; the last
 // block to finish sums the partials over blocks in fixed order into rho[N] (deterministic:
 // the grid and the tile->block assignment are fixed by the plan).
@@ -45,6 +54,7 @@ __device__ __forceinline__ void reduce_finalize(double2 (&acc)[N], double2 *part
     __shared__ double2 fin[W];
     __shared__ int is_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();  // red/fin may be reused by consecutive calls
 #pragma unroll
     for (int n = 0; n < N; ++n) {
 #pragma unroll
@@ -87,325 +97,434 @@ __device__ __forceinline__ void reduce_finalize(double2 (&acc)[N], double2 *part
 }
 
 // --------------------------------------------------------------------------------------------
-// Slide step (k >= L), persistent over tiles.  Tile tau = T consecutive fibres (the v lowest
-// "mid" digits vary inside a tile).  Thread t owns fibres f = t + j*BLOCK (j < F) of every tile
-// it visits; it issues all F*N 16-byte loads of a tile before any arithmetic.  With PREF the
-// loads of the thread's next tile are issued before the current tile is computed and stored
-// (register double buffering), so HBM requests stay in flight through the FP64 work.
+// Fused slide kernel.  Persistent CTAs over a contiguous, static range of tiles.  Tile tau = TILE
+// consecutive outer fibres (the v lowest outer slots vary inside a tile).  Thread (r, t) with
+// r = threadIdx.x / TILE, t = threadIdx.x % TILE works on outer fibre t; during sub-step s it holds
+// the N entries of the fibre along inner digit s whose other inner digits are the digits of r.
+// A warp therefore covers 32 consecutive outer fibres with ONE inner combination r: every table
+// index (inner factors, 'last', K' row) is warp-uniform and the 32 lanes read 32 consecutive
+// ARDM entries per load.  Between sub-steps the CTA re-distributes entries through shared memory.
+// Inner digit i (i < S) is slot (p0 + i) mod L with address stride pw_in[i]; entry e = sum_i d_i N^i
+// of outer fibre t lives at tile_base + lofs[t].x + sum_i d_i pw_in[i].
 // --------------------------------------------------------------------------------------------
-__device__ __forceinline__ long long tile_base(const SlideArgs &a, int tau) {
-    return a.p_ge_v ? (long long)(tau % a.Qlo) * a.T + (long long)(tau / a.Qlo) * a.pw_p1
-                    : (long long)tau * a.tile_stride;
+template <int N, int S>
+__device__ __forceinline__ int fib_elem(int s, int r, int v) {  // entry of fibre r along digit s, value v
+    int e = 0, rr = r, pw = 1;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+        int d;
+        if (i == s) d = v;
+        else { d = rr % N; rr /= N; }
+        e += d * pw;
+        pw *= N;
+    }
+    return e;
+}
+template <int N, int S>
+__device__ __forceinline__ int fib_digit(int s, int r, int i) {  // digit i (i != s) of fibre r along s
+    int rr = r;
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+        if (q == s) continue;
+        if (q == i) return rr % N;
+        rr /= N;
+    }
+    return 0;
 }
 
-template <int M, bool LAT, int BLOCK, int F, int MINB, bool PREF, bool RO>
-__global__ void __launch_bounds__(BLOCK, MINB) k_slide(const __grid_constant__ SlideArgs a) {
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int TILE, int MINB, bool RO>
+__global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ FusedArgs a) {
     constexpr int N = M * M;
     constexpr int D = n_classes(M, LAT);
+    constexpr int Q = cpow(N, S - 1);    // inner combinations per sub-step (= fibres per super-fibre)
     constexpr int NK = RO ? 2 : 1;
+    static_assert(S == 1 || TILE * Q == BLOCK, "fused kernel: one thread per (outer fibre, inner combination)");
+    static_assert(S == 1 || TILE % 32 == 0, "fused kernel: warp-uniform inner combination");
+    static_assert(!SYM || (M == 2 && D == 2), "symmetric moments are the M = 2 s = (+s,-s) case");
     const SmallLayout lay{N, D, 0};
-    __shared__ double2 sK[2][N][N];   // K'(new, last): [0] propagate, [1] terminal (readout)
-    __shared__ double2 sB[2][D][N];   // beta_d(old):   [0] propagate, [1] terminal
+    __shared__ double2 sK[2][N][N];           // K'(new, last): [0] propagate, [1] terminal
+    __shared__ double2 sIn[S][S][2][D][N];    // inner-slot factors exp(delta_d psi_lag(sigma))
+    __shared__ double2 xch[S > 1 ? cpow(N, S) * TILE : 1];  // [entry][outer fibre] exchange buffer
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
-    for (int i = threadIdx.x; i < 2 * D * N; i += BLOCK) (&sB[0][0][0])[i] = a.small[lay.beta(a.variant, 0) + i];
+    for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
 
-    int off[F], lastlo[F];
-    bool valid[F];
+    const int r = threadIdx.x / TILE, t = threadIdx.x % TILE;
+    const bool valid = t < a.T && r < Q;
+    const int2 lo = valid ? a.lofs[t] : make_int2(0, 0);
+    long long off_ld = lo.x, off_st = lo.x;  // this thread's fibre along digit 0 (load) / S-1 (store)
 #pragma unroll
-    for (int j = 0; j < F; ++j) {
-        const int fl = threadIdx.x + j * BLOCK;
-        valid[j] = fl < a.T;
-        const int2 o = valid[j] ? a.lofs[fl] : make_int2(0, 0);
-        off[j] = o.x;
-        lastlo[j] = o.y;
+    for (int i = 1; i < S; ++i) off_ld += (long long)fib_digit<N, S>(0, r, i) * a.pw_in[i];
+#pragma unroll
+    for (int i = 0; i < S - 1; ++i) off_st += (long long)fib_digit<N, S>(S - 1, r, i) * a.pw_in[i];
+    double2 accR[RO ? S : 1][RO ? N : 1];
+#pragma unroll
+    for (int s = 0; s < (RO ? S : 1); ++s)
+#pragma unroll
+        for (int n = 0; n < (RO ? N : 1); ++n) accR[s][n] = make_double2(0.0, 0.0);
+
+    // contiguous, static tile range per CTA (deterministic readout order)
+    const int per = a.n_tiles / (int)gridDim.x, rem = a.n_tiles % (int)gridDim.x;
+    const int t_begin = (int)blockIdx.x * per + min((int)blockIdx.x, rem);
+    const int t_end = t_begin + per + ((int)blockIdx.x < rem ? 1 : 0);
+    // Tile-uniform data.  Tile-independent part, once per kernel:
+    //   KI[s][kap][r][new][last] = K'_kap(new, last) * prod_{i != s} inner_i(class(new), digit_i(r))
+    // Per tile (pipelined through rings, one barrier per tile):
+    //   stage A (tile i+2): Ehi[s][kap][d] = product of the outer digit-group tables g >= 1, base, last
+    //   stage B (tile i+1): KU[s][kap][r][new][last] = KI * Ehi[s][kap][class(new)]
+    // so KU holds every factor of output row `new` except the per-fibre outer group 0.
+    constexpr int NKU = S * NK * Q * N * N;
+    __shared__ double2 KI[S][NK][Q][N][N];
+    __shared__ double2 KU[3][S][NK][Q][N][N];
+    __shared__ double2 sEhi[4][S][NK][D];
+    __shared__ long long sBase[4];
+    __shared__ int sLast[4];
+    __syncthreads();  // sK, sIn loaded
+    for (int j = threadIdx.x; j < NKU; j += BLOCK) {
+        const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
+                  s = j / (N * N * Q * NK);
+        const int c = class_of(M, LAT, nw / M, nw % M);
+        double2 e = sK[kap][nw][last];
+        if (c > 0)
+            for (int i = 0; i < S; ++i)
+                if (i != s) e = cmul(e, sIn[s][i][kap][c - 1][fib_digit<N, S>(s, rr, i)]);
+        KI[s][kap][rr][nw][last] = e;
     }
-    double2 acc[RO ? N : 1];
-#pragma unroll
-    for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
-    __syncthreads();
-
-    double2 x[F][N], xn[PREF ? F : 1][N];
-    auto load = [&](int tau, double2 (&dst)[PREF ? F : 1][N], int jj) {
-        const double2 *src = a.A + tile_base(a, tau) + off[jj];
-#pragma unroll
-        for (int v = 0; v < N; ++v) dst[PREF ? jj : 0][v] = __ldcs(src + v * a.pw_p);
+    auto stage_a = [&](int tau, int slot) {
+        if ((int)threadIdx.x < S * NK * D) {
+            const int s = threadIdx.x / (NK * D), kap = (threadIdx.x / D) % NK, d = threadIdx.x % D;
+            double2 e = make_double2(1.0, 0.0);
+            for (int g = 1; g < a.G; ++g)
+                e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
+            sEhi[slot][s][kap][d] = e;
+        }
+        if ((int)threadIdx.x == BLOCK - 1) {
+            long long b = 0;
+            for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+            sBase[slot] = b;
+            sLast[slot] = a.last_div > 0 ? (tau / a.last_div) % N : 0;
+        }
     };
-    int tau = blockIdx.x;
-    if (PREF && tau < a.n_tiles) {
+    auto stage_b = [&](int aslot, int kslot) {
+        for (int j = threadIdx.x; j < NKU; j += BLOCK) {
+            const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
+                      s = j / (N * N * Q * NK);
+            const int c = class_of(M, LAT, nw / M, nw % M);
+            const double2 e = KI[s][kap][rr][nw][last];
+            KU[kslot][s][kap][rr][nw][last] = c > 0 ? cmul(e, sEhi[aslot][s][kap][c - 1]) : e;
+        }
+    };
+    if (t_begin < t_end) stage_a(t_begin, 0);
+    if (t_begin + 1 < t_end) stage_a(t_begin + 1, 1);
+    __syncthreads();
+    if (t_begin < t_end) stage_b(0, 0);
+    __syncthreads();
+    // register prefetch: the loads of tile i+1 are in flight while tile i is computed
+    double2 xn[N];
+    if (valid && t_begin < t_end) {
 #pragma unroll
-        for (int j = 0; j < F; ++j)
-            if (valid[j]) load(tau, xn, j);
+        for (int v = 0; v < N; ++v) xn[v] = __ldcs(a.A + sBase[0] + off_ld + v * a.pw_in[0]);
     }
-    for (; tau < a.n_tiles; tau += gridDim.x) {
-        if (PREF) {
+    for (int tau = t_begin, it = 0; tau < t_end; ++tau, ++it) {
+        const int buf = it % 3, abuf = it % 4;
+        double2 xf[N];
 #pragma unroll
-            for (int j = 0; j < F; ++j)
+        for (int v = 0; v < N; ++v) xf[v] = xn[v];
+        if (tau + 1 < t_end) stage_b((it + 1) % 4, (it + 1) % 3);
+        if (tau + 2 < t_end) stage_a(tau + 2, (it + 2) % 4);
+        __syncthreads();
+        if (valid && tau + 1 < t_end) {
 #pragma unroll
-                for (int v = 0; v < N; ++v) x[j][v] = xn[PREF ? j : 0][v];
-            const int tn = tau + gridDim.x;
-            if (tn < a.n_tiles) {
+            for (int v = 0; v < N; ++v) xn[v] = __ldcs(a.A + sBase[(it + 1) % 4] + off_ld + v * a.pw_in[0]);
+        }
+        const long long base = sBase[abuf];
+        const int last0 = lo.y >= 0 ? lo.y : sLast[abuf];
 #pragma unroll
-                for (int j = 0; j < F; ++j)
-                    if (valid[j]) load(tn, xn, j);
-            }
-        } else {
-            const long long b0 = tile_base(a, tau);
+        for (int s = 0; s < S; ++s) {
+            if (s > 0) {  // re-distribute the super-fibres: fibres along digit s-1 -> along digit s
+                if (valid) {
 #pragma unroll
-            for (int j = 0; j < F; ++j)
-                if (valid[j]) {
-                    const double2 *src = a.A + b0 + off[j];
-#pragma unroll
-                    for (int v = 0; v < N; ++v) x[j][v] = __ldcs(src + v * a.pw_p);
+                    for (int v = 0; v < N; ++v) xch[fib_elem<N, S>(s - 1, r, v) * TILE + t] = xf[v];
                 }
-        }
-        const long long base = tile_base(a, tau);
-        // tile-uniform factors: product of the group tables g >= 1
-        double2 Et[NK][D];
+                __syncthreads();
+                if (valid) {
 #pragma unroll
-        for (int kap = 0; kap < NK; ++kap)
+                    for (int v = 0; v < N; ++v) xf[v] = xch[fib_elem<N, S>(s, r, v) * TILE + t];
+                }
+                __syncthreads();
+            }
+            if (!valid) continue;
+            const bool ro = RO && a.rho[s] != nullptr;
+            const int last = s == 0 ? last0 : fib_digit<N, S>(s, r, s - 1);  // warp-uniform for s > 0
+            const double2(&ku)[NK][Q][N][N] = KU[buf][s];
+            // per-fibre outer group-0 factor of class d, kind kap
+            auto e0 = [&](int kap, int d) { return __ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t]); };
+            // moments m_d = sum_old beta_d(old) x(old) for both kinds, S0 = sum_old x(old)
+            double2 S0, m[NK][D];
+            if constexpr (SYM) {
+                // M = 2 with s = (+s, -s): beta_1 = (c, rho, 1/rho, conj c), beta_2 = 1/beta_1, so with
+                // u = x00 + x11, w = x00 - x11, p = x01 + x10, q = x01 - x10:
+                //   m_{1,2} = [Re c u + ch p] +- [i Im c w + sh q],  ch/sh = (rho +- 1/rho)/2
+                const double2 u = cadd(xf[0], xf[3]), w = make_double2(xf[0].x - xf[3].x, xf[0].y - xf[3].y);
+                const double2 p = cadd(xf[1], xf[2]), q = make_double2(xf[1].x - xf[2].x, xf[1].y - xf[2].y);
+                S0 = cadd(u, p);
 #pragma unroll
-            for (int d = 0; d < D; ++d) Et[kap][d] = make_double2(1.0, 0.0);
-        for (int g = 1; g < a.G; ++g) {
-            const int idx = (tau / a.gdiv[g]) % a.gmod[g];
+                for (int kap = 0; kap < NK; ++kap) {
+                    if (kap == 1 && !ro) break;
+                    const double cr = a.sym[s][kap][0], ci = a.sym[s][kap][1], ch = a.sym[s][kap][2], sh = a.sym[s][kap][3];
+                    const double2 A = make_double2(fma(cr, u.x, ch * p.x), fma(cr, u.y, ch * p.y));
+                    const double2 Bv = make_double2(fma(-ci, w.y, sh * q.x), fma(ci, w.x, sh * q.y));
+                    m[kap][0] = cadd(A, Bv);
+                    m[kap][D - 1] = make_double2(A.x - Bv.x, A.y - Bv.y);
+                }
+            } else {
+                S0 = xf[0];
 #pragma unroll
-            for (int kap = 0; kap < NK; ++kap)
+                for (int v = 1; v < N; ++v) S0 = cadd(S0, xf[v]);
 #pragma unroll
-                for (int d = 0; d < D; ++d)
-                    Et[kap][d] = cmul(Et[kap][d], __ldg(&a.Etab[((size_t)(kap * a.G + g) * D + d) * a.X + idx]));
-        }
-        const int last_t = a.last_div > 0 ? (tau / a.last_div) % N : 0;
+                for (int kap = 0; kap < NK; ++kap) {
+                    if (kap == 1 && !ro) break;
 #pragma unroll
-        for (int j = 0; j < F; ++j) {
-            if (!valid[j]) continue;
-            const int fl = threadIdx.x + j * BLOCK;
-            const int last = lastlo[j] >= 0 ? lastlo[j] : last_t;
-            double2 S0 = x[j][0];
+                    for (int d = 0; d < D; ++d) {
+                        double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
 #pragma unroll
-            for (int v = 1; v < N; ++v) S0 = cadd(S0, x[j][v]);
+                        for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                        m[kap][d] = mm;
+                    }
+                }
+            }
+            if (ro) {  // rho(t_{k+s}) from the pre-step values, off-diagonal rows (terminal classes)
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    const double2 pt = cmul(e0(NK - 1, d), m[NK - 1][d]);
+#pragma unroll
+                    for (int aa = 0; aa < M; ++aa)
+#pragma unroll
+                        for (int bb = 0; bb < M; ++bb)
+                            if (class_of(M, LAT, aa, bb) == d + 1)
+                                accR[RO ? s : 0][RO ? aa * M + bb : 0] =
+                                    cfma(ku[NK - 1][r][aa * M + bb][last], pt, accR[RO ? s : 0][RO ? aa * M + bb : 0]);
+                }
+            }
             double2 P[D];
 #pragma unroll
-            for (int d = 0; d < D; ++d) {
-                double2 s = cmul(sB[0][d][0], x[j][0]);
-#pragma unroll
-                for (int v = 1; v < N; ++v) s = cfma(sB[0][d][v], x[j][v], s);
-                const double2 e = cmul(Et[0][d], __ldg(&a.Etab[(size_t)d * a.X + fl]));
-                P[d] = cmul(e, s);
-            }
-            double2 *dst = a.A + base + off[j];
+            for (int d = 0; d < D; ++d) P[d] = cmul(e0(0, d), m[0][d]);
 #pragma unroll
             for (int aa = 0; aa < M; ++aa)
 #pragma unroll
                 for (int bb = 0; bb < M; ++bb) {
                     const int nw = aa * M + bb;
                     const int c = class_of(M, LAT, aa, bb);
-                    const double2 o = cmul(sK[0][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
-                    __stcs(dst + nw * a.pw_p, o);
-                    if (RO && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
+                    xf[nw] = cmul(ku[0][r][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
+                    if (ro && c == 0)  // diagonal rows of rho: the propagated value itself
+                        accR[RO ? s : 0][RO ? nw : 0] = cadd(accR[RO ? s : 0][RO ? nw : 0], xf[nw]);
                 }
-            if (RO) {
+        }
+        if (valid) {
 #pragma unroll
-                for (int d = 0; d < D; ++d) {
-                    double2 s = cmul(sB[1][d][0], x[j][0]);
-#pragma unroll
-                    for (int v = 1; v < N; ++v) s = cfma(sB[1][d][v], x[j][v], s);
-                    const double2 e =
-                        cmul(Et[NK - 1][d], __ldg(&a.Etab[((size_t)(1 * a.G + 0) * D + d) * a.X + fl]));
-                    P[d] = cmul(e, s);
-                }
-#pragma unroll
-                for (int aa = 0; aa < M; ++aa)
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const int nw = aa * M + bb;
-                        const int c = class_of(M, LAT, aa, bb);
-                        if (c != 0) acc[RO ? nw : 0] = cfma(sK[1][nw][last], P[c > 0 ? c - 1 : 0], acc[RO ? nw : 0]);
-                    }
-            }
+            for (int v = 0; v < N; ++v) __stcs(a.A + base + off_st + v * a.pw_in[S - 1], xf[v]);
         }
     }
-    if constexpr (RO) reduce_finalize<N, BLOCK>(acc, a.partials, a.rho, a.counter);
-}
-
-// --------------------------------------------------------------------------------------------
-// TMA-staged slide step.  Persistent CTAs stream tiles through an S-stage shared-memory ring:
-// thread 0 issues 1-D bulk copies (cp.async.bulk, TMA engine) global -> smem completing on a
-// per-stage mbarrier, all threads compute their fibres in smem and overwrite them in place, and
-// thread 0 writes the stage back with a bulk smem -> global copy.  Up to S-1 tiles of loads are in
-// flight per CTA independently of the register budget.  Tile = N segments of T contiguous entries
-// (contracted digit p above the tile digits) or one contiguous block of N*T entries (p below).
-// --------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred P;\n WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-        " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int NPEND> __device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NPEND) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-template <int N>
-__device__ __forceinline__ void tma_load_tile(const SlideArgs &a, double2 *stage, int tau, uint64_t *bar) {
-    const long long base = tile_base(a, tau);
-    const unsigned seg = (unsigned)a.T * 16u;
-    mbar_expect_tx(bar, seg * N);
-    if (a.p_ge_v) {
+    if constexpr (RO) {
 #pragma unroll
-        for (int v = 0; v < N; ++v) bulk_g2s(stage + v * a.T, a.A + base + v * a.pw_p, seg, bar);
-    } else {
-        bulk_g2s(stage, a.A + base, seg * N, bar);
+        for (int s = 0; s < S; ++s)
+            if (a.rho[s] != nullptr)
+                reduce_finalize<N, BLOCK>(accR[RO ? s : 0], a.partials + (size_t)s * kPartialsMax * N, a.rho[s],
+                                          a.counter + s);
     }
 }
 
-template <int N>
-__device__ __forceinline__ void tma_store_tile(const SlideArgs &a, const double2 *stage, int tau) {
-    const long long base = tile_base(a, tau);
-    const unsigned seg = (unsigned)a.T * 16u;
-    if (a.p_ge_v) {
-#pragma unroll
-        for (int v = 0; v < N; ++v) bulk_s2g(a.A + base + v * a.pw_p, stage + v * a.T, seg);
-    } else {
-        bulk_s2g(a.A + base, stage, seg * N);
-    }
-    bulk_commit();
-}
-
-template <int M, bool LAT, int BLOCK, int F, int S, bool RO>
-__global__ void __launch_bounds__(BLOCK, 1) k_slide_tma(const __grid_constant__ SlideArgs a) {
+// --------------------------------------------------------------------------------------------
+// Register variant of the fused slide kernel: one thread per outer fibre holds its whole
+// super-fibre (N^S entries) in registers, so the S sub-steps need no exchange and no barrier;
+// 16 independent 16-byte loads per thread (M = 2, S = 2) keep HBM busy.  Same tables, tile
+// pipeline and arithmetic as k_fused; readout accumulators live in shared memory.
+// --------------------------------------------------------------------------------------------
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool RO>
+__global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__ FusedArgs a) {
     constexpr int N = M * M;
     constexpr int D = n_classes(M, LAT);
+    constexpr int Q = cpow(N, S - 1);    // fibres per super-fibre and sub-step
+    constexpr int NS = Q * N;
     constexpr int NK = RO ? 2 : 1;
+    static_assert(!SYM || (M == 2 && D == 2), "symmetric moments are the M = 2 s = (+s,-s) case");
     const SmallLayout lay{N, D, 0};
-    extern __shared__ __align__(128) double2 ring[];  // [S][N*T]
     __shared__ double2 sK[2][N][N];
-    __shared__ double2 sB[2][D][N];
-    __shared__ __align__(8) uint64_t full[S];
+    __shared__ double2 sIn[S][S][2][D][N];
+    extern __shared__ double2 dyn_smem[];  // readout accumulators [S][N][BLOCK] (RO only)
+    auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
-    for (int i = threadIdx.x; i < 2 * D * N; i += BLOCK) (&sB[0][0][0])[i] = a.small[lay.beta(a.variant, 0) + i];
-    const int stage_elems = N * a.T;
-    // my tiles: tau_i = blockIdx.x + i * gridDim.x, i < n_my
-    const int n_my = a.n_tiles > (int)blockIdx.x ? (a.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int i = 0; i < S - 1 && i < n_my; ++i)
-            tma_load_tile<N>(a, ring + (size_t)i * stage_elems, blockIdx.x + i * gridDim.x, &full[i]);
-    }
-    int off[F], lastlo[F];
-    bool valid[F];
-#pragma unroll
-    for (int j = 0; j < F; ++j) {
-        const int fl = threadIdx.x + j * BLOCK;
-        valid[j] = fl < a.T;
-        const int2 o = valid[j] ? a.lofs[fl] : make_int2(0, 0);
-        off[j] = o.x;
-        lastlo[j] = o.y;
-    }
-    const int sstride = a.p_ge_v ? a.T : (int)a.pw_p;  // smem distance between the N values of a fibre
-    double2 acc[RO ? N : 1];
-#pragma unroll
-    for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
-    __syncthreads();
+    for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
+    if constexpr (RO)
+        for (int s = 0; s < S; ++s)
+            for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
 
-    for (int i = 0; i < n_my; ++i) {
-        const int st = i % S;
-        const int tau = blockIdx.x + i * gridDim.x;
-        double2 *stage = ring + (size_t)st * stage_elems;
-        double2 Et[NK][D];
+    const int t = threadIdx.x;
+    const bool valid = t < a.T;
+    const int2 lo = valid ? a.lofs[t] : make_int2(0, 0);
+    const int per = a.n_tiles / (int)gridDim.x, rem = a.n_tiles % (int)gridDim.x;
+    const int t_begin = (int)blockIdx.x * per + min((int)blockIdx.x, rem);
+    const int t_end = t_begin + per + ((int)blockIdx.x < rem ? 1 : 0);
+    constexpr int NKU = S * NK * Q * N * N;
+    __shared__ double2 KI[S][NK][Q][N][N];
+    __shared__ double2 KU[3][S][NK][Q][N][N];
+    __shared__ double2 sEhi[4][S][NK][D];
+    __shared__ long long sBase[4];
+    __shared__ int sLast[4];
+    __syncthreads();
+    for (int j = threadIdx.x; j < NKU; j += BLOCK) {
+        const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
+                  s = j / (N * N * Q * NK);
+        const int c = class_of(M, LAT, nw / M, nw % M);
+        double2 e = sK[kap][nw][last];
+        if (c > 0)
+            for (int i = 0; i < S; ++i)
+                if (i != s) e = cmul(e, sIn[s][i][kap][c - 1][fib_digit<N, S>(s, rr, i)]);
+        KI[s][kap][rr][nw][last] = e;
+    }
+    auto stage_a = [&](int tau, int slot) {
+        if ((int)threadIdx.x < S * NK * D) {
+            const int s = threadIdx.x / (NK * D), kap = (threadIdx.x / D) % NK, d = threadIdx.x % D;
+            double2 e = make_double2(1.0, 0.0);
+            for (int g = 1; g < a.G; ++g)
+                e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
+            sEhi[slot][s][kap][d] = e;
+        }
+        if ((int)threadIdx.x == BLOCK - 1) {
+            long long b = 0;
+            for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+            sBase[slot] = b;
+            sLast[slot] = a.last_div > 0 ? (tau / a.last_div) % N : 0;
+        }
+    };
+    auto stage_b = [&](int aslot, int kslot) {
+        for (int j = threadIdx.x; j < NKU; j += BLOCK) {
+            const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
+                      s = j / (N * N * Q * NK);
+            const int c = class_of(M, LAT, nw / M, nw % M);
+            const double2 e = KI[s][kap][rr][nw][last];
+            KU[kslot][s][kap][rr][nw][last] = c > 0 ? cmul(e, sEhi[aslot][s][kap][c - 1]) : e;
+        }
+    };
+    if (t_begin < t_end) stage_a(t_begin, 0);
+    if (t_begin + 1 < t_end) stage_a(t_begin + 1, 1);
+    __syncthreads();
+    if (t_begin < t_end) stage_b(0, 0);
+    for (int tau = t_begin, it = 0; tau < t_end; ++tau, ++it) {
+        const int buf = it % 3, abuf = it % 4;
+        if (tau + 1 < t_end) stage_b((it + 1) % 4, (it + 1) % 3);
+        if (tau + 2 < t_end) stage_a(tau + 2, (it + 2) % 4);
+        __syncthreads();
+        if (!valid) continue;
+        const long long base = sBase[abuf] + lo.x;
+        double2 x[NS];
 #pragma unroll
-        for (int kap = 0; kap < NK; ++kap)
+        for (int e = 0; e < NS; ++e) {
+            long long o = base;
 #pragma unroll
-            for (int d = 0; d < D; ++d) Et[kap][d] = make_double2(1.0, 0.0);
-        for (int g = 1; g < a.G; ++g) {
-            const int idx = (tau / a.gdiv[g]) % a.gmod[g];
+            for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
+            x[e] = __ldcs(a.A + o);
+        }
+        const int last0 = lo.y >= 0 ? lo.y : sLast[abuf];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const bool ro = RO && a.rho[s] != nullptr;
+            double2 E0[NK][D];  // per-fibre outer group-0 factor (same for every fibre of this thread)
 #pragma unroll
             for (int kap = 0; kap < NK; ++kap)
 #pragma unroll
                 for (int d = 0; d < D; ++d)
-                    Et[kap][d] = cmul(Et[kap][d], __ldg(&a.Etab[((size_t)(kap * a.G + g) * D + d) * a.X + idx]));
-        }
-        const int last_t = a.last_div > 0 ? (tau / a.last_div) % N : 0;
-        mbar_wait(&full[st], (unsigned)(i / S) & 1u);
+                    E0[kap][d] = (kap == 0 || ro) ? __ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t])
+                                                  : make_double2(0.0, 0.0);
+            double2 acc[RO ? N : 1];
 #pragma unroll
-        for (int j = 0; j < F; ++j) {
-            if (!valid[j]) continue;
-            const int fl = threadIdx.x + j * BLOCK;
-            const int last = lastlo[j] >= 0 ? lastlo[j] : last_t;
-            double2 *xp = stage + off[j];
-            double2 x[N];
+            for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int v = 0; v < N; ++v) x[v] = xp[v * sstride];
-            double2 S0 = x[0];
+            for (int r = 0; r < Q; ++r) {
+                double2 xf[N];
 #pragma unroll
-            for (int v = 1; v < N; ++v) S0 = cadd(S0, x[v]);
-            double2 P[D];
+                for (int v = 0; v < N; ++v) xf[v] = x[fib_elem<N, S>(s, r, v)];
+                const int last = s == 0 ? last0 : fib_digit<N, S>(s, r, s - 1);
+                const double2(&ku)[NK][Q][N][N] = KU[buf][s];
+                double2 S0, m[NK][D];
+                if constexpr (SYM) {
+                    const double2 u = cadd(xf[0], xf[3]), w = make_double2(xf[0].x - xf[3].x, xf[0].y - xf[3].y);
+                    const double2 p = cadd(xf[1], xf[2]), q = make_double2(xf[1].x - xf[2].x, xf[1].y - xf[2].y);
+                    S0 = cadd(u, p);
 #pragma unroll
-            for (int d = 0; d < D; ++d) {
-                double2 sacc = cmul(sB[0][d][0], x[0]);
+                    for (int kap = 0; kap < NK; ++kap) {
+                        if (kap == 1 && !ro) break;
+                        const double cr = a.sym[s][kap][0], ci = a.sym[s][kap][1], ch = a.sym[s][kap][2], sh = a.sym[s][kap][3];
+                        const double2 A = make_double2(fma(cr, u.x, ch * p.x), fma(cr, u.y, ch * p.y));
+                        const double2 Bv = make_double2(fma(-ci, w.y, sh * q.x), fma(ci, w.x, sh * q.y));
+                        m[kap][0] = cadd(A, Bv);
+                        m[kap][D - 1] = make_double2(A.x - Bv.x, A.y - Bv.y);
+                    }
+                } else {
+                    S0 = xf[0];
 #pragma unroll
-                for (int v = 1; v < N; ++v) sacc = cfma(sB[0][d][v], x[v], sacc);
-                P[d] = cmul(cmul(Et[0][d], __ldg(&a.Etab[(size_t)d * a.X + fl])), sacc);
-            }
+                    for (int v = 1; v < N; ++v) S0 = cadd(S0, xf[v]);
 #pragma unroll
-            for (int aa = 0; aa < M; ++aa)
+                    for (int kap = 0; kap < NK; ++kap) {
+                        if (kap == 1 && !ro) break;
 #pragma unroll
-                for (int bb = 0; bb < M; ++bb) {
-                    const int nw = aa * M + bb;
-                    const int c = class_of(M, LAT, aa, bb);
-                    const double2 o = cmul(sK[0][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
-                    xp[nw * sstride] = o;
-                    if (RO && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
+                        for (int d = 0; d < D; ++d) {
+                            double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
+#pragma unroll
+                            for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                            m[kap][d] = mm;
+                        }
+                    }
                 }
-            if (RO) {
+                if (ro) {
 #pragma unroll
-                for (int d = 0; d < D; ++d) {
-                    double2 sacc = cmul(sB[1][d][0], x[0]);
+                    for (int d = 0; d < D; ++d) {
+                        const double2 pt = cmul(E0[NK - 1][d], m[NK - 1][d]);
 #pragma unroll
-                    for (int v = 1; v < N; ++v) sacc = cfma(sB[1][d][v], x[v], sacc);
-                    P[d] = cmul(cmul(Et[NK - 1][d], __ldg(&a.Etab[((size_t)(1 * a.G + 0) * D + d) * a.X + fl])), sacc);
+                        for (int aa = 0; aa < M; ++aa)
+#pragma unroll
+                            for (int bb = 0; bb < M; ++bb)
+                                if (class_of(M, LAT, aa, bb) == d + 1)
+                                    acc[RO ? aa * M + bb : 0] = cfma(ku[NK - 1][r][aa * M + bb][last], pt, acc[RO ? aa * M + bb : 0]);
+                    }
                 }
+                double2 P[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) P[d] = cmul(E0[0][d], m[0][d]);
 #pragma unroll
                 for (int aa = 0; aa < M; ++aa)
 #pragma unroll
                     for (int bb = 0; bb < M; ++bb) {
                         const int nw = aa * M + bb;
                         const int c = class_of(M, LAT, aa, bb);
-                        if (c != 0) acc[RO ? nw : 0] = cfma(sK[1][nw][last], P[c > 0 ? c - 1 : 0], acc[RO ? nw : 0]);
+                        const double2 o = cmul(ku[0][r][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
+                        x[fib_elem<N, S>(s, r, nw)] = o;
+                        if (ro && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
                     }
             }
-        }
-        fence_async_smem();  // make this thread's smem writes visible to the TMA (async proxy)
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            tma_store_tile<N>(a, stage, tau);
-            // refill the stage of tile i-1 (its store was the previous bulk group) with tile i-1+S
-            if (i + S - 1 < n_my) {
-                const int rs = (i + S - 1) % S;
-                if (i >= 1) bulk_wait_read<1>();
-                tma_load_tile<N>(a, ring + (size_t)rs * stage_elems, blockIdx.x + (i + S - 1) * gridDim.x, &full[rs]);
+            if (ro) {
+#pragma unroll
+                for (int n = 0; n < N; ++n)
+                    accS[RO ? s : 0][RO ? n : 0][RO ? t : 0] = cadd(accS[RO ? s : 0][RO ? n : 0][RO ? t : 0], acc[RO ? n : 0]);
             }
         }
+#pragma unroll
+        for (int e = 0; e < NS; ++e) {
+            long long o = base;
+#pragma unroll
+            for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
+            __stcs(a.A + o, x[e]);
+        }
     }
-    if (threadIdx.x == 0) bulk_wait_all();
-    if constexpr (RO) reduce_finalize<N, BLOCK>(acc, a.partials, a.rho, a.counter);
+    if constexpr (RO) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (a.rho[s] != nullptr) {
+                double2 tt[N];
+#pragma unroll
+                for (int n = 0; n < N; ++n) tt[n] = accS[RO ? s : 0][RO ? n : 0][RO ? t : 0];
+                reduce_finalize<N, BLOCK>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s);
+            }
+    }
 }
 
 // --------------------------------------------------------------------------------------------
@@ -471,121 +590,138 @@ __global__ void __launch_bounds__(256) k_grow(const __grid_constant__ GrowArgs a
 }
 
 // --------------------------------------------------------------------------------------------
-// Slide-kernel variants (tile shape and pipelining); the plan picks one per M (env override
-// QUAPI_SLIDE_VARIANT=<id> for tuning).  v = tile digits (T = N^v), w = hi-group digits.
+// Launch configuration per M (FusedShape in qp_internal.h) and dispatch.
 // --------------------------------------------------------------------------------------------
-// Variant registry.  R(id, M, block, F, v, w, minBlocks, prefetch): register-path k_slide;
-// T(id, M, block, F, v, w, stages): TMA-staged k_slide_tma (smem = stages * N^(v+1) * 16 B).
-#define QP_REG_VARIANTS(R)              \
-    R(0, 2, 256, 4, 5, 6, 1, false)     \
-    R(1, 2, 256, 1, 4, 6, 3, false)     \
-    R(2, 2, 256, 1, 4, 6, 2, true)      \
-    R(3, 2, 128, 2, 4, 6, 4, false)     \
-    R(10, 3, 384, 2, 3, 3, 1, false)    \
-    R(11, 3, 768, 1, 3, 3, 1, false)    \
-    R(12, 3, 768, 1, 3, 3, 1, true)     \
-    R(20, 4, 256, 1, 2, 3, 2, false)
-#define QP_TMA_VARIANTS(T)              \
-    T(5, 2, 256, 1, 4, 6, 4)            \
-    T(6, 2, 256, 1, 4, 6, 3)            \
-    T(7, 2, 256, 4, 5, 6, 3)            \
-    T(8, 2, 128, 2, 4, 6, 4)            \
-    T(13, 3, 256, 3, 3, 3, 2)           \
-    T(14, 3, 384, 2, 3, 3, 2)
+// (M, S) -> block, tile digits v (TILE = N^v outer fibres; TILE * N^(S-1) = block for S > 1), min blocks/SM
+#define QP_FUSED_CFGS(X)         \
+    X(2, 1, 256, 4, 256, 3)      \
+    X(2, 2, 256, 3, 64, 3)       \
+    X(3, 1, 736, 3, 736, 1)      \
+    X(4, 1, 256, 2, 256, 2)
+// register variant k_fused_r: (M, S, block = tile, v, min blocks)
+#define QP_FUSED_R_CFGS(X)       \
+    X(2, 2, 256, 4, 2)
 
-static const SlideVariant kVariants[] = {
-#define R(id, M, B, F, V, W, MB, PF) {id, M, B, F, V, W, MB, PF ? 1 : 0, 0},
-#define T(id, M, B, F, V, W, ST) {id, M, B, F, V, W, 1, 0, ST},
-    QP_REG_VARIANTS(R) QP_TMA_VARIANTS(T)
-#undef R
-#undef T
-};
-
-const SlideVariant *find_variant(int id) {
-    for (const auto &v : kVariants)
-        if (v.id == id) return &v;
-    return nullptr;
+FusedShape fused_shape(int M) {
+    switch (M) {
+    case 2: return FusedShape{2, 4};
+    case 3: return FusedShape{1, 3};
+    default: return FusedShape{1, 2};
+    }
 }
 
-int default_variant(int M) { return M == 2 ? 3 : (M == 3 ? 11 : 20); }
+bool has_reg_variant(int M, int S) {
+#define X(M_, S_, B, V, MB) if (M == M_ && S == S_) return true;
+    QP_FUSED_R_CFGS(X)
+#undef X
+    return false;
+}
+static bool use_reg_variant(int M, int S, int kind) { return kind == 1 && has_reg_variant(M, S); }
 
-template <int M, bool LAT, int BLOCK, int F, int MINB, bool PREF>
-static cudaError_t slide_t(const SlideArgs &a, int grid, cudaStream_t s) {
-    if (a.rho) k_slide<M, LAT, BLOCK, F, MINB, PREF, true><<<grid, BLOCK, 0, s>>>(a);
-    else k_slide<M, LAT, BLOCK, F, MINB, PREF, false><<<grid, BLOCK, 0, s>>>(a);
-    return cudaGetLastError();
+int fused_tile_digits(int M, int S, int kind) {
+    if (use_reg_variant(M, S, kind)) {
+#define X(M_, S_, B, V, MB) if (M == M_ && S == S_) return V;
+        QP_FUSED_R_CFGS(X)
+#undef X
+    }
+#define X(M_, S_, B, V, TL, MB) if (M == M_ && S == S_) return V;
+    QP_FUSED_CFGS(X)
+#undef X
+    return -1;
 }
 
-template <int M, bool LAT, int BLOCK, int F, int MINB, bool PREF>
-static int occ_t() {
-    int o1 = 0, o2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_slide<M, LAT, BLOCK, F, MINB, PREF, true>, BLOCK, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_slide<M, LAT, BLOCK, F, MINB, PREF, false>, BLOCK, 0);
-    return o1 < o2 ? o1 : o2;
+int fused_block(int M, int S, int kind) {
+    if (use_reg_variant(M, S, kind)) {
+#define X(M_, S_, B, V, MB) if (M == M_ && S == S_) return B;
+        QP_FUSED_R_CFGS(X)
+#undef X
+    }
+#define X(M_, S_, B, V, TL, MB) if (M == M_ && S == S_) return B;
+    QP_FUSED_CFGS(X)
+#undef X
+    return 0;
 }
 
-template <int M, bool LAT, int BLOCK, int F, int S>
-static size_t tma_smem(int T) { return (size_t)S * M * M * T * 16; }
+template <int M, int S, int BLOCK>
+static constexpr size_t fused_r_dyn_smem() { return (size_t)S * M * M * BLOCK * 16; }
 
-template <int M, bool LAT, int BLOCK, int F, int S>
-static cudaError_t slide_tma_t(const SlideArgs &a, int grid, cudaStream_t s) {
-    const size_t sm = tma_smem<M, LAT, BLOCK, F, S>(a.T);
-    if (a.rho) {
-        cudaFuncSetAttribute(k_slide_tma<M, LAT, BLOCK, F, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_slide_tma<M, LAT, BLOCK, F, S, true><<<grid, BLOCK, sm, s>>>(a);
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB>
+static cudaError_t fused_r_t(const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    constexpr size_t dyn = fused_r_dyn_smem<M, S, BLOCK>();
+    if (ro) {
+        cudaFuncSetAttribute(k_fused_r<M, LAT, SYM, S, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        k_fused_r<M, LAT, SYM, S, BLOCK, MINB, true><<<grid, BLOCK, dyn, s>>>(a);
     } else {
-        cudaFuncSetAttribute(k_slide_tma<M, LAT, BLOCK, F, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_slide_tma<M, LAT, BLOCK, F, S, false><<<grid, BLOCK, sm, s>>>(a);
+        k_fused_r<M, LAT, SYM, S, BLOCK, MINB, false><<<grid, BLOCK, 0, s>>>(a);
     }
     return cudaGetLastError();
 }
 
-template <int M, bool LAT, int BLOCK, int F, int S>
-static int occ_tma_t(int T) {
-    const size_t sm = tma_smem<M, LAT, BLOCK, F, S>(T);
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB>
+static int fused_r_occ_t() {
+    constexpr size_t dyn = fused_r_dyn_smem<M, S, BLOCK>();
     int o1 = 0, o2 = 0;
-    cudaFuncSetAttribute(k_slide_tma<M, LAT, BLOCK, F, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_slide_tma<M, LAT, BLOCK, F, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_slide_tma<M, LAT, BLOCK, F, S, true>, BLOCK, sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_slide_tma<M, LAT, BLOCK, F, S, false>, BLOCK, sm);
+    cudaFuncSetAttribute(k_fused_r<M, LAT, SYM, S, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused_r<M, LAT, SYM, S, BLOCK, MINB, true>, BLOCK, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused_r<M, LAT, SYM, S, BLOCK, MINB, false>, BLOCK, 0);
     return o1 < o2 ? o1 : o2;
 }
 
-// M = 2: the lattice and general class maps are the same set of classes; the host uses LAT = false.
-cudaError_t launch_slide(int variant, bool lattice, const SlideArgs &a, int grid, cudaStream_t s) {
-#define R(id, M, B, F, V, W, MB, PF)                                               \
-    if (variant == id) {                                                            \
-        if (M > 2 && lattice) return slide_t<M, (M > 2), B, F, MB, PF>(a, grid, s); \
-        return slide_t<M, false, B, F, MB, PF>(a, grid, s);                         \
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int TILE, int MINB>
+static cudaError_t fused_t(const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    if (ro) k_fused<M, LAT, SYM, S, BLOCK, TILE, MINB, true><<<grid, BLOCK, 0, s>>>(a);
+    else k_fused<M, LAT, SYM, S, BLOCK, TILE, MINB, false><<<grid, BLOCK, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int TILE, int MINB>
+static int fused_occ_t() {
+    int o1 = 0, o2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused<M, LAT, SYM, S, BLOCK, TILE, MINB, true>, BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused<M, LAT, SYM, S, BLOCK, TILE, MINB, false>, BLOCK, 0);
+    return o1 < o2 ? o1 : o2;
+}
+
+// M = 2: the lattice and general class maps give the same classes; the host uses LAT = false.
+cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    if (use_reg_variant(M, S, kind)) {
+#define X(M_, S_, B, V, MB)                                                                        \
+        if (M == M_ && S == S_) {                                                                  \
+            if (M_ == 2 && sym) return fused_r_t<M_, false, (M_ == 2), S_, B, MB>(a, ro, grid, s);  \
+            return fused_r_t<M_, false, false, S_, B, MB>(a, ro, grid, s);                          \
+        }
+        QP_FUSED_R_CFGS(X)
+#undef X
     }
-#define T(id, M, B, F, V, W, ST)                                                   \
-    if (variant == id) {                                                            \
-        if (M > 2 && lattice) return slide_tma_t<M, (M > 2), B, F, ST>(a, grid, s); \
-        return slide_tma_t<M, false, B, F, ST>(a, grid, s);                         \
+#define X(M_, S_, B, V, TL, MB)                                                                   \
+    if (M == M_ && S == S_) {                                                                     \
+        if (M_ == 2 && sym) return fused_t<M_, false, (M_ == 2), S_, B, TL, MB>(a, ro, grid, s);   \
+        if (M_ > 2 && lattice) return fused_t<M_, (M_ > 2), false, S_, B, TL, MB>(a, ro, grid, s); \
+        return fused_t<M_, false, false, S_, B, TL, MB>(a, ro, grid, s);                           \
     }
-    QP_REG_VARIANTS(R)
-    QP_TMA_VARIANTS(T)
-#undef R
-#undef T
+    QP_FUSED_CFGS(X)
+#undef X
     return cudaErrorInvalidValue;
 }
 
-int slide_occupancy(int variant, bool lattice, int T) {
-#define R(id, M, B, F, V, W, MB, PF)                                   \
-    if (variant == id) {                                                \
-        if (M > 2 && lattice) return occ_t<M, (M > 2), B, F, MB, PF>(); \
-        return occ_t<M, false, B, F, MB, PF>();                         \
+int fused_occupancy(int M, bool lattice, bool sym, int kind, int S) {
+    if (use_reg_variant(M, S, kind)) {
+#define X(M_, S_, B, V, MB)                                                             \
+        if (M == M_ && S == S_) {                                                       \
+            if (M_ == 2 && sym) return fused_r_occ_t<M_, false, (M_ == 2), S_, B, MB>();  \
+            return fused_r_occ_t<M_, false, false, S_, B, MB>();                          \
+        }
+        QP_FUSED_R_CFGS(X)
+#undef X
     }
-#define T(id, M, B, F, V, W, ST)                                           \
-    if (variant == id) {                                                    \
-        if (M > 2 && lattice) return occ_tma_t<M, (M > 2), B, F, ST>(T_); \
-        return occ_tma_t<M, false, B, F, ST>(T_);                          \
+#define X(M_, S_, B, V, TL, MB)                                                         \
+    if (M == M_ && S == S_) {                                                           \
+        if (M_ == 2 && sym) return fused_occ_t<M_, false, (M_ == 2), S_, B, TL, MB>();   \
+        if (M_ > 2 && lattice) return fused_occ_t<M_, (M_ > 2), false, S_, B, TL, MB>(); \
+        return fused_occ_t<M_, false, false, S_, B, TL, MB>();                           \
     }
-    const int T_ = T;
-    QP_REG_VARIANTS(R)
-    QP_TMA_VARIANTS(T)
-#undef R
-#undef T
+    QP_FUSED_CFGS(X)
+#undef X
     return 0;
 }
 

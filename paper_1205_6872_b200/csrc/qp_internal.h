@@ -37,28 +37,39 @@ struct SmallLayout {
     __host__ __device__ int total() const { return 2 * N * N + 4 * D * N + 2 * L * L * N; }
 };
 
-// Per-launch arguments of the slide step (k >= L).  All tables are device pointers into d_work.
-struct SlideArgs {
+constexpr int kMaxS = 4;  // max steps fused into one launch (FusedArgs arrays)
+
+// Per-launch arguments of the fused slide kernel: steps k..k+S-1 (k >= L) on the super-fibres of
+// inner slots p0..p0+S-1 (mod L).  All tables are device pointers into d_work.
+struct FusedArgs {
     double2 *A;              // ARDM, N^L entries, in place
-    const double2 *small;    // SmallLayout block
-    const double2 *Etab;     // E tables for this p: [kappa][g][d][X]
-    const int2 *lofs;        // [T]: x = in-tile element offset of fibre f_local, y = 'last' digit or -1
-    double2 *partials;       // [grid][N] readout block partials
-    double2 *rho;            // [N] readout destination, nullptr => no readout this step
-    unsigned *counter;       // last-block-done counter (reset by the last block)
-    long long pw_p;          // N^p: stride of the contracted digit
-    long long pw_p1;         // N^(p+1)
-    long long tile_stride;   // p <  v: N^(v+1) elements per tile
-    int n_tiles;             // N^(L-1-v)
-    int T;                   // fibres per tile = N^v
-    int p_ge_v;              // 1 if every tile digit lies below p
-    int Qlo;                 // p >= v: N^(p-v) tiles share one hi block
-    int G;                   // number of digit groups (group 0 = tile-local digits)
+    const double2 *small;    // SmallLayout block (K', beta)
+    const double2 *inner;    // [S][S][2][D][N]: inner-slot factors per sub-step
+    const double2 *Etab;     // [S][2][G][D][X]: outer digit-group factor tables per sub-step
+    const long long *goff;   // [G][X]: address offset of outer digit group g >= 1
+    const int2 *lofs;        // [T]: x = address offset of tile-local fibre t, y = 'last' digit of sub-step 0 or -1
+    double2 *partials;       // [kMaxS][kPartialsMax][N] readout block partials
+    unsigned *counter;       // [kMaxS] last-block-done counters
+    double2 *rho[kMaxS];     // readout destination per sub-step, nullptr => none
+    long long pw_in[kMaxS];  // N^(slot of inner digit i)
+    int n_tiles;             // N^(L-S-v)
+    int T;                   // outer fibres per tile = N^v (<= block)
+    int G;                   // digit groups (group 0 = tile-local)
     int X;                   // entries per group table (padded)
     int gdiv[kMaxGroups];    // group g >= 1: index = (tau / gdiv[g]) % gmod[g]
     int gmod[kMaxGroups];
-    int last_div;            // 'last' digit is a tile digit: (tau / last_div) % N; else -1
-    int variant;             // 0 steady (k > L), 1 first slide (k == L)
+    int last_div;            // sub-step 0 'last' digit is a tile digit: (tau / last_div) % N; else -1
+    // beta_d(old) = exp(delta_d psi_L(old)) of each sub-step (kernel-parameter constant bank):
+    // [sub-step][0 propagate / 1 terminal][class][old]; the first slide step k == L uses the
+    // initial-edge classes (partner sigma_0)
+    double2 beta[kMaxS][2][kMaxD][kMaxN];
+    // M = 2, s = (+s, -s): beta_1 = (c, rho, 1/rho, conj c); {Re c, Im c, (rho+1/rho)/2, (rho-1/rho)/2}
+    double sym[kMaxS][2][4];
+};
+
+// Fused-kernel shape for one M: max fused steps and outer digit-group size w.
+struct FusedShape {
+    int S, w;
 };
 
 // Per-launch arguments of the growth step k (1 <= k < L): A_{k-1} (N^k) -> A_k (N^(k+1)).
@@ -74,15 +85,14 @@ struct GrowArgs {
     double delta[kMaxD];     // Delta s of each class (index d-1)
 };
 
-// Slide-kernel variant: launch shape and pipelining (kernels.cu registry).
-struct SlideVariant {
-    int id, M, block, F, v, w, minb, prefetch, stages;  // stages > 0 => TMA-staged kernel
-};
-const SlideVariant *find_variant(int id);
-int default_variant(int M);
+FusedShape fused_shape(int M);
+// kind: 0 = warp-mapped k_fused, 1 = register k_fused_r (where a config exists for (M, S))
+bool has_reg_variant(int M, int S);
+int fused_tile_digits(int M, int S, int kind);  // v: T = N^v outer fibres per tile
+int fused_block(int M, int S, int kind);
 // Launchers (kernels.cu).  Return cudaError_t of the launch.
-cudaError_t launch_slide(int variant, bool lattice, const SlideArgs &a, int grid, cudaStream_t s);
-int slide_occupancy(int variant, bool lattice, int T);  // resident CTAs per SM (needs a device)
+cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool readout, int grid, cudaStream_t s);
+int fused_occupancy(int M, bool lattice, bool sym, int kind, int S);  // resident CTAs per SM (needs a device)
 cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaStream_t s);
 
 }  // namespace qp

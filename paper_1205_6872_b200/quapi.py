@@ -60,7 +60,7 @@ class qp_sizes(ctypes.Structure):
         ("pmc_bytes", ctypes.c_double), ("n_out", ctypes.c_int64), ("n_steps", ctypes.c_int64),
         ("bytes_per_step", ctypes.c_int64), ("lattice", ctypes.c_int32), ("n_classes", ctypes.c_int32),
         ("grid", ctypes.c_int32), ("block", ctypes.c_int32), ("tile_fibres", ctypes.c_int32),
-        ("setup_seconds", ctypes.c_double), ("init_h2d_bytes", ctypes.c_int64),
+        ("setup_seconds", ctypes.c_double), ("init_h2d_bytes", ctypes.c_int64), ("fuse_steps", ctypes.c_int32),
     ]
 
 
@@ -143,6 +143,7 @@ class Sizes:
     tile_fibres: int
     setup_seconds: float
     init_h2d_bytes: int
+    fuse_steps: int
 
 
 class Plan:

@@ -178,14 +178,36 @@ def test_sigma_x_symmetry_full_size():
     assert np.abs(b - X @ a @ X).max() < 1e-12
 
 
-@pytest.mark.parametrize("variant,M,L,n", [(0, 2, 7, 20), (1, 2, 7, 20), (2, 2, 7, 20), (3, 2, 7, 20),
-                                           (2, 2, 3, 9), (5, 2, 7, 20), (6, 2, 8, 21), (7, 2, 8, 21), (8, 2, 7, 20),
-                                           (5, 2, 3, 9), (7, 2, 3, 9), (10, 3, 5, 12), (11, 3, 5, 12), (12, 3, 5, 12),
-                                           (13, 3, 5, 12), (14, 3, 5, 12), (20, 4, 4, 8)])
-def test_every_slide_variant(variant, M, L, n, monkeypatch):
-    """Each tile shape / pipelining variant of k_slide against the oracle."""
-    monkeypatch.setenv("QUAPI_SLIDE_VARIANT", str(variant))
+@pytest.mark.parametrize("kind", ["reg", "warp"])
+@pytest.mark.parametrize("nosym", [False, True])
+@pytest.mark.parametrize("fuse", [1, 2])
+@pytest.mark.parametrize("M,L,n", [(2, 2, 9), (2, 3, 12), (2, 5, 17), (2, 7, 20), (2, 8, 23), (3, 4, 11), (4, 3, 8)])
+def test_fusion_depths(fuse, M, L, n, nosym, kind, monkeypatch):
+    """k_fused with 1 and 2 time steps per HBM pass (QUAPI_FUSE_S caps the depth) against the oracle;
+    odd n and L exercise partial groups and super-fibres that wrap around the ring.  For M = 2 with
+    s = (+1, -1) the symmetric-moment kernel runs unless QUAPI_NO_SYM is set."""
+    if nosym and M != 2:
+        pytest.skip("symmetric moments are M = 2 only")
+    monkeypatch.setenv("QUAPI_FUSE_S", str(fuse))
+    monkeypatch.setenv("QUAPI_FUSED_KIND", kind)
+    if nosym:
+        monkeypatch.setenv("QUAPI_NO_SYM", "1")
     for lat in (True, False) if M > 2 else (True,):
-        w = W.random_problem(300 + variant, M, L, n, kind=W.J_DEBYE, lattice_s=lat)
+        w = W.random_problem(300 + 10 * M + L, M, L, n, kind=W.J_DEBYE, lattice_s=lat)
         rg, plan, _ = gpu_run(w)
+        assert plan.sizes.fuse_steps == (min(fuse, L - 1) if M == 2 else 1)
         check(rg, O.run(P(w)))
+
+
+def test_fusion_grouping_independent_of_segments():
+    """Fusion groups are aligned on k - L, so splitting qp_steps at group boundaries is bit-identical."""
+    w = W.CONFIGS[2].with_(L=6, n_steps=31)
+    whole, _, _ = gpu_run(w)
+    plan = Q.Plan(w)
+    ardm, work = plan.alloc()
+    plan.init(ardm, work)
+    f = plan.sizes.fuse_steps
+    cuts = [1, 6, 6 + f, 6 + 3 * f, 6 + 5 * f, 32]
+    for k0, k1 in zip(cuts[:-1], cuts[1:]):
+        plan.steps(k0, k1, ardm, work)
+    assert np.array_equal(plan.read_rho(work), whole)
