@@ -335,9 +335,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
 
 // --------------------------------------------------------------------------------------------
 // Register variant of the fused slide kernel: one thread per outer fibre holds its whole
-// super-fibre (N^S entries) in registers, so the S sub-steps need no exchange and no barrier;
-// 16 independent 16-byte loads per thread (M = 2, S = 2) keep HBM busy.  Same tables, tile
-// pipeline and arithmetic as k_fused; readout accumulators live in shared memory.
+// super-fibre (N^S entries) in registers, so the S sub-steps need no exchange; 16 independent
+// 16-byte loads per thread (M = 2, S = 2) keep HBM busy.  Warps are independent: each warp owns
+// a contiguous, static range of tiles (T = N^v outer fibres), builds the tile's factor table KU
+// in its own shared-memory slice (warp-synchronous, no CTA barrier in the main loop) and sweeps
+// the tile in chunks of 32 outer fibres, lane = outer fibre.  Readout accumulators live in
+// shared memory; the CTA reduction at the end is in fixed order (deterministic).
 // --------------------------------------------------------------------------------------------
 template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool RO>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__ FusedArgs a) {
@@ -346,6 +349,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
     constexpr int Q = cpow(N, S - 1);    // fibres per super-fibre and sub-step
     constexpr int NS = Q * N;
     constexpr int NK = RO ? 2 : 1;
+    constexpr int W = BLOCK / 32;
     static_assert(!SYM || (M == 2 && D == 2), "symmetric moments are the M = 2 s = (+s,-s) case");
     const SmallLayout lay{N, D, 0};
     __shared__ double2 sK[2][N][N];
@@ -358,18 +362,20 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
         for (int s = 0; s < S; ++s)
             for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
 
-    const int t = threadIdx.x;
-    const bool valid = t < a.T;
-    const int2 lo = valid ? a.lofs[t] : make_int2(0, 0);
-    const int per = a.n_tiles / (int)gridDim.x, rem = a.n_tiles % (int)gridDim.x;
-    const int t_begin = (int)blockIdx.x * per + min((int)blockIdx.x, rem);
-    const int t_end = t_begin + per + ((int)blockIdx.x < rem ? 1 : 0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // contiguous, static tile range per warp (deterministic readout order)
+    const int gw = (int)blockIdx.x * W + warp, nw_tot = (int)gridDim.x * W;
+    const int per = a.n_tiles / nw_tot, rem = a.n_tiles % nw_tot;
+    const int t_begin = gw * per + min(gw, rem);
+    const int t_end = t_begin + per + (gw < rem ? 1 : 0);
     constexpr int NKU = S * NK * Q * N * N;
+    // KI (tile independent, per CTA): K'_kap(new, last) * prod_{i != s} inner_i(class(new), digit_i(r))
     __shared__ double2 KI[S][NK][Q][N][N];
-    __shared__ double2 KU[3][S][NK][Q][N][N];
-    __shared__ double2 sEhi[4][S][NK][D];
-    __shared__ long long sBase[4];
-    __shared__ int sLast[4];
+    // per warp: KU = KI * Ehi(tile) and the tile's base offset / 'last' digit
+    __shared__ double2 KU[W][S][NK][Q][N][N];
+    __shared__ double2 sEhi[W][S][NK][D];
+    __shared__ long long sBase[W];
+    __shared__ int sLast[W];
     __syncthreads();
     for (int j = threadIdx.x; j < NKU; j += BLOCK) {
         const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
@@ -381,139 +387,142 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
                 if (i != s) e = cmul(e, sIn[s][i][kap][c - 1][fib_digit<N, S>(s, rr, i)]);
         KI[s][kap][rr][nw][last] = e;
     }
-    auto stage_a = [&](int tau, int slot) {
-        if ((int)threadIdx.x < S * NK * D) {
-            const int s = threadIdx.x / (NK * D), kap = (threadIdx.x / D) % NK, d = threadIdx.x % D;
+    __syncthreads();
+    const double2(&ki)[S][NK][Q][N][N] = KI;
+    double2(&ku_w)[S][NK][Q][N][N] = KU[warp];
+    for (int tau = t_begin; tau < t_end; ++tau) {
+        // warp-synchronous tile setup
+        if (lane < S * NK * D) {
+            const int s = lane / (NK * D), kap = (lane / D) % NK, d = lane % D;
             double2 e = make_double2(1.0, 0.0);
             for (int g = 1; g < a.G; ++g)
                 e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
-            sEhi[slot][s][kap][d] = e;
+            sEhi[warp][s][kap][d] = e;
         }
-        if ((int)threadIdx.x == BLOCK - 1) {
+        if (lane == 31) {
             long long b = 0;
             for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
-            sBase[slot] = b;
-            sLast[slot] = a.last_div > 0 ? (tau / a.last_div) % N : 0;
+            sBase[warp] = b;
+            sLast[warp] = a.last_div > 0 ? (tau / a.last_div) % N : 0;
         }
-    };
-    auto stage_b = [&](int aslot, int kslot) {
-        for (int j = threadIdx.x; j < NKU; j += BLOCK) {
+        __syncwarp();
+        for (int j = lane; j < NKU; j += 32) {
             const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
                       s = j / (N * N * Q * NK);
             const int c = class_of(M, LAT, nw / M, nw % M);
-            const double2 e = KI[s][kap][rr][nw][last];
-            KU[kslot][s][kap][rr][nw][last] = c > 0 ? cmul(e, sEhi[aslot][s][kap][c - 1]) : e;
+            const double2 e = ki[s][kap][rr][nw][last];
+            ku_w[s][kap][rr][nw][last] = c > 0 ? cmul(e, sEhi[warp][s][kap][c - 1]) : e;
         }
-    };
-    if (t_begin < t_end) stage_a(t_begin, 0);
-    if (t_begin + 1 < t_end) stage_a(t_begin + 1, 1);
-    __syncthreads();
-    if (t_begin < t_end) stage_b(0, 0);
-    for (int tau = t_begin, it = 0; tau < t_end; ++tau, ++it) {
-        const int buf = it % 3, abuf = it % 4;
-        if (tau + 1 < t_end) stage_b((it + 1) % 4, (it + 1) % 3);
-        if (tau + 2 < t_end) stage_a(tau + 2, (it + 2) % 4);
-        __syncthreads();
-        if (!valid) continue;
-        const long long base = sBase[abuf] + lo.x;
-        double2 x[NS];
+        __syncwarp();
+        const long long tbase = sBase[warp];
+        const int last_t = sLast[warp];
+        for (int t = lane; t < ((a.T + 31) & ~31); t += 32) {
+            if (t >= a.T) continue;
+            const int2 lo = __ldg(&a.lofs[t]);
+            const long long base = tbase + lo.x;
+            double2 x[NS];
 #pragma unroll
-        for (int e = 0; e < NS; ++e) {
-            long long o = base;
+            for (int e = 0; e < NS; ++e) {
+                long long o = base;
 #pragma unroll
-            for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
-            x[e] = __ldcs(a.A + o);
-        }
-        const int last0 = lo.y >= 0 ? lo.y : sLast[abuf];
+                for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
+                x[e] = __ldcs(a.A + o);
+            }
+            const int last0 = lo.y >= 0 ? lo.y : last_t;
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const bool ro = RO && a.rho[s] != nullptr;
-            double2 E0[NK][D];  // per-fibre outer group-0 factor (same for every fibre of this thread)
+            for (int s = 0; s < S; ++s) {
+                const bool ro = RO && a.rho[s] != nullptr;
+                double2 E0[NK][D];  // outer group-0 factor of this outer fibre
 #pragma unroll
-            for (int kap = 0; kap < NK; ++kap)
+                for (int kap = 0; kap < NK; ++kap)
 #pragma unroll
-                for (int d = 0; d < D; ++d)
-                    E0[kap][d] = (kap == 0 || ro) ? __ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t])
-                                                  : make_double2(0.0, 0.0);
-            double2 acc[RO ? N : 1];
+                    for (int d = 0; d < D; ++d)
+                        E0[kap][d] = (kap == 0 || ro) ? __ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t])
+                                                      : make_double2(0.0, 0.0);
+                double2 acc[RO ? N : 1];
 #pragma unroll
-            for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
+                for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int r = 0; r < Q; ++r) {
-                double2 xf[N];
+                for (int r = 0; r < Q; ++r) {
+                    double2 xf[N];
 #pragma unroll
-                for (int v = 0; v < N; ++v) xf[v] = x[fib_elem<N, S>(s, r, v)];
-                const int last = s == 0 ? last0 : fib_digit<N, S>(s, r, s - 1);
-                const double2(&ku)[NK][Q][N][N] = KU[buf][s];
-                double2 S0, m[NK][D];
-                if constexpr (SYM) {
-                    const double2 u = cadd(xf[0], xf[3]), w = make_double2(xf[0].x - xf[3].x, xf[0].y - xf[3].y);
-                    const double2 p = cadd(xf[1], xf[2]), q = make_double2(xf[1].x - xf[2].x, xf[1].y - xf[2].y);
-                    S0 = cadd(u, p);
+                    for (int v = 0; v < N; ++v) xf[v] = x[fib_elem<N, S>(s, r, v)];
+                    const int last = s == 0 ? last0 : fib_digit<N, S>(s, r, s - 1);
+                    const double2(&ku)[NK][Q][N][N] = ku_w[s];
+                    double2 S0, m[NK][D];
+                    if constexpr (SYM) {
+                        const double2 u = cadd(xf[0], xf[3]), w = make_double2(xf[0].x - xf[3].x, xf[0].y - xf[3].y);
+                        const double2 p = cadd(xf[1], xf[2]), q = make_double2(xf[1].x - xf[2].x, xf[1].y - xf[2].y);
+                        S0 = cadd(u, p);
 #pragma unroll
-                    for (int kap = 0; kap < NK; ++kap) {
-                        if (kap == 1 && !ro) break;
-                        const double cr = a.sym[s][kap][0], ci = a.sym[s][kap][1], ch = a.sym[s][kap][2], sh = a.sym[s][kap][3];
-                        const double2 A = make_double2(fma(cr, u.x, ch * p.x), fma(cr, u.y, ch * p.y));
-                        const double2 Bv = make_double2(fma(-ci, w.y, sh * q.x), fma(ci, w.x, sh * q.y));
-                        m[kap][0] = cadd(A, Bv);
-                        m[kap][D - 1] = make_double2(A.x - Bv.x, A.y - Bv.y);
-                    }
-                } else {
-                    S0 = xf[0];
+                        for (int kap = 0; kap < NK; ++kap) {
+                            if (kap == 1 && !ro) break;
+                            const double cr = a.sym[s][kap][0], ci = a.sym[s][kap][1], ch = a.sym[s][kap][2],
+                                         sh = a.sym[s][kap][3];
+                            const double2 A = make_double2(fma(cr, u.x, ch * p.x), fma(cr, u.y, ch * p.y));
+                            const double2 Bv = make_double2(fma(-ci, w.y, sh * q.x), fma(ci, w.x, sh * q.y));
+                            m[kap][0] = cadd(A, Bv);
+                            m[kap][D - 1] = make_double2(A.x - Bv.x, A.y - Bv.y);
+                        }
+                    } else {
+                        S0 = xf[0];
 #pragma unroll
-                    for (int v = 1; v < N; ++v) S0 = cadd(S0, xf[v]);
+                        for (int v = 1; v < N; ++v) S0 = cadd(S0, xf[v]);
 #pragma unroll
-                    for (int kap = 0; kap < NK; ++kap) {
-                        if (kap == 1 && !ro) break;
+                        for (int kap = 0; kap < NK; ++kap) {
+                            if (kap == 1 && !ro) break;
 #pragma unroll
-                        for (int d = 0; d < D; ++d) {
-                            double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
+                            for (int d = 0; d < D; ++d) {
+                                double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
 #pragma unroll
-                            for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
-                            m[kap][d] = mm;
+                                for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                                m[kap][d] = mm;
+                            }
                         }
                     }
+                    if (ro) {
+#pragma unroll
+                        for (int d = 0; d < D; ++d) {
+                            const double2 pt = cmul(E0[NK - 1][d], m[NK - 1][d]);
+#pragma unroll
+                            for (int aa = 0; aa < M; ++aa)
+#pragma unroll
+                                for (int bb = 0; bb < M; ++bb)
+                                    if (class_of(M, LAT, aa, bb) == d + 1)
+                                        acc[RO ? aa * M + bb : 0] =
+                                            cfma(ku[NK - 1][r][aa * M + bb][last], pt, acc[RO ? aa * M + bb : 0]);
+                        }
+                    }
+                    double2 P[D];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) P[d] = cmul(E0[0][d], m[0][d]);
+#pragma unroll
+                    for (int aa = 0; aa < M; ++aa)
+#pragma unroll
+                        for (int bb = 0; bb < M; ++bb) {
+                            const int nw = aa * M + bb;
+                            const int c = class_of(M, LAT, aa, bb);
+                            const double2 o = cmul(ku[0][r][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
+                            x[fib_elem<N, S>(s, r, nw)] = o;
+                            if (ro && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
+                        }
                 }
                 if (ro) {
 #pragma unroll
-                    for (int d = 0; d < D; ++d) {
-                        const double2 pt = cmul(E0[NK - 1][d], m[NK - 1][d]);
-#pragma unroll
-                        for (int aa = 0; aa < M; ++aa)
-#pragma unroll
-                            for (int bb = 0; bb < M; ++bb)
-                                if (class_of(M, LAT, aa, bb) == d + 1)
-                                    acc[RO ? aa * M + bb : 0] = cfma(ku[NK - 1][r][aa * M + bb][last], pt, acc[RO ? aa * M + bb : 0]);
-                    }
+                    for (int n = 0; n < N; ++n)
+                        accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0] =
+                            cadd(accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0], acc[RO ? n : 0]);
                 }
-                double2 P[D];
-#pragma unroll
-                for (int d = 0; d < D; ++d) P[d] = cmul(E0[0][d], m[0][d]);
-#pragma unroll
-                for (int aa = 0; aa < M; ++aa)
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const int nw = aa * M + bb;
-                        const int c = class_of(M, LAT, aa, bb);
-                        const double2 o = cmul(ku[0][r][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
-                        x[fib_elem<N, S>(s, r, nw)] = o;
-                        if (ro && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
-                    }
             }
-            if (ro) {
 #pragma unroll
-                for (int n = 0; n < N; ++n)
-                    accS[RO ? s : 0][RO ? n : 0][RO ? t : 0] = cadd(accS[RO ? s : 0][RO ? n : 0][RO ? t : 0], acc[RO ? n : 0]);
+            for (int e = 0; e < NS; ++e) {
+                long long o = base;
+#pragma unroll
+                for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
+                __stcs(a.A + o, x[e]);
             }
         }
-#pragma unroll
-        for (int e = 0; e < NS; ++e) {
-            long long o = base;
-#pragma unroll
-            for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
-            __stcs(a.A + o, x[e]);
-        }
+        __syncwarp();  // KU / sEhi of this warp are rewritten for the next tile
     }
     if constexpr (RO) {
 #pragma unroll
@@ -521,7 +530,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
             if (a.rho[s] != nullptr) {
                 double2 tt[N];
 #pragma unroll
-                for (int n = 0; n < N; ++n) tt[n] = accS[RO ? s : 0][RO ? n : 0][RO ? t : 0];
+                for (int n = 0; n < N; ++n) tt[n] = accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0];
                 reduce_finalize<N, BLOCK>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s);
             }
     }

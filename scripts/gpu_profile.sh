@@ -7,7 +7,7 @@ tail -3 gpurun_out/bench.err
 cat gpurun_out/bench.json
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 60 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_fused -s 2 -c ${NCU_COUNT:-4} -o gpurun_out/prof -f \
-    python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_fused -s 2 -c ${NCU_COUNT:-3} -o gpurun_out/prof -f \
+    python bench.py --steps 20 --warmup 4 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/ncu_full.log
 ls -la gpurun_out
