@@ -363,11 +363,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
             for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // contiguous, static tile range per warp (deterministic readout order)
+    // work unit = (tile, chunk of 32 outer fibres); contiguous, static unit range per warp
+    // (deterministic readout order); the warp rebuilds its tile tables when the tile changes
+    const int CH = (a.T + 31) >> 5;
+    const long long n_units = (long long)a.n_tiles * CH;
     const int gw = (int)blockIdx.x * W + warp, nw_tot = (int)gridDim.x * W;
-    const int per = a.n_tiles / nw_tot, rem = a.n_tiles % nw_tot;
-    const int t_begin = gw * per + min(gw, rem);
-    const int t_end = t_begin + per + (gw < rem ? 1 : 0);
+    const long long per = n_units / nw_tot, rem = n_units % nw_tot;
+    const long long u_begin = gw * per + min((long long)gw, rem);
+    const long long u_end = u_begin + per + (gw < rem ? 1 : 0);
     constexpr int NKU = S * NK * Q * N * N;
     // KI (tile independent, per CTA): K'_kap(new, last) * prod_{i != s} inner_i(class(new), digit_i(r))
     __shared__ double2 KI[S][NK][Q][N][N];
@@ -390,33 +393,40 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
     __syncthreads();
     const double2(&ki)[S][NK][Q][N][N] = KI;
     double2(&ku_w)[S][NK][Q][N][N] = KU[warp];
-    for (int tau = t_begin; tau < t_end; ++tau) {
-        // warp-synchronous tile setup
-        if (lane < S * NK * D) {
-            const int s = lane / (NK * D), kap = (lane / D) % NK, d = lane % D;
-            double2 e = make_double2(1.0, 0.0);
-            for (int g = 1; g < a.G; ++g)
-                e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
-            sEhi[warp][s][kap][d] = e;
+    int cur_tile = -1;
+    long long tbase = 0;
+    int last_t = 0;
+    for (long long u = u_begin; u < u_end; ++u) {
+        const int tau = (int)(u / CH), t = (int)(u % CH) * 32 + lane;
+        if (tau != cur_tile) {  // warp-synchronous tile setup
+            __syncwarp();       // previous tile's KU no longer in use
+            cur_tile = tau;
+            if (lane < S * NK * D) {
+                const int s = lane / (NK * D), kap = (lane / D) % NK, d = lane % D;
+                double2 e = make_double2(1.0, 0.0);
+                for (int g = 1; g < a.G; ++g)
+                    e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
+                sEhi[warp][s][kap][d] = e;
+            }
+            if (lane == 31) {
+                long long b = 0;
+                for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+                sBase[warp] = b;
+                sLast[warp] = a.last_div > 0 ? (tau / a.last_div) % N : 0;
+            }
+            __syncwarp();
+            for (int j = lane; j < NKU; j += 32) {
+                const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
+                          s = j / (N * N * Q * NK);
+                const int c = class_of(M, LAT, nw / M, nw % M);
+                const double2 e = ki[s][kap][rr][nw][last];
+                ku_w[s][kap][rr][nw][last] = c > 0 ? cmul(e, sEhi[warp][s][kap][c - 1]) : e;
+            }
+            __syncwarp();
+            tbase = sBase[warp];
+            last_t = sLast[warp];
         }
-        if (lane == 31) {
-            long long b = 0;
-            for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
-            sBase[warp] = b;
-            sLast[warp] = a.last_div > 0 ? (tau / a.last_div) % N : 0;
-        }
-        __syncwarp();
-        for (int j = lane; j < NKU; j += 32) {
-            const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
-                      s = j / (N * N * Q * NK);
-            const int c = class_of(M, LAT, nw / M, nw % M);
-            const double2 e = ki[s][kap][rr][nw][last];
-            ku_w[s][kap][rr][nw][last] = c > 0 ? cmul(e, sEhi[warp][s][kap][c - 1]) : e;
-        }
-        __syncwarp();
-        const long long tbase = sBase[warp];
-        const int last_t = sLast[warp];
-        for (int t = lane; t < ((a.T + 31) & ~31); t += 32) {
+        {
             if (t >= a.T) continue;
             const int2 lo = __ldg(&a.lofs[t]);
             const long long base = tbase + lo.x;
@@ -522,7 +532,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
                 __stcs(a.A + o, x[e]);
             }
         }
-        __syncwarp();  // KU / sEhi of this warp are rewritten for the next tile
     }
     if constexpr (RO) {
 #pragma unroll
@@ -607,9 +616,11 @@ __global__ void __launch_bounds__(256) k_grow(const __grid_constant__ GrowArgs a
     X(2, 2, 256, 3, 64, 3)       \
     X(3, 1, 736, 3, 736, 1)      \
     X(4, 1, 256, 2, 256, 2)
-// register variant k_fused_r: (M, S, block = tile, v, min blocks)
+// register variant k_fused_r: (M, S, block, v, min blocks)
 #define QP_FUSED_R_CFGS(X)       \
-    X(2, 2, 256, 4, 2)
+    X(2, 1, 256, 4, 2)           \
+    X(2, 2, 256, 4, 2)           \
+    X(3, 1, 256, 3, 2)
 
 FusedShape fused_shape(int M) {
     switch (M) {
@@ -697,6 +708,7 @@ cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const F
 #define X(M_, S_, B, V, MB)                                                                        \
         if (M == M_ && S == S_) {                                                                  \
             if (M_ == 2 && sym) return fused_r_t<M_, false, (M_ == 2), S_, B, MB>(a, ro, grid, s);  \
+            if (M_ > 2 && lattice) return fused_r_t<M_, (M_ > 2), false, S_, B, MB>(a, ro, grid, s); \
             return fused_r_t<M_, false, false, S_, B, MB>(a, ro, grid, s);                          \
         }
         QP_FUSED_R_CFGS(X)
@@ -718,6 +730,7 @@ int fused_occupancy(int M, bool lattice, bool sym, int kind, int S) {
 #define X(M_, S_, B, V, MB)                                                             \
         if (M == M_ && S == S_) {                                                       \
             if (M_ == 2 && sym) return fused_r_occ_t<M_, false, (M_ == 2), S_, B, MB>();  \
+            if (M_ > 2 && lattice) return fused_r_occ_t<M_, (M_ > 2), false, S_, B, MB>(); \
             return fused_r_occ_t<M_, false, false, S_, B, MB>();                          \
         }
         QP_FUSED_R_CFGS(X)
