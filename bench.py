@@ -141,6 +141,11 @@ def main():
     ap.add_argument("--cfg", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo stages the all-to-all through host memory; tests only)")
+    ap.add_argument("--mode", default="shard", choices=["shard", "replica"],
+                    help="N > 1: shard one ARDM over the ranks (strong scaling, NCCL all-to-all re-shard) "
+                         "or run independent replicas (weak scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -157,11 +162,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.dist_backend)
+    local = local % max(1, torch.cuda.device_count())  # several ranks per GPU only for gloo tests
     torch.cuda.set_device(local)
     B.build()
 
     base = W.CONFIGS[args.cfg]
+    if world > 1 and args.mode == "shard":
+        return bench_sharded(args, base, world, rank, local)
     K, Wm, L = args.steps, max(args.warmup, 3), base.L
     n_total = L - 1 + Wm + K  # growth steps, then W warm-up and K timed slide steps
     w = base.with_(n_steps=n_total)
@@ -229,7 +237,8 @@ def main():
         step_equiv = 32 * sz.ardm_entries * (K / (ms / 1e3)) / 1e9  # north_star's 2*16*N^L B per step
         line = {
             "metric": METRIC, "value": steps_per_s, "unit": "steps/s", "n_gpus": world, "steps": K,
-            "warmup": Wm, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+            "warmup": Wm, "ms_per_step": ms_max / K, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": base.name, "ardm_entries": sz.ardm_entries, "ardm_bytes": sz.ardm_bytes,
                        "readout": "every step (allPoints), fused", "l2": "inputs larger than L2 (4.3 GB ARDM)",
@@ -254,6 +263,87 @@ def main():
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def bench_sharded(args, base, world, rank, local):
+    """N > 1, one ARDM sharded over the ranks: K slide steps including every re-shard (pack kernel,
+    NCCL all_to_all_single over NVLink, unpack kernel) inside the timed region (strong scaling)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1205_6872_b200 import sharded as SH
+    K, Wm, L = args.steps, max(args.warmup, 3), base.L
+    w = base.with_(n_steps=L - 1 + Wm + K)
+    stream = torch.cuda.current_stream()
+    me = SH.ShardRank(w, world, rank, device=f"cuda:{local}", stream=stream)
+    ex = SH.dist_exchange()
+    me.growth_and_extract()
+    SH.advance([me], L, L + Wm, ex)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        ev0.record(stream)
+        launches = SH.advance([me], L + Wm, L + Wm + K, ex)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    part = me.plan.read_rho(me.work, stream)
+    pt = torch.from_numpy(part.view(np.float64).copy()).cuda()
+    gathered = [torch.empty_like(pt) for _ in range(world)] if rank == 0 else None
+    dist.gather(pt, gathered, dst=0)
+    sz = me.plan.sizes
+    ssz = me.sizes
+    del me
+    torch.cuda.empty_cache()
+    e2e = None
+    if not args.no_e2e:  # the whole sharded public-API run of the BASELINE config, host in -> host rho
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rho_e = SH.solve_distributed(base)
+        el = time.perf_counter() - t0
+        tt = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": base.n_steps / float(tt.item()), "unit": "steps/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": int(base.N * 16 * (base.n_steps + 1) * world / base.n_steps),
+               "seconds": float(tt.item()), "steps": base.n_steps}
+        if rank == 0:
+            e2e["max_abs_trace_err"] = float(np.abs(np.einsum("kii->k", rho_e) - 1).max())
+    if rank == 0:
+        parts = [g.cpu().numpy().view(np.complex128).reshape(part.shape) for g in gathered]
+        rho = SH.combine_rho(parts, np.arange(w.n_steps + 1), L)
+        steps_per_s = K / (ms_max / 1e3)
+        peak, peak_kind = _peaks()
+        passes = K / max(1, sz.fuse_steps)
+        agg = 32 * sz.ardm_entries * passes / (ms_max / 1e3) / 1e9  # algorithmic HBM bytes of all ranks
+        line = {
+            "metric": METRIC, "value": steps_per_s, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": Wm,
+            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": base.name, "ardm_entries": sz.ardm_entries, "parallelism": f"sharded x{world}",
+                       "shard_slots": ssz.shard_slots, "segment_steps": ssz.segment_steps,
+                       "local_entries": ssz.local_entries, "exchange_entries_per_rank": ssz.exchange_entries,
+                       "readout": "every step (allPoints), fused", "l2": "inputs larger than L2",
+                       "collective": "all_to_all_single (NCCL) every segment_steps steps"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": agg, "peak": peak * world, "unit": "GB/s",
+                         "frac": agg / (peak * world), "peak_kind": peak_kind + " x n_gpus",
+                         "traffic": None, "note": "aggregate algorithmic bytes incl. re-shard time"},
+            "clocks": clk.summary(),
+            "max_abs_trace_err": float(np.abs(np.einsum("kii->k", rho) - 1).max()),
+            "e2e": e2e,
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
     return 0
 
 

@@ -135,6 +135,38 @@ qp_status qp_read_rho(const qp_plan *plan, const void *d_work, qp_c64 *rho_out, 
 /* [sync] Whole run: qp_init + qp_steps(1, n_steps+1) + qp_read_rho. */
 qp_status qp_run(qp_plan *plan, void *d_ardm, void *d_work, void *stream, qp_c64 *rho_out);
 
+/* ---------------------------------------------------------------- sharded execution (multi-GPU)
+   SURVEY §8(e): G ranks (one per GPU) each hold, during segment j, the ARDM entries whose z shard
+   ring slots Z_j (the z most recently written slots at the segment start k_j = L + j (L - z)) take
+   one of the rank's owned value combos; the L - z steps of a segment never contract a shard slot and
+   run shard-locally.  Between segments the caller re-shards: qp_shard_pack -> all-to-all (NCCL,
+   counts from qp_shard_counts, ordered by rank) -> qp_shard_unpack.  Growth (k < L) runs
+   replicated on the full ARDM before qp_shard_extract.  Readouts of slide steps are this rank's
+   partial sums (sum over ranks in rank order for rho); growth readouts are complete on every rank. */
+typedef struct {
+    int32_t n_ranks, rank;
+    int32_t shard_slots;       /* z                                                                 */
+    int32_t segment_steps;     /* L - z steps between re-shards                                     */
+    int64_t local_entries;     /* this rank's ARDM entries (n_own * N^(L-z))                        */
+    int64_t max_local_entries; /* over ranks                                                        */
+    int64_t exchange_entries;  /* entries this rank sends (and receives) per re-shard               */
+    int64_t work_bytes;        /* workspace including the shard launch tables                       */
+} qp_shard_sizes;
+
+/* Host only; call before qp_init (the workspace grows: query work_bytes again). 2 <= n_ranks. */
+qp_status qp_shard_configure(qp_plan *plan, int32_t n_ranks, int32_t rank);
+qp_status qp_shard_query(const qp_plan *plan, qp_shard_sizes *out);
+/* entries sent to / received from every rank at each re-shard: [n_ranks] each */
+qp_status qp_shard_counts(const qp_plan *plan, int64_t *send_counts, int64_t *recv_counts);
+/* After qp_init + qp_steps(1, L) on the full ARDM: copy this rank's segment-0 blocks to d_local. */
+qp_status qp_shard_extract(qp_plan *plan, const void *d_full, void *d_local, void *stream);
+/* Steps k_begin..k_end-1 inside the current segment on the local blocks (fused, readout partials). */
+qp_status qp_shard_steps(qp_plan *plan, int64_t k_begin, int64_t k_end, void *d_local, void *d_work, void *stream,
+                         int64_t *n_launch);
+/* Re-shard from segment j to j+1: pack local -> send (rank-major), unpack recv -> local (advances j). */
+qp_status qp_shard_pack(qp_plan *plan, const void *d_local, void *d_send, void *stream);
+qp_status qp_shard_unpack(qp_plan *plan, const void *d_recv, void *d_local, void *stream);
+
 const char *qp_last_error(void);
 void qp_plan_destroy(qp_plan *plan);
 /* Library build identification, e.g. "quapi 0.1 sm_100a". */

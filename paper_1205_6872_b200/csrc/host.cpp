@@ -23,6 +23,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -336,6 +338,25 @@ struct qp_plan {
     int64_t next_k = 1;
     bool inited = false;
     double setup_seconds = 0.0;
+    // ---- sharded execution (multi-GPU); see qp_shard_configure
+    struct Shard {
+        bool on = false;
+        int G = 1, rank = 0, z = 0, seg_len = 0;
+        int64_t NZ = 1, blk = 0;                     // combos per shard-slot set, entries per block
+        std::vector<int64_t> c_lo, n_own;            // owned combo range per rank
+        std::vector<LaunchSet> sets;                 // shard launch sets
+        std::map<std::tuple<int, int, int>, size_t> index;  // (zstart, p0, S) -> sets
+        int64_t seg = 0;                             // current segment
+        bool extracted = false;
+    } sh;
+    int64_t seg_begin(int64_t j) const { return L + j * sh.seg_len; }
+    std::vector<int> zset(int64_t j) const {         // shard slots of segment j, ascending
+        std::vector<int> z;
+        const int64_t k = seg_begin(j);
+        for (int i = 0; i < sh.z; ++i) z.push_back((int)(((k - 1 - i) % L + L) % L));
+        std::sort(z.begin(), z.end());
+        return z;
+    }
     int64_t slot_of(int64_t k) const {
         auto it = std::lower_bound(out_steps.begin(), out_steps.end(), k);
         return (it != out_steps.end() && *it == k) ? int64_t(it - out_steps.begin()) : -1;
@@ -401,6 +422,120 @@ qp_status compute_eta(qp_plan &P, const qp_problem &pr) {
     return QP_OK;
 }
 
+// Tables of one fused launch over inner slots p0..p0+S-1 (mod L) of a local layout from which the
+// shard slots `removed` are absent (empty for an unsharded plan).
+void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &removed, qp_plan::LaunchSet &ls) {
+    const int N = P.N, M = P.M, L = P.L, D = P.D;
+    ls.p0 = p0;
+    ls.S = S;
+    std::vector<int> inner(S), outer;
+    for (int i = 0; i < S; ++i) inner[i] = (p0 + i) % L;
+    // shard slots (removed) are not stored: the remaining slots keep their order, slot q sits at
+    // position pos[q] of the local layout (stride N^pos[q])
+    std::vector<int> pos(L, -1);
+    for (int q = 0, n = 0; q < L; ++q)
+        if (std::find(removed.begin(), removed.end(), q) == removed.end()) pos[q] = n++;
+    for (int q = 0; q < L; ++q)
+        if (pos[q] >= 0 && std::find(inner.begin(), inner.end(), q) == inner.end()) outer.push_back(q);  // ascending
+    const int nout = (int)outer.size();
+    const int v = std::min(qp::fused_tile_digits(M, S, P.kind), nout), w = std::max(1, P.shape.w);
+    const int hi = nout - v;
+    const int G = 1 + (hi + w - 1) / w;
+    const int T = (int)ipow(N, v);
+    int X = T;
+    for (int g = 1; g < G; ++g) X = std::max<int>(X, (int)ipow(N, std::min(w, hi - (g - 1) * w)));
+    auto g_first = [&](int g) { return g == 0 ? 0 : v + (g - 1) * w; };
+    auto g_size = [&](int g) { return g == 0 ? v : std::min(w, hi - (g - 1) * w); };
+    // outer digit group tables: per sub-step s, kind kap, exponent over the group's digits
+    ls.Etab.assign((size_t)S * 2 * G * D * X, make_double2(1.0, 0.0));
+    for (int st = 0; st < S; ++st)
+        for (int g = 0; g < G; ++g) {
+            const int i0 = g_first(g), nd = g_size(g);
+            for (int x = 0; x < (int)ipow(N, nd); ++x) {
+                cd Ps[2] = {0.0, 0.0};
+                int r = x;
+                for (int t = 0; t < nd; ++t) {
+                    const int dig = r % N;
+                    r /= N;
+                    const int lag = ((p0 + st - outer[i0 + t]) % L + L) % L;  // 1..L-1
+                    Ps[0] += psi(P, dig, P.eta[lag]);  // propagate: partner interior
+                    Ps[1] += psi(P, dig, P.E[lag]);    // terminal (readout) edge class
+                }
+                for (int kap = 0; kap < 2; ++kap)
+                    for (int d = 0; d < D; ++d)
+                        ls.Etab[((((size_t)st * 2 + kap) * G + g) * D + d) * X + x] = d2(std::exp(P.delta[d] * Ps[kap]));
+            }
+        }
+    // inner-slot factors: sub-step st, inner digit i != st (new value if i < st, old if i > st)
+    ls.inner.assign((size_t)S * S * 2 * D * N, make_double2(1.0, 0.0));
+    for (int st = 0; st < S; ++st)
+        for (int i = 0; i < S; ++i) {
+            if (i == st) continue;
+            const int lag = i < st ? st - i : L - (i - st);
+            for (int kap = 0; kap < 2; ++kap)
+                for (int d = 0; d < D; ++d)
+                    for (int sg = 0; sg < N; ++sg)
+                        ls.inner[((((size_t)st * S + i) * 2 + kap) * D + d) * N + sg] =
+                            d2(std::exp(P.delta[d] * psi(P, sg, kap == 0 ? P.eta[lag] : P.E[lag])));
+        }
+    // address offsets of the outer digit groups g >= 1 and of the tile-local fibres
+    ls.goff.assign((size_t)G * X, 0);
+    for (int g = 1; g < G; ++g) {
+        const int i0 = g_first(g), nd = g_size(g);
+        for (int x = 0; x < (int)ipow(N, nd); ++x) {
+            long long o = 0;
+            int r = x;
+            for (int t = 0; t < nd; ++t) { o += (long long)(r % N) * ipow(N, pos[outer[i0 + t]]); r /= N; }
+            ls.goff[(size_t)g * X + x] = o;
+        }
+    }
+    const int qlast = (p0 - 1 + L) % L;  // sub-step 0's 'last' point sigma_{k-1}
+    const int ilast = (int)(std::find(outer.begin(), outer.end(), qlast) - outer.begin());
+    ls.lofs.assign(T, make_int2(0, -1));
+    for (int fl = 0; fl < T; ++fl) {
+        long long o = 0;
+        int r = fl;
+        for (int t = 0; t < v; ++t) { o += (long long)(r % N) * ipow(N, pos[outer[t]]); r /= N; }
+        const int lastd = ilast < v ? (int)((fl / ipow(N, ilast)) % N) : -1;
+        ls.lofs[fl] = make_int2((int)o, lastd);
+    }
+    qp::FusedArgs &a = ls.args;
+    for (int i = 0; i < S; ++i) a.pw_in[i] = ipow(N, pos[inner[i]]);
+    a.n_tiles = (int)ipow(N, hi);
+    a.T = T;
+    a.G = G;
+    a.X = X;
+    for (int g = 1; g < G; ++g) {
+        a.gdiv[g] = (int)ipow(N, (g - 1) * w);
+        a.gmod[g] = (int)ipow(N, g_size(g));
+    }
+    a.last_div = (ilast >= v && ilast < nout) ? (int)ipow(N, ilast - v) : -1;
+    a.fixed_last = -1;  // set per launch when sub-step 0's 'last' slot is a shard slot
+    for (int st = 0; st < qp::kMaxS; ++st)
+        for (int kap = 0; kap < 2; ++kap)
+            for (int d = 0; d < qp::kMaxD; ++d) a.fixfac[st][kap][d] = make_double2(1.0, 0.0);
+
+}
+
+void compute_layout(qp_plan &P) {
+    const int N = P.N;
+    size_t off = 0;
+    P.off_small = off; off = align256(off + P.small.size() * sizeof(double2));
+    auto place = [&](qp_plan::LaunchSet &ls) {
+        ls.off_inner = off; off = align256(off + ls.inner.size() * sizeof(double2));
+        ls.off_E = off;     off = align256(off + ls.Etab.size() * sizeof(double2));
+        ls.off_goff = off;  off = align256(off + ls.goff.size() * sizeof(long long));
+        ls.off_lofs = off;  off = align256(off + ls.lofs.size() * sizeof(int2));
+    };
+    for (auto &ls : P.sets) place(ls);
+    for (auto &ls : P.sh.sets) place(ls);
+    P.tables_end = off;
+    P.off_part = off;  off = align256(off + (size_t)qp::kMaxS * qp::kPartialsMax * N * sizeof(double2));
+    P.off_rho = off;   off = align256(off + std::max<size_t>(1, P.out_steps.size()) * N * sizeof(double2));
+    P.off_cnt = off;   off = align256(off + 256);
+    P.work_bytes = off;
+}
+
 void build_tables(qp_plan &P) {
     const int N = P.N, M = P.M, L = P.L, D = P.D;
     // ---- K and self-factor-weighted K'
@@ -443,105 +578,11 @@ void build_tables(qp_plan &P) {
     if (const char *ev = std::getenv("QUAPI_FUSE_S")) P.Smax = std::max(1, std::min(P.Smax, std::atoi(ev)));
     P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
     for (int p0 = 0; p0 < L; ++p0)
-        for (int S = 1; S <= P.Smax; ++S) {
-            qp_plan::LaunchSet &ls = P.sets[(size_t)p0 * P.Smax + (S - 1)];
-            ls.p0 = p0;
-            ls.S = S;
-            std::vector<int> inner(S), outer;
-            for (int i = 0; i < S; ++i) inner[i] = (p0 + i) % L;
-            for (int q = 0; q < L; ++q)
-                if (std::find(inner.begin(), inner.end(), q) == inner.end()) outer.push_back(q);  // ascending
-            const int nout = (int)outer.size();
-            const int v = std::min(qp::fused_tile_digits(M, S, P.kind), nout), w = std::max(1, P.shape.w);
-            const int hi = nout - v;
-            const int G = 1 + (hi + w - 1) / w;
-            const int T = (int)ipow(N, v);
-            int X = T;
-            for (int g = 1; g < G; ++g) X = std::max<int>(X, (int)ipow(N, std::min(w, hi - (g - 1) * w)));
-            auto g_first = [&](int g) { return g == 0 ? 0 : v + (g - 1) * w; };
-            auto g_size = [&](int g) { return g == 0 ? v : std::min(w, hi - (g - 1) * w); };
-            // outer digit group tables: per sub-step s, kind kap, exponent over the group's digits
-            ls.Etab.assign((size_t)S * 2 * G * D * X, make_double2(1.0, 0.0));
-            for (int st = 0; st < S; ++st)
-                for (int g = 0; g < G; ++g) {
-                    const int i0 = g_first(g), nd = g_size(g);
-                    for (int x = 0; x < (int)ipow(N, nd); ++x) {
-                        cd Ps[2] = {0.0, 0.0};
-                        int r = x;
-                        for (int t = 0; t < nd; ++t) {
-                            const int dig = r % N;
-                            r /= N;
-                            const int lag = ((p0 + st - outer[i0 + t]) % L + L) % L;  // 1..L-1
-                            Ps[0] += psi(P, dig, P.eta[lag]);  // propagate: partner interior
-                            Ps[1] += psi(P, dig, P.E[lag]);    // terminal (readout) edge class
-                        }
-                        for (int kap = 0; kap < 2; ++kap)
-                            for (int d = 0; d < D; ++d)
-                                ls.Etab[((((size_t)st * 2 + kap) * G + g) * D + d) * X + x] = d2(std::exp(P.delta[d] * Ps[kap]));
-                    }
-                }
-            // inner-slot factors: sub-step st, inner digit i != st (new value if i < st, old if i > st)
-            ls.inner.assign((size_t)S * S * 2 * D * N, make_double2(1.0, 0.0));
-            for (int st = 0; st < S; ++st)
-                for (int i = 0; i < S; ++i) {
-                    if (i == st) continue;
-                    const int lag = i < st ? st - i : L - (i - st);
-                    for (int kap = 0; kap < 2; ++kap)
-                        for (int d = 0; d < D; ++d)
-                            for (int sg = 0; sg < N; ++sg)
-                                ls.inner[((((size_t)st * S + i) * 2 + kap) * D + d) * N + sg] =
-                                    d2(std::exp(P.delta[d] * psi(P, sg, kap == 0 ? P.eta[lag] : P.E[lag])));
-                }
-            // address offsets of the outer digit groups g >= 1 and of the tile-local fibres
-            ls.goff.assign((size_t)G * X, 0);
-            for (int g = 1; g < G; ++g) {
-                const int i0 = g_first(g), nd = g_size(g);
-                for (int x = 0; x < (int)ipow(N, nd); ++x) {
-                    long long o = 0;
-                    int r = x;
-                    for (int t = 0; t < nd; ++t) { o += (long long)(r % N) * ipow(N, outer[i0 + t]); r /= N; }
-                    ls.goff[(size_t)g * X + x] = o;
-                }
-            }
-            const int qlast = (p0 - 1 + L) % L;  // sub-step 0's 'last' point sigma_{k-1}
-            const int ilast = (int)(std::find(outer.begin(), outer.end(), qlast) - outer.begin());
-            ls.lofs.assign(T, make_int2(0, -1));
-            for (int fl = 0; fl < T; ++fl) {
-                long long o = 0;
-                int r = fl;
-                for (int t = 0; t < v; ++t) { o += (long long)(r % N) * ipow(N, outer[t]); r /= N; }
-                const int lastd = ilast < v ? (int)((fl / ipow(N, ilast)) % N) : -1;
-                ls.lofs[fl] = make_int2((int)o, lastd);
-            }
-            qp::FusedArgs &a = ls.args;
-            for (int i = 0; i < S; ++i) a.pw_in[i] = ipow(N, inner[i]);
-            a.n_tiles = (int)ipow(N, hi);
-            a.T = T;
-            a.G = G;
-            a.X = X;
-            for (int g = 1; g < G; ++g) {
-                a.gdiv[g] = (int)ipow(N, (g - 1) * w);
-                a.gmod[g] = (int)ipow(N, g_size(g));
-            }
-            a.last_div = ilast >= v ? (int)ipow(N, ilast - v) : -1;
-        }
+        for (int S = 1; S <= P.Smax; ++S) build_launch_set(P, p0, S, {}, P.sets[(size_t)p0 * P.Smax + (S - 1)]);
     // ---- A_0(sigma_0) = rho0(sigma_0) I(sigma_0, sigma_0; eta_00 = G(1/2))   (Eq. 13, reading C.3-2)
     P.A0.assign(N, 0.0);
     for (int sg = 0; sg < N; ++sg) P.A0[sg] = P.rho0[sg] * std::exp(dsig(P, sg) * psi(P, sg, P.self_end));
-    // ---- workspace layout
-    size_t off = 0;
-    P.off_small = off; off = align256(off + P.small.size() * sizeof(double2));
-    for (auto &ls : P.sets) {
-        ls.off_inner = off; off = align256(off + ls.inner.size() * sizeof(double2));
-        ls.off_E = off;     off = align256(off + ls.Etab.size() * sizeof(double2));
-        ls.off_goff = off;  off = align256(off + ls.goff.size() * sizeof(long long));
-        ls.off_lofs = off;  off = align256(off + ls.lofs.size() * sizeof(int2));
-    }
-    P.tables_end = off;
-    P.off_part = off;  off = align256(off + (size_t)qp::kMaxS * qp::kPartialsMax * N * sizeof(double2));
-    P.off_rho = off;   off = align256(off + std::max<size_t>(1, P.out_steps.size()) * N * sizeof(double2));
-    P.off_cnt = off;   off = align256(off + 256);
-    P.work_bytes = off;
+    compute_layout(P);
 }
 
 qp_status validate(const qp_problem *pr) {
@@ -695,7 +736,11 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
     QP_CUDA(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
     char *w = (char *)d_work;
     QP_CUDA(cudaMemcpyAsync(w + P->off_small, P->small.data(), P->small.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
-    for (const auto &ls : P->sets) {
+    std::vector<const qp_plan::LaunchSet *> all;
+    for (const auto &ls : P->sets) all.push_back(&ls);
+    for (const auto &ls : P->sh.sets) all.push_back(&ls);
+    for (const auto *lsp : all) {
+        const auto &ls = *lsp;
         QP_CUDA(cudaMemcpyAsync(w + ls.off_inner, ls.inner.data(), ls.inner.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
         QP_CUDA(cudaMemcpyAsync(w + ls.off_E, ls.Etab.data(), ls.Etab.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
         QP_CUDA(cudaMemcpyAsync(w + ls.off_goff, ls.goff.data(), ls.goff.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
@@ -721,6 +766,8 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
         P->grid[S] = std::max(1, std::min<int>({nt, P->sms * occ, qp::kPartialsMax}));
     }
     P->next_k = 1;
+    P->sh.seg = 0;
+    P->sh.extracted = false;
     P->inited = true;
     return QP_OK;
 }
@@ -819,6 +866,279 @@ qp_status qp_run(qp_plan *P, void *d_ardm, void *d_work, void *stream, qp_c64 *r
     if ((st = qp_init(P, d_ardm, d_work, stream))) return st;
     if ((st = qp_steps(P, 1, P->n_steps + 1, d_ardm, d_work, stream, nullptr))) return st;
     return qp_read_rho(P, d_work, rho_out, stream);
+}
+
+}  // extern "C"
+
+// ===================================================================================== sharding
+// Multi-GPU execution.  G ranks each hold, for the current segment j, the ARDM
+// entries whose z shard slots Z_j = {(k_j - 1 - i) mod L, i < z} (the most recently written slots,
+// k_j = L + j (L - z)) take one of the rank's owned combos c in [c_lo, c_lo + n_own): one block of
+// N^(L-z) entries per combo, the other slots in ascending order.  The L - z steps of a segment never
+// contract a shard slot, so they run shard-locally (k_fused with the combo's fixed factors); between
+// segments the data is re-sharded on Z_{j+1} (pack -> NCCL all-to-all by the caller -> unpack).
+namespace {
+
+void shard_combo_digits(const qp_plan &P, int64_t c, int *dig) {
+    for (int i = 0; i < P.sh.z; ++i) { dig[i] = (int)(c % P.N); c /= P.N; }
+}
+
+// positions of the non-shard slots (ascending) in a segment's local layout
+std::vector<int> local_pos(const qp_plan &P, const std::vector<int> &Z) {
+    std::vector<int> pos(P.L, -1);
+    for (int q = 0, n = 0; q < P.L; ++q)
+        if (std::find(Z.begin(), Z.end(), q) == Z.end()) pos[q] = n++;
+    return pos;
+}
+
+}  // namespace
+
+extern "C" {
+
+qp_status qp_shard_configure(qp_plan *P, int32_t n_ranks, int32_t rank) {
+    if (!P) return err(QP_ERR_ARG, "arg: NULL plan");
+    if (n_ranks < 2 || rank < 0 || rank >= n_ranks) return err(QP_ERR_ARG, "arg: need n_ranks >= 2 and 0 <= rank < n_ranks");
+    const int L = P->L, N = P->N;
+    // smallest z with at most 10% load imbalance of the N^z combos over the ranks
+    // (segments need 2z <= L - 1 so that consecutive shard-slot sets are disjoint); else the smallest
+    // z with N^z >= n_ranks
+    int z = 0, zmin = 0;
+    for (int zz = 1; 2 * zz <= L - 1; ++zz) {
+        const double nz = std::pow((double)N, zz);
+        if (nz < n_ranks) continue;
+        if (!zmin) zmin = zz;
+        if (std::ceil(nz / n_ranks) / (nz / n_ranks) <= 1.1 + 1e-12) { z = zz; break; }
+    }
+    if (!z) z = zmin;
+    if (!z) return err(QP_ERR_CONFIG, "config: cannot shard L = %d over %d ranks (need N^z >= ranks, 2z <= L-1)", L, n_ranks);
+    auto &sh = P->sh;
+    sh = qp_plan::Shard{};
+    sh.on = true;
+    sh.G = n_ranks;
+    sh.rank = rank;
+    sh.z = z;
+    sh.seg_len = L - z;
+    sh.NZ = ipow(N, z);
+    sh.blk = ipow(N, L - z);
+    sh.c_lo.resize(n_ranks);
+    sh.n_own.resize(n_ranks);
+    for (int r = 0; r < n_ranks; ++r) {
+        const int64_t base = sh.NZ / n_ranks, extra = sh.NZ % n_ranks;
+        sh.n_own[r] = base + (r < extra ? 1 : 0);
+        sh.c_lo[r] = r * base + std::min<int64_t>(r, extra);
+    }
+    // launch sets for every segment start slot of the (periodic) schedule
+    std::vector<int> starts;
+    for (int64_t j = 0;; ++j) {
+        const int zs = (int)(P->seg_begin(j) % L);
+        if (std::find(starts.begin(), starts.end(), zs) != starts.end()) break;
+        starts.push_back(zs);
+    }
+    for (int zs : starts) {
+        std::vector<int> Z;
+        for (int i = 0; i < z; ++i) Z.push_back(((zs - 1 - i) % L + L) % L);
+        std::sort(Z.begin(), Z.end());
+        for (int m = 0; m < sh.seg_len; ++m)
+            for (int S = 1; S <= P->Smax && m + S <= sh.seg_len; ++S) {
+                const int p0 = (zs + m) % L;
+                sh.index[std::make_tuple(zs, p0, S)] = sh.sets.size();
+                sh.sets.emplace_back();
+                build_launch_set(*P, p0, S, Z, sh.sets.back());
+            }
+    }
+    compute_layout(*P);
+    return QP_OK;
+}
+
+qp_status qp_shard_query(const qp_plan *P, qp_shard_sizes *o) {
+    if (!P || !o) return err(QP_ERR_ARG, "arg: NULL plan or out");
+    if (!P->sh.on) return err(QP_ERR_ARG, "arg: plan is not sharded (qp_shard_configure)");
+    const auto &sh = P->sh;
+    o->n_ranks = sh.G;
+    o->rank = sh.rank;
+    o->shard_slots = sh.z;
+    o->segment_steps = sh.seg_len;
+    o->local_entries = sh.n_own[sh.rank] * sh.blk;
+    int64_t mx = 0;
+    for (int r = 0; r < sh.G; ++r) mx = std::max(mx, sh.n_own[r]);
+    o->max_local_entries = mx * sh.blk;
+    o->exchange_entries = sh.n_own[sh.rank] * sh.blk;  // everything moves (incl. the part kept locally)
+    o->work_bytes = (int64_t)P->work_bytes;
+    return QP_OK;
+}
+
+qp_status qp_shard_counts(const qp_plan *P, int64_t *send_counts, int64_t *recv_counts) {
+    if (!P || !send_counts || !recv_counts) return err(QP_ERR_ARG, "arg: NULL plan or output");
+    if (!P->sh.on) return err(QP_ERR_ARG, "arg: plan is not sharded");
+    const auto &sh = P->sh;
+    const int64_t rest = ipow(P->N, P->L - 2 * sh.z);
+    for (int r = 0; r < sh.G; ++r) {
+        send_counts[r] = sh.n_own[sh.rank] * sh.n_own[r] * rest;
+        recv_counts[r] = sh.n_own[r] * sh.n_own[sh.rank] * rest;
+    }
+    return QP_OK;
+}
+
+qp_status qp_shard_extract(qp_plan *P, const void *d_full, void *d_local, void *stream) {
+    if (!P || !d_full || !d_local) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
+    if (!P->sh.on || !P->inited) return err(QP_ERR_ARG, "arg: plan not sharded / not initialised");
+    if (P->next_k != P->L) return err(QP_ERR_ARG, "arg: extract after the growth steps 1..L-1 (next step %lld)", (long long)P->next_k);
+    const auto &sh = P->sh;
+    const std::vector<int> Z = P->zset(0);
+    qp::PermuteArgs a{};
+    a.dst = (double2 *)d_local;
+    a.src = (const double2 *)d_full;
+    a.count = sh.n_own[sh.rank] * sh.blk;
+    a.scatter = 0;
+    int f = 0;
+    for (int q = 0; q < P->L; ++q)
+        if (std::find(Z.begin(), Z.end(), q) == Z.end()) { a.rad[f] = P->N; a.ncd[f] = 0; a.str[f][0] = ipow(P->N, q); ++f; }
+    a.rad[f] = sh.n_own[sh.rank]; a.lo[f] = sh.c_lo[sh.rank]; a.ncd[f] = sh.z;
+    for (int i = 0; i < sh.z; ++i) a.str[f][i] = ipow(P->N, Z[i]);
+    a.nf = f + 1;
+    QP_CUDA(qp::launch_permute(P->M, a, P->sms, (cudaStream_t)stream));
+    P->sh.extracted = true;
+    return QP_OK;
+}
+
+qp_status qp_shard_pack(qp_plan *P, const void *d_local, void *d_send, void *stream) {
+    if (!P || !d_local || !d_send) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
+    if (!P->sh.on || !P->sh.extracted) return err(QP_ERR_ARG, "arg: plan not sharded / no local data");
+    const auto &sh = P->sh;
+    const std::vector<int> Z0 = P->zset(sh.seg), Z1 = P->zset(sh.seg + 1);
+    const std::vector<int> pos = local_pos(*P, Z0);
+    int64_t off = 0;
+    for (int r = 0; r < sh.G; ++r) {
+        qp::PermuteArgs a{};
+        a.dst = (double2 *)d_send + off;
+        a.src = (const double2 *)d_local;
+        a.scatter = 0;
+        int f = 0;
+        for (int q = 0; q < P->L; ++q)  // the other slots, ascending
+            if (std::find(Z0.begin(), Z0.end(), q) == Z0.end() && std::find(Z1.begin(), Z1.end(), q) == Z1.end()) {
+                a.rad[f] = P->N; a.ncd[f] = 0; a.str[f][0] = ipow(P->N, pos[q]); ++f;
+            }
+        a.rad[f] = sh.n_own[r]; a.lo[f] = sh.c_lo[r]; a.ncd[f] = sh.z;  // destination's combos of Z_{j+1}
+        for (int i = 0; i < sh.z; ++i) a.str[f][i] = ipow(P->N, pos[Z1[i]]);
+        ++f;
+        a.rad[f] = sh.n_own[sh.rank]; a.ncd[f] = 0; a.str[f][0] = sh.blk;  // my blocks (combos of Z_j)
+        a.nf = f + 1;
+        a.count = sh.n_own[sh.rank] * sh.n_own[r] * ipow(P->N, P->L - 2 * sh.z);
+        QP_CUDA(qp::launch_permute(P->M, a, P->sms, (cudaStream_t)stream));
+        off += a.count;
+    }
+    return QP_OK;
+}
+
+qp_status qp_shard_unpack(qp_plan *P, const void *d_recv, void *d_local, void *stream) {
+    if (!P || !d_recv || !d_local) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
+    if (!P->sh.on || !P->sh.extracted) return err(QP_ERR_ARG, "arg: plan not sharded / no local data");
+    auto &sh = P->sh;
+    const std::vector<int> Z0 = P->zset(sh.seg), Z1 = P->zset(sh.seg + 1);
+    const std::vector<int> pos = local_pos(*P, Z1);
+    int64_t off = 0;
+    for (int r = 0; r < sh.G; ++r) {
+        qp::PermuteArgs a{};
+        a.dst = (double2 *)d_local;
+        a.src = (const double2 *)d_recv + off;
+        a.scatter = 1;
+        int f = 0;
+        for (int q = 0; q < P->L; ++q)
+            if (std::find(Z0.begin(), Z0.end(), q) == Z0.end() && std::find(Z1.begin(), Z1.end(), q) == Z1.end()) {
+                a.rad[f] = P->N; a.ncd[f] = 0; a.str[f][0] = ipow(P->N, pos[q]); ++f;
+            }
+        a.rad[f] = sh.n_own[sh.rank]; a.ncd[f] = 0; a.str[f][0] = sh.blk;  // my new blocks (combos of Z_{j+1})
+        ++f;
+        a.rad[f] = sh.n_own[r]; a.lo[f] = sh.c_lo[r]; a.ncd[f] = sh.z;  // source's combos of Z_j
+        for (int i = 0; i < sh.z; ++i) a.str[f][i] = ipow(P->N, pos[Z0[i]]);
+        a.nf = f + 1;
+        a.count = sh.n_own[r] * sh.n_own[sh.rank] * ipow(P->N, P->L - 2 * sh.z);
+        QP_CUDA(qp::launch_permute(P->M, a, P->sms, (cudaStream_t)stream));
+        off += a.count;
+    }
+    sh.seg += 1;
+    return QP_OK;
+}
+
+qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_local, void *d_work, void *stream,
+                         int64_t *n_launch) {
+    if (n_launch) *n_launch = 0;
+    if (!P || !d_local || !d_work) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
+    auto &sh = P->sh;
+    if (!sh.on || !sh.extracted) return err(QP_ERR_ARG, "arg: plan not sharded / no local data (qp_shard_extract)");
+    const int64_t s0 = P->seg_begin(sh.seg), s1 = s0 + sh.seg_len;
+    if (k_begin != P->next_k || k_begin < s0 || k_end > s1 || k_end < k_begin || k_end > P->n_steps + 1)
+        return err(QP_ERR_ARG, "arg: shard steps must be in order within segment [%lld, %lld), next step %lld",
+                   (long long)s0, (long long)s1, (long long)P->next_k);
+    cudaStream_t s = (cudaStream_t)stream;
+    char *w = (char *)d_work;
+    const int L = P->L, N = P->N;
+    const std::vector<int> Z = P->zset(sh.seg);
+    const int zs = (int)(s0 % L);
+    int64_t launched = 0;
+    for (int64_t k = k_begin; k < k_end;) {
+        const int64_t grp_end = s0 + ((k - s0) / P->Smax + 1) * P->Smax;
+        const int S = (int)(std::min<int64_t>({grp_end, k_end, s1}) - k);
+        const int p0 = (int)(k % L);
+        const auto it = sh.index.find(std::make_tuple(zs, p0, S));
+        if (it == sh.index.end()) return err(QP_ERR_ARG, "internal: no shard launch set for (%d, %d, %d)", zs, p0, S);
+        const qp_plan::LaunchSet &ls = sh.sets[it->second];
+        for (int64_t b = 0; b < sh.n_own[sh.rank]; ++b) {
+            qp::FusedArgs a = ls.args;
+            a.A = (double2 *)d_local + b * sh.blk;
+            a.small = (const double2 *)(w + P->off_small);
+            a.inner = (const double2 *)(w + ls.off_inner);
+            a.Etab = (const double2 *)(w + ls.off_E);
+            a.goff = (const long long *)(w + ls.off_goff);
+            a.lofs = (const int2 *)(w + ls.off_lofs);
+            a.partials = (double2 *)(w + P->off_part);
+            a.counter = (unsigned *)(w + P->off_cnt);
+            a.rho_accumulate = b > 0 ? 1 : 0;
+            int dig[8];
+            shard_combo_digits(*P, sh.c_lo[sh.rank] + b, dig);
+            bool ro = false;
+            const qp::SmallLayout lay{N, P->D, L};
+            for (int st = 0; st < S; ++st) {
+                const int64_t slot = P->slot_of(k + st);
+                a.rho[st] = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * N : nullptr;
+                ro |= slot >= 0;
+                const int var = (k + st == L) ? 1 : 0;
+                for (int kap = 0; kap < 2; ++kap)
+                    for (int d = 0; d < P->D; ++d)
+                        for (int old = 0; old < N; ++old)
+                            a.beta[st][kap][d][old] = P->small[lay.beta(var, kap) + d * N + old];
+                if (P->sym)
+                    for (int kap = 0; kap < 2; ++kap) {
+                        const double2 c = a.beta[st][kap][0][0];
+                        const double rho = a.beta[st][kap][0][1].x;
+                        a.sym[st][kap][0] = c.x;
+                        a.sym[st][kap][1] = c.y;
+                        a.sym[st][kap][2] = 0.5 * (rho + 1.0 / rho);
+                        a.sym[st][kap][3] = 0.5 * (rho - 1.0 / rho);
+                    }
+                // fixed shard-slot digits: their Eq. 9 factor for this sub-step (propagate / terminal)
+                for (int kap = 0; kap < 2; ++kap) {
+                    cd Ps = 0.0;
+                    for (int i = 0; i < sh.z; ++i) {
+                        const int lag = ((p0 + st - Z[i]) % L + L) % L;
+                        Ps += psi(*P, dig[i], kap == 0 ? P->eta[lag] : P->E[lag]);
+                    }
+                    for (int d = 0; d < P->D; ++d) a.fixfac[st][kap][d] = d2(std::exp(P->delta[d] * Ps));
+                }
+            }
+            const int qlast = (p0 - 1 + L) % L;
+            a.fixed_last = -1;
+            for (int i = 0; i < sh.z; ++i)
+                if (Z[i] == qlast) a.fixed_last = dig[i];
+            const cudaError_t e = qp::launch_fused(P->M, P->lattice, P->sym, P->kind, S, a, ro, P->grid[S], s);
+            if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: shard launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
+            ++launched;
+        }
+        k += S;
+        P->next_k = k;
+    }
+    if (n_launch) *n_launch = launched;
+    return QP_OK;
 }
 
 }  // extern "C"

@@ -48,7 +48,7 @@ __host__ __device__ constexpr int cpow(int b, int e) { return e == 0 ? 1 : b * c
 // the grid and the tile->block assignment are fixed by the plan).
 template <int N, int BLOCK>
 __device__ __forceinline__ void reduce_finalize(double2 (&acc)[N], double2 *partials, double2 *rho,
-                                                unsigned *counter) {
+                                                unsigned *counter, bool accumulate = false) {
     constexpr int W = BLOCK / 32;
     __shared__ double2 red[W][N];
     __shared__ double2 fin[W];
@@ -89,7 +89,7 @@ __device__ __forceinline__ void reduce_finalize(double2 (&acc)[N], double2 *part
         if (threadIdx.x == 0) {
             double2 t = fin[0];
             for (int w = 1; w < W; ++w) t = cadd(t, fin[w]);
-            rho[n] = t;
+            rho[n] = accumulate ? cadd(rho[n], t) : t;
         }
         __syncthreads();
     }
@@ -195,13 +195,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
             double2 e = make_double2(1.0, 0.0);
             for (int g = 1; g < a.G; ++g)
                 e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
-            sEhi[slot][s][kap][d] = e;
+            sEhi[slot][s][kap][d] = cmul(e, a.fixfac[s][kap][d]);
         }
         if ((int)threadIdx.x == BLOCK - 1) {
             long long b = 0;
             for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
             sBase[slot] = b;
-            sLast[slot] = a.last_div > 0 ? (tau / a.last_div) % N : 0;
+            sLast[slot] = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
         }
     };
     auto stage_b = [&](int aslot, int kslot) {
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
         for (int s = 0; s < S; ++s)
             if (a.rho[s] != nullptr)
                 reduce_finalize<N, BLOCK>(accR[RO ? s : 0], a.partials + (size_t)s * kPartialsMax * N, a.rho[s],
-                                          a.counter + s);
+                                          a.counter + s, a.rho_accumulate != 0);
     }
 }
 
@@ -406,13 +406,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
                 double2 e = make_double2(1.0, 0.0);
                 for (int g = 1; g < a.G; ++g)
                     e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
-                sEhi[warp][s][kap][d] = e;
+                sEhi[warp][s][kap][d] = cmul(e, a.fixfac[s][kap][d]);
             }
             if (lane == 31) {
                 long long b = 0;
                 for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
                 sBase[warp] = b;
-                sLast[warp] = a.last_div > 0 ? (tau / a.last_div) % N : 0;
+                sLast[warp] = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
             }
             __syncwarp();
             for (int j = lane; j < NKU; j += 32) {
@@ -540,7 +540,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
                 double2 tt[N];
 #pragma unroll
                 for (int n = 0; n < N; ++n) tt[n] = accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0];
-                reduce_finalize<N, BLOCK>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s);
+                reduce_finalize<N, BLOCK>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
+                                          a.rho_accumulate != 0);
             }
     }
 }
@@ -761,6 +762,52 @@ cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaSt
     case 4: return lattice ? grow_t<4, true>(a, grid, s) : grow_t<4, false>(a, grid, s);
     default: return cudaErrorInvalidValue;
     }
+}
+
+}  // namespace qp
+
+// ============================================================================================
+// Re-shard data movement (multi-GPU path): one generic digit-permutation copy.
+// The dense side index i is a mixed-radix number over `nf` fields (innermost first); field f has
+// radix rad[f] and contributes to the strided side's address either linearly (ncd[f] == 0:
+// value * str[f][0]) or as a combo of ncd[f] base-N digits of (lo[f] + value) with strides
+// str[f][0..ncd-1].  gather: dst[i] = src[addr(i)];  scatter: dst[addr(i)] = src[i].
+// ============================================================================================
+namespace qp {
+
+template <int N>
+__global__ void __launch_bounds__(256) k_permute(const PermuteArgs a) {
+    const long long stride = (long long)gridDim.x * 256;
+    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < a.count; i += stride) {
+        long long rest = i, addr = a.base;
+        for (int f = 0; f < a.nf; ++f) {
+            const long long v = rest % a.rad[f];
+            rest /= a.rad[f];
+            if (a.ncd[f] == 0) {
+                addr += v * a.str[f][0];
+            } else {
+                long long c = a.lo[f] + v;
+                for (int j = 0; j < a.ncd[f]; ++j) {
+                    addr += (c % N) * a.str[f][j];
+                    c /= N;
+                }
+            }
+        }
+        if (a.scatter) a.dst[addr] = __ldcs(a.src + i);
+        else a.dst[i] = __ldcs(a.src + addr);
+    }
+}
+
+cudaError_t launch_permute(int M, const PermuteArgs &a, int sms, cudaStream_t s) {
+    if (a.count <= 0) return cudaSuccess;
+    const int grid = (int)std::min<long long>((a.count + 255) / 256, (long long)sms * 16);
+    switch (M) {
+    case 2: k_permute<4><<<grid, 256, 0, s>>>(a); break;
+    case 3: k_permute<9><<<grid, 256, 0, s>>>(a); break;
+    case 4: k_permute<16><<<grid, 256, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 }  // namespace qp

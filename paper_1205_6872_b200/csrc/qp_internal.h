@@ -59,18 +59,38 @@ struct FusedArgs {
     int gdiv[kMaxGroups];    // group g >= 1: index = (tau / gdiv[g]) % gmod[g]
     int gmod[kMaxGroups];
     int last_div;            // sub-step 0 'last' digit is a tile digit: (tau / last_div) % N; else -1
+    int fixed_last;          // sub-step 0 'last' slot is a (fixed) shard slot: its value; else -1
+    int rho_accumulate;      // 1: rho[n] += sum (several shard blocks contribute to one step)
     // beta_d(old) = exp(delta_d psi_L(old)) of each sub-step (kernel-parameter constant bank):
     // [sub-step][0 propagate / 1 terminal][class][old]; the first slide step k == L uses the
     // initial-edge classes (partner sigma_0)
     double2 beta[kMaxS][2][kMaxD][kMaxN];
     // M = 2, s = (+s, -s): beta_1 = (c, rho, 1/rho, conj c); {Re c, Im c, (rho+1/rho)/2, (rho-1/rho)/2}
     double sym[kMaxS][2][4];
+    // sharded layouts: factor of the fixed shard-slot digits of this block, per sub-step / kind / class
+    double2 fixfac[kMaxS][2][kMaxD];
 };
 
 // Fused-kernel shape for one M: max fused steps and outer digit-group size w.
 struct FusedShape {
     int S, w;
 };
+
+// Generic digit-permutation copy for the re-shard (kernels.cu: k_permute).
+constexpr int kMaxFields = kMaxL + 4;
+struct PermuteArgs {
+    double2 *dst;
+    const double2 *src;
+    long long count;         // dense-side entries
+    long long base;          // address offset on the strided side
+    int nf;                  // fields, innermost first
+    int scatter;             // 0: dst[i] = src[addr(i)], 1: dst[addr(i)] = src[i]
+    long long rad[kMaxFields];
+    long long lo[kMaxFields];
+    int ncd[kMaxFields];     // 0 = linear field, else number of base-N digits of the combo (lo + value)
+    long long str[kMaxFields][4];
+};
+cudaError_t launch_permute(int M, const PermuteArgs &a, int sms, cudaStream_t s);
 
 // Per-launch arguments of the growth step k (1 <= k < L): A_{k-1} (N^k) -> A_k (N^(k+1)).
 struct GrowArgs {

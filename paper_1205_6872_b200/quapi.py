@@ -64,9 +64,19 @@ class qp_sizes(ctypes.Structure):
     ]
 
 
+class qp_shard_sizes(ctypes.Structure):
+    _fields_ = [
+        ("n_ranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("shard_slots", ctypes.c_int32),
+        ("segment_steps", ctypes.c_int32), ("local_entries", ctypes.c_int64), ("max_local_entries", ctypes.c_int64),
+        ("exchange_entries", ctypes.c_int64), ("work_bytes", ctypes.c_int64),
+    ]
+
+
 # Every symbol include/quapi.h declares (tests check the library exports all of them).
 EXPORTS = ("qp_plan_create", "qp_plan_query", "qp_plan_eta", "qp_plan_propagator", "qp_init", "qp_steps",
-           "qp_read_rho", "qp_run", "qp_last_error", "qp_plan_destroy", "qp_version")
+           "qp_read_rho", "qp_run", "qp_last_error", "qp_plan_destroy", "qp_version",
+           "qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_extract", "qp_shard_steps",
+           "qp_shard_pack", "qp_shard_unpack")
 
 _lib = None
 
@@ -95,6 +105,17 @@ def lib() -> ctypes.CDLL:
                                ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
         L.qp_read_rho.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(qp_c64), ctypes.c_void_p]
         L.qp_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(qp_c64)]
+        vp = ctypes.c_void_p
+        L.qp_shard_configure.argtypes = [vp, ctypes.c_int32, ctypes.c_int32]
+        L.qp_shard_query.argtypes = [vp, ctypes.POINTER(qp_shard_sizes)]
+        L.qp_shard_counts.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        L.qp_shard_extract.argtypes = [vp, vp, vp, vp]
+        L.qp_shard_steps.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp, ctypes.POINTER(ctypes.c_int64)]
+        L.qp_shard_pack.argtypes = [vp, vp, vp, vp]
+        L.qp_shard_unpack.argtypes = [vp, vp, vp, vp]
+        for f in ("qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_extract", "qp_shard_steps",
+                  "qp_shard_pack", "qp_shard_unpack"):
+            getattr(L, f).restype = ctypes.c_int
         L.qp_last_error.restype = ctypes.c_char_p
         L.qp_version.restype = ctypes.c_char_p
         L.qp_plan_destroy.argtypes = [ctypes.c_void_p]
@@ -250,6 +271,44 @@ class Plan:
                             ctypes.c_void_p(self._stream_ptr(stream)), buf))
         self.launches += self.w.n_steps
         return _to_numpy(buf, (n, self.w.M, self.w.M))[:n]
+
+
+    # ---- sharded execution (multi-GPU); see include/quapi.h and paper_1205_6872_b200/sharded.py
+    def shard(self, n_ranks: int, rank: int) -> "qp_shard_sizes":
+        _check(lib().qp_shard_configure(self._h, int(n_ranks), int(rank)))
+        return self.shard_sizes
+
+    @property
+    def shard_sizes(self) -> "qp_shard_sizes":
+        o = qp_shard_sizes()
+        _check(lib().qp_shard_query(self._h, ctypes.byref(o)))
+        return o
+
+    def shard_counts(self):
+        n = self.shard_sizes.n_ranks
+        snd, rcv = (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)()
+        _check(lib().qp_shard_counts(self._h, snd, rcv))
+        return list(snd), list(rcv)
+
+    def shard_extract(self, full, local, stream=None):
+        _check(lib().qp_shard_extract(self._h, ctypes.c_void_p(full.data_ptr()), ctypes.c_void_p(local.data_ptr()),
+                                      ctypes.c_void_p(self._stream_ptr(stream))))
+
+    def shard_steps(self, k_begin: int, k_end: int, local, work, stream=None) -> int:
+        n = ctypes.c_int64(0)
+        _check(lib().qp_shard_steps(self._h, int(k_begin), int(k_end), ctypes.c_void_p(local.data_ptr()),
+                                    ctypes.c_void_p(work.data_ptr()), ctypes.c_void_p(self._stream_ptr(stream)),
+                                    ctypes.byref(n)))
+        self.launches += n.value
+        return n.value
+
+    def shard_pack(self, local, send, stream=None):
+        _check(lib().qp_shard_pack(self._h, ctypes.c_void_p(local.data_ptr()), ctypes.c_void_p(send.data_ptr()),
+                                   ctypes.c_void_p(self._stream_ptr(stream))))
+
+    def shard_unpack(self, recv, local, stream=None):
+        _check(lib().qp_shard_unpack(self._h, ctypes.c_void_p(recv.data_ptr()), ctypes.c_void_p(local.data_ptr()),
+                                     ctypes.c_void_p(self._stream_ptr(stream))))
 
 
 def solve(w: W.Workload, out_steps: Optional[Sequence[int]] = None, device: str = "cuda", **kw) -> np.ndarray:
