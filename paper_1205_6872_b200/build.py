@@ -22,7 +22,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(d) for d in DEPS):
         return SO
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", SO, *SOURCES]
+    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", SO, *SOURCES, "-lpthread"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -16,6 +16,8 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <complex>
@@ -410,15 +412,32 @@ qp_status compute_eta(qp_plan &P, const qp_problem &pr) {
         return QP_OK;
     }
     Bath b{pr.kind, pr.coupling, pr.omega_c, pr.kT, pr.J, pr.J_user, pr.J_cutoff};
-    qp_status st;
-    if ((st = eta_class(b, WinClass{true, dt, 0, 0, 0}, &P.self_int, "self_interior", 0))) return st;
-    if ((st = eta_class(b, WinClass{true, 0.5 * dt, 0, 0, 0}, &P.self_end, "self_end", 0))) return st;
+    // the 3L+2 class integrals are independent: run them on host threads (the paper's §V notes the
+    // eta setup becomes the bottleneck once propagation runs on the GPU)
+    struct Job { WinClass c; cd *out; const char *name; int lag; qp_status st; std::string msg; };
+    std::vector<Job> jobs;
+    jobs.push_back({WinClass{true, dt, 0, 0, 0}, &P.self_int, "self_interior", 0, QP_OK, {}});
+    jobs.push_back({WinClass{true, 0.5 * dt, 0, 0, 0}, &P.self_end, "self_end", 0, QP_OK, {}});
     for (int j = 1; j <= L; ++j) {
-        if ((st = eta_class(b, WinClass{false, 0, dt, dt, j * dt}, &P.eta[j], "eta", j))) return st;
-        if ((st = eta_class(b, WinClass{false, 0, dt, 0.5 * dt, (j - 0.25) * dt}, &P.E[j], "edge", j))) return st;
-        if ((st = eta_class(b, WinClass{false, 0, 0.5 * dt, 0.5 * dt, (j - 0.5) * dt}, &P.TI[j], "terminal_initial", j)))
-            return st;
+        jobs.push_back({WinClass{false, 0, dt, dt, j * dt}, &P.eta[j], "eta", j, QP_OK, {}});
+        jobs.push_back({WinClass{false, 0, dt, 0.5 * dt, (j - 0.25) * dt}, &P.E[j], "edge", j, QP_OK, {}});
+        jobs.push_back({WinClass{false, 0, 0.5 * dt, 0.5 * dt, (j - 0.5) * dt}, &P.TI[j], "terminal_initial", j, QP_OK, {}});
     }
+    const int nth = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+        for (size_t i = next++; i < jobs.size(); i = next++) {
+            Job &jb = jobs[i];
+            jb.st = eta_class(b, jb.c, jb.out, jb.name, jb.lag);
+            if (jb.st) jb.msg = g_err;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nth; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto &th : pool) th.join();
+    for (const Job &jb : jobs)
+        if (jb.st) return err(jb.st, "%s", jb.msg.c_str());
     return QP_OK;
 }
 
@@ -574,7 +593,7 @@ void build_tables(qp_plan &P) {
     //      inner slots p0..p0+S-1 and the factor / address tables of the L-S outer slots
     P.shape = qp::fused_shape(M);
     P.Smax = std::max(1, std::min(P.shape.S, L - 1));
-    if (const char *ek = std::getenv("QUAPI_FUSED_KIND")) P.kind = (ek[0] == 'w') ? 0 : 1;
+    if (const char *ek = std::getenv("QUAPI_FUSED_KIND")) P.kind = (ek[0] == 'w') ? 0 : (ek[0] == 'a' ? 2 : (ek[0] == 's' ? 3 : 1));
     if (const char *ev = std::getenv("QUAPI_FUSE_S")) P.Smax = std::max(1, std::min(P.Smax, std::atoi(ev)));
     P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
     for (int p0 = 0; p0 < L; ++p0)

@@ -342,7 +342,21 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
 // the tile in chunks of 32 outer fibres, lane = outer fibre.  Readout accumulators live in
 // shared memory; the CTA reduction at the end is in fixed order (deterministic).
 // --------------------------------------------------------------------------------------------
-template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool RO>
+#ifndef QP_L2_AHEAD
+#define QP_L2_AHEAD 0
+#endif
+constexpr long long kL2Ahead = QP_L2_AHEAD;  // units of L2 prefetch distance in k_fused_r
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NPEND> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(NPEND) : "memory");
+}
+
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool ASYNC, bool RO>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__ FusedArgs a) {
     constexpr int N = M * M;
     constexpr int D = n_classes(M, LAT);
@@ -354,7 +368,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
     const SmallLayout lay{N, D, 0};
     __shared__ double2 sK[2][N][N];
     __shared__ double2 sIn[S][S][2][D][N];
-    extern __shared__ double2 dyn_smem[];  // readout accumulators [S][N][BLOCK] (RO only)
+    // dynamic shared memory: readout accumulators [S][N][BLOCK] (RO only), then (ASYNC only) a
+    // per-warp double buffer [2][NS][32] of super-fibres staged by cp.async one chunk ahead
+    extern __shared__ double2 dyn_smem[];
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
@@ -396,6 +412,24 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
     int cur_tile = -1;
     long long tbase = 0;
     int last_t = 0;
+    double2(*stg)[NS][32] = reinterpret_cast<double2(*)[NS][32]>(
+        dyn_smem + (RO ? S * N * BLOCK : 0) + (ASYNC ? (size_t)warp * 2 * NS * 32 : 0));
+    auto issue = [&](long long u, int b) {  // stage unit u's super-fibres (this lane's) into buffer b
+        const int tau = (int)(u / CH), t = (int)(u % CH) * 32 + lane;
+        if (t < a.T) {
+            long long base = __ldg(&a.lofs[t]).x;
+            for (int g = 1; g < a.G; ++g) base += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+#pragma unroll
+            for (int e = 0; e < NS; ++e) {
+                long long o = base;
+#pragma unroll
+                for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
+                cp_async16(&stg[b][e][lane], a.A + o);
+            }
+        }
+        cp_async_commit();
+    };
+    if (ASYNC && u_begin < u_end) issue(u_begin, 0);
     for (long long u = u_begin; u < u_end; ++u) {
         const int tau = (int)(u / CH), t = (int)(u % CH) * 32 + lane;
         if (tau != cur_tile) {  // warp-synchronous tile setup
@@ -426,17 +460,43 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
             tbase = sBase[warp];
             last_t = sLast[warp];
         }
+        if (ASYNC) {
+            if (u + 1 < u_end) issue(u + 1, (int)((u + 1 - u_begin) & 1));
+            else cp_async_commit();
+            cp_async_wait<1>();  // this lane's copies of unit u have landed
+        } else if (kL2Ahead > 0 && u + kL2Ahead < u_end) {
+            // pull unit u+kL2Ahead into L2 (no registers held): its loads later hit L2 instead of HBM
+            const long long un = u + kL2Ahead;
+            const int taun = (int)(un / CH), tn = (int)(un % CH) * 32 + lane;
+            if (tn < a.T) {
+                long long base = __ldg(&a.lofs[tn]).x;
+                for (int g = 1; g < a.G; ++g) base += __ldg(&a.goff[(size_t)g * a.X + (taun / a.gdiv[g]) % a.gmod[g]]);
+#pragma unroll
+                for (int e = 0; e < NS; ++e) {
+                    long long o = base;
+#pragma unroll
+                    for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.A + o));
+                }
+            }
+        }
         {
             if (t >= a.T) continue;
             const int2 lo = __ldg(&a.lofs[t]);
             const long long base = tbase + lo.x;
             double2 x[NS];
+            if (ASYNC) {
+                const int b = (int)((u - u_begin) & 1);
 #pragma unroll
-            for (int e = 0; e < NS; ++e) {
-                long long o = base;
+                for (int e = 0; e < NS; ++e) x[e] = stg[b][e][lane];
+            } else {
 #pragma unroll
-                for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
-                x[e] = __ldcs(a.A + o);
+                for (int e = 0; e < NS; ++e) {
+                    long long o = base;
+#pragma unroll
+                    for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
+                    x[e] = __ldcs(a.A + o);
+                }
             }
             const int last0 = lo.y >= 0 ? lo.y : last_t;
 #pragma unroll
@@ -533,6 +593,242 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
             }
         }
     }
+    if (ASYNC) cp_async_wait<0>();
+    if constexpr (RO) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (a.rho[s] != nullptr) {
+                double2 tt[N];
+#pragma unroll
+                for (int n = 0; n < N; ++n) tt[n] = accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0];
+                reduce_finalize<N, BLOCK>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
+                                          a.rho_accumulate != 0);
+            }
+    }
+}
+
+// --------------------------------------------------------------------------------------------
+// Split-register variant (S = 2, even N): two lanes share one super-fibre, each holding half of it
+// (N^2/2 entries: inner digit 1 in its half {p N/2 .. p N/2 + N/2 - 1}).  Sub-step 0 (fibres along
+// digit 0) is complete in each lane; the halves are then swapped across the lane pair with warp
+// shuffles (lane ^ 16) so that sub-step 1 (fibres along digit 1) is complete too, and each lane
+// stores its new half directly.  Half the registers of k_fused_r per lane -> twice the warps per SM
+// for the same bytes in flight.  Lane l: outer fibre (l & 15) of the chunk, part p = l >> 4.
+// --------------------------------------------------------------------------------------------
+template <int M, bool LAT, bool SYM, int BLOCK, int MINB, bool RO>
+__global__ void __launch_bounds__(BLOCK, MINB) k_fused_p2(const __grid_constant__ FusedArgs a) {
+    constexpr int N = M * M;
+    constexpr int S = 2;
+    constexpr int H = N / 2;             // digit-1 values per part
+    constexpr int D = n_classes(M, LAT);
+    constexpr int Q = N;                 // fibres per super-fibre and sub-step
+    constexpr int NK = RO ? 2 : 1;
+    constexpr int W = BLOCK / 32;
+    static_assert(N % 2 == 0, "split variant needs even N");
+    static_assert(!SYM || (M == 2 && D == 2), "symmetric moments are the M = 2 s = (+s,-s) case");
+    const SmallLayout lay{N, D, 0};
+    __shared__ double2 sK[2][N][N];
+    __shared__ double2 sIn[S][S][2][D][N];
+    extern __shared__ double2 dyn_smem[];  // readout accumulators [S][N][BLOCK] (RO only)
+    auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem);
+    for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
+    for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
+    if constexpr (RO)
+        for (int s = 0; s < S; ++s)
+            for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int part = lane >> 4, sub = lane & 15;
+    const int CH = (a.T + 15) >> 4;
+    const long long n_units = (long long)a.n_tiles * CH;
+    const int gw = (int)blockIdx.x * W + warp, nw_tot = (int)gridDim.x * W;
+    const long long per = n_units / nw_tot, rem = n_units % nw_tot;
+    const long long u_begin = gw * per + min((long long)gw, rem);
+    const long long u_end = u_begin + per + (gw < rem ? 1 : 0);
+    constexpr int NKU = S * NK * Q * N * N;
+    __shared__ double2 KI[S][NK][Q][N][N];
+    __shared__ double2 KU[W][S][NK][Q][N][N];
+    __shared__ double2 sEhi[W][S][NK][D];
+    __shared__ long long sBase[W];
+    __shared__ int sLast[W];
+    __syncthreads();
+    for (int j = threadIdx.x; j < NKU; j += BLOCK) {
+        const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
+                  s = j / (N * N * Q * NK);
+        const int c = class_of(M, LAT, nw / M, nw % M);
+        double2 e = sK[kap][nw][last];
+        if (c > 0)
+            for (int i = 0; i < S; ++i)
+                if (i != s) e = cmul(e, sIn[s][i][kap][c - 1][fib_digit<N, S>(s, rr, i)]);
+        KI[s][kap][rr][nw][last] = e;
+    }
+    __syncthreads();
+    const double2(&ki)[S][NK][Q][N][N] = KI;
+    double2(&ku_w)[S][NK][Q][N][N] = KU[warp];
+    int cur_tile = -1;
+    long long tbase = 0;
+    int last_t = 0;
+    for (long long u = u_begin; u < u_end; ++u) {
+        const int tau = (int)(u / CH), t = (int)(u % CH) * 16 + sub;
+        if (tau != cur_tile) {  // warp-synchronous tile setup
+            __syncwarp();
+            cur_tile = tau;
+            if (lane < S * NK * D) {
+                const int s = lane / (NK * D), kap = (lane / D) % NK, d = lane % D;
+                double2 e = make_double2(1.0, 0.0);
+                for (int g = 1; g < a.G; ++g)
+                    e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
+                sEhi[warp][s][kap][d] = cmul(e, a.fixfac[s][kap][d]);
+            }
+            if (lane == 31) {
+                long long b = 0;
+                for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+                sBase[warp] = b;
+                sLast[warp] = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
+            }
+            __syncwarp();
+            for (int j = lane; j < NKU; j += 32) {
+                const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
+                          s = j / (N * N * Q * NK);
+                const int c = class_of(M, LAT, nw / M, nw % M);
+                const double2 e = ki[s][kap][rr][nw][last];
+                ku_w[s][kap][rr][nw][last] = c > 0 ? cmul(e, sEhi[warp][s][kap][c - 1]) : e;
+            }
+            __syncwarp();
+            tbase = sBase[warp];
+            last_t = sLast[warp];
+        }
+        const bool valid = t < a.T;
+        const int2 lo = valid ? __ldg(&a.lofs[t]) : make_int2(0, 0);
+        const long long base = tbase + lo.x;
+        // X[i][v]: digit 1 = part*H + i, digit 0 = v
+        double2 X[H][N];
+        if (valid) {
+#pragma unroll
+            for (int i = 0; i < H; ++i)
+#pragma unroll
+                for (int v = 0; v < N; ++v) X[i][v] = __ldcs(a.A + base + (long long)v * a.pw_in[0] + (long long)(part * H + i) * a.pw_in[1]);
+        }
+        const int last0 = lo.y >= 0 ? lo.y : last_t;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s == 1) {
+                // swap halves across the lane pair: keep digit 0 in {part*H + jj}, all digit-1 values.
+                // Send X[i][(1-part)*H + jj] (the partner's digit-0 half), receive the partner's X[i][part*H + jj].
+                double2 Y[N][H];  // Y[d1][jj], d0 = part*H + jj
+#pragma unroll
+                for (int i = 0; i < H; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < H; ++jj) {
+                        const double2 keep = part == 0 ? X[i][jj] : X[i][H + jj];
+                        const double2 give = part == 0 ? X[i][H + jj] : X[i][jj];
+                        double2 got;
+                        got.x = __shfl_xor_sync(0xffffffffu, give.x, 16);
+                        got.y = __shfl_xor_sync(0xffffffffu, give.y, 16);
+                        // own digit-1 values are part*H + i, the partner's (1-part)*H + i
+                        if (part == 0) { Y[i][jj] = keep; Y[H + i][jj] = got; }
+                        else { Y[H + i][jj] = keep; Y[i][jj] = got; }
+                    }
+#pragma unroll
+                for (int i = 0; i < H; ++i)
+#pragma unroll
+                    for (int v = 0; v < N; ++v) X[i][v] = make_double2(0.0, 0.0);
+                // re-use X as [jj][d1] storage: X_(jj)[d1]
+#pragma unroll
+                for (int jj = 0; jj < H; ++jj)
+#pragma unroll
+                    for (int d1 = 0; d1 < N; ++d1) X[jj][d1] = Y[d1][jj];
+            }
+            if (!valid) continue;
+            const bool ro = RO && a.rho[s] != nullptr;
+            double2 E0[NK][D];
+#pragma unroll
+            for (int kap = 0; kap < NK; ++kap)
+#pragma unroll
+                for (int d = 0; d < D; ++d)
+                    E0[kap][d] = (kap == 0 || ro) ? __ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t])
+                                                  : make_double2(0.0, 0.0);
+            double2 acc[RO ? N : 1];
+#pragma unroll
+            for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
+            const double2(&ku)[NK][Q][N][N] = ku_w[s];
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                double2(&xf)[N] = X[i];
+                // fibre index r = value of the other inner digit; 'last' = digit 0 for sub-step 1
+                const int r = part * H + i;
+                const int last = s == 0 ? last0 : r;
+                double2 S0, m[NK][D];
+                if constexpr (SYM) {
+                    const double2 uu = cadd(xf[0], xf[3]), w = make_double2(xf[0].x - xf[3].x, xf[0].y - xf[3].y);
+                    const double2 p = cadd(xf[1], xf[2]), q = make_double2(xf[1].x - xf[2].x, xf[1].y - xf[2].y);
+                    S0 = cadd(uu, p);
+#pragma unroll
+                    for (int kap = 0; kap < NK; ++kap) {
+                        if (kap == 1 && !ro) break;
+                        const double cr = a.sym[s][kap][0], ci = a.sym[s][kap][1], ch = a.sym[s][kap][2], sh = a.sym[s][kap][3];
+                        const double2 A = make_double2(fma(cr, uu.x, ch * p.x), fma(cr, uu.y, ch * p.y));
+                        const double2 Bv = make_double2(fma(-ci, w.y, sh * q.x), fma(ci, w.x, sh * q.y));
+                        m[kap][0] = cadd(A, Bv);
+                        m[kap][D - 1] = make_double2(A.x - Bv.x, A.y - Bv.y);
+                    }
+                } else {
+                    S0 = xf[0];
+#pragma unroll
+                    for (int v = 1; v < N; ++v) S0 = cadd(S0, xf[v]);
+#pragma unroll
+                    for (int kap = 0; kap < NK; ++kap) {
+                        if (kap == 1 && !ro) break;
+#pragma unroll
+                        for (int d = 0; d < D; ++d) {
+                            double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
+#pragma unroll
+                            for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                            m[kap][d] = mm;
+                        }
+                    }
+                }
+                if (ro) {
+#pragma unroll
+                    for (int d = 0; d < D; ++d) {
+                        const double2 pt = cmul(E0[NK - 1][d], m[NK - 1][d]);
+#pragma unroll
+                        for (int aa = 0; aa < M; ++aa)
+#pragma unroll
+                            for (int bb = 0; bb < M; ++bb)
+                                if (class_of(M, LAT, aa, bb) == d + 1)
+                                    acc[RO ? aa * M + bb : 0] = cfma(ku[NK - 1][r][aa * M + bb][last], pt, acc[RO ? aa * M + bb : 0]);
+                    }
+                }
+                double2 P[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) P[d] = cmul(E0[0][d], m[0][d]);
+#pragma unroll
+                for (int aa = 0; aa < M; ++aa)
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const int nw = aa * M + bb;
+                        const int c = class_of(M, LAT, aa, bb);
+                        const double2 o = cmul(ku[0][r][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
+                        xf[nw] = o;
+                        if (ro && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
+                    }
+            }
+            if (ro) {
+#pragma unroll
+                for (int n = 0; n < N; ++n)
+                    accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0] =
+                        cadd(accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0], acc[RO ? n : 0]);
+            }
+        }
+        if (valid) {  // X[jj][d1]: digit 0 = part*H + jj
+#pragma unroll
+            for (int jj = 0; jj < H; ++jj)
+#pragma unroll
+                for (int d1 = 0; d1 < N; ++d1)
+                    __stcs(a.A + base + (long long)(part * H + jj) * a.pw_in[0] + (long long)d1 * a.pw_in[1], X[jj][d1]);
+        }
+    }
     if constexpr (RO) {
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -617,11 +913,18 @@ __global__ void __launch_bounds__(256) k_grow(const __grid_constant__ GrowArgs a
     X(2, 2, 256, 3, 64, 3)       \
     X(3, 1, 736, 3, 736, 1)      \
     X(4, 1, 256, 2, 256, 2)
-// register variant k_fused_r: (M, S, block, v, min blocks)
-#define QP_FUSED_R_CFGS(X)       \
-    X(2, 1, 256, 4, 2)           \
-    X(2, 2, 256, 4, 2)           \
-    X(3, 1, 256, 3, 2)
+// register variant k_fused_r: (M, S, block, v, min blocks, cp.async staging)
+#define QP_FUSED_R_CFGS(X)           \
+    X(2, 1, 256, 4, 2, false)        \
+    X(2, 2, 256, 4, 2, false)        \
+    X(3, 1, 256, 3, 2, false)
+// split-register variant k_fused_p2 (S = 2 only): (M, S, block, v, min blocks, unused)
+#define QP_FUSED_P_CFGS(X)           \
+    X(2, 2, 256, 4, 3, false)
+#define QP_FUSED_A_CFGS(X)           \
+    X(2, 1, 128, 4, 2, true)         \
+    X(2, 2, 128, 4, 2, true)         \
+    X(3, 1, 128, 3, 2, true)
 
 FusedShape fused_shape(int M) {
     switch (M) {
@@ -631,20 +934,32 @@ FusedShape fused_shape(int M) {
     }
 }
 
-bool has_reg_variant(int M, int S) {
-#define X(M_, S_, B, V, MB) if (M == M_ && S == S_) return true;
-    QP_FUSED_R_CFGS(X)
+// kind: 0 = warp-mapped k_fused, 1 = register k_fused_r, 2 = register k_fused_r with cp.async staging
+bool has_reg_variant(int M, int S, int kind) {
+    if (kind == 3) {
+#define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return true;
+        QP_FUSED_P_CFGS(X)
 #undef X
-    return false;
-}
-static bool use_reg_variant(int M, int S, int kind) { return kind == 1 && has_reg_variant(M, S); }
-
-int fused_tile_digits(int M, int S, int kind) {
-    if (use_reg_variant(M, S, kind)) {
-#define X(M_, S_, B, V, MB) if (M == M_ && S == S_) return V;
+    }
+    if (kind == 1) {
+#define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return true;
         QP_FUSED_R_CFGS(X)
 #undef X
     }
+    if (kind == 2) {
+#define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return true;
+        QP_FUSED_A_CFGS(X)
+#undef X
+    }
+    return false;
+}
+
+int fused_tile_digits(int M, int S, int kind) {
+#define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return V;
+    if (kind == 1 && has_reg_variant(M, S, 1)) { QP_FUSED_R_CFGS(X) }
+    if (kind == 2 && has_reg_variant(M, S, 2)) { QP_FUSED_A_CFGS(X) }
+    if (kind == 3 && has_reg_variant(M, S, 3)) { QP_FUSED_P_CFGS(X) }
+#undef X
 #define X(M_, S_, B, V, TL, MB) if (M == M_ && S == S_) return V;
     QP_FUSED_CFGS(X)
 #undef X
@@ -652,39 +967,65 @@ int fused_tile_digits(int M, int S, int kind) {
 }
 
 int fused_block(int M, int S, int kind) {
-    if (use_reg_variant(M, S, kind)) {
-#define X(M_, S_, B, V, MB) if (M == M_ && S == S_) return B;
-        QP_FUSED_R_CFGS(X)
+#define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return B;
+    if (kind == 1 && has_reg_variant(M, S, 1)) { QP_FUSED_R_CFGS(X) }
+    if (kind == 2 && has_reg_variant(M, S, 2)) { QP_FUSED_A_CFGS(X) }
+    if (kind == 3 && has_reg_variant(M, S, 3)) { QP_FUSED_P_CFGS(X) }
 #undef X
-    }
 #define X(M_, S_, B, V, TL, MB) if (M == M_ && S == S_) return B;
     QP_FUSED_CFGS(X)
 #undef X
     return 0;
 }
 
-template <int M, int S, int BLOCK>
-static constexpr size_t fused_r_dyn_smem() { return (size_t)S * M * M * BLOCK * 16; }
+template <int M, int S, int BLOCK, bool ASYNC>
+static constexpr size_t fused_r_dyn_smem(bool ro) {
+    return ((ro ? (size_t)S * M * M * BLOCK : 0) + (ASYNC ? (size_t)(BLOCK / 32) * 2 * cpow(M * M, S) * 32 : 0)) * 16;
+}
 
-template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB>
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool ASYNC>
 static cudaError_t fused_r_t(const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
-    constexpr size_t dyn = fused_r_dyn_smem<M, S, BLOCK>();
+    const size_t dyn = fused_r_dyn_smem<M, S, BLOCK, ASYNC>(ro);
     if (ro) {
-        cudaFuncSetAttribute(k_fused_r<M, LAT, SYM, S, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        k_fused_r<M, LAT, SYM, S, BLOCK, MINB, true><<<grid, BLOCK, dyn, s>>>(a);
+        cudaFuncSetAttribute(k_fused_r<M, LAT, SYM, S, BLOCK, MINB, ASYNC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        k_fused_r<M, LAT, SYM, S, BLOCK, MINB, ASYNC, true><<<grid, BLOCK, dyn, s>>>(a);
     } else {
-        k_fused_r<M, LAT, SYM, S, BLOCK, MINB, false><<<grid, BLOCK, 0, s>>>(a);
+        cudaFuncSetAttribute(k_fused_r<M, LAT, SYM, S, BLOCK, MINB, ASYNC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        k_fused_r<M, LAT, SYM, S, BLOCK, MINB, ASYNC, false><<<grid, BLOCK, dyn, s>>>(a);
     }
     return cudaGetLastError();
 }
 
-template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB>
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool ASYNC>
 static int fused_r_occ_t() {
-    constexpr size_t dyn = fused_r_dyn_smem<M, S, BLOCK>();
     int o1 = 0, o2 = 0;
-    cudaFuncSetAttribute(k_fused_r<M, LAT, SYM, S, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused_r<M, LAT, SYM, S, BLOCK, MINB, true>, BLOCK, dyn);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused_r<M, LAT, SYM, S, BLOCK, MINB, false>, BLOCK, 0);
+    const size_t d1 = fused_r_dyn_smem<M, S, BLOCK, ASYNC>(true), d2 = fused_r_dyn_smem<M, S, BLOCK, ASYNC>(false);
+    cudaFuncSetAttribute(k_fused_r<M, LAT, SYM, S, BLOCK, MINB, ASYNC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d1);
+    cudaFuncSetAttribute(k_fused_r<M, LAT, SYM, S, BLOCK, MINB, ASYNC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d2);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused_r<M, LAT, SYM, S, BLOCK, MINB, ASYNC, true>, BLOCK, d1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused_r<M, LAT, SYM, S, BLOCK, MINB, ASYNC, false>, BLOCK, d2);
+    return o1 < o2 ? o1 : o2;
+}
+
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool ASYNC>
+static cudaError_t fused_p_t(const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    const size_t dyn = ro ? (size_t)S * M * M * BLOCK * 16 : 0;
+    if (ro) {
+        cudaFuncSetAttribute(k_fused_p2<M, LAT, SYM, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        k_fused_p2<M, LAT, SYM, BLOCK, MINB, true><<<grid, BLOCK, dyn, s>>>(a);
+    } else {
+        k_fused_p2<M, LAT, SYM, BLOCK, MINB, false><<<grid, BLOCK, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool ASYNC>
+static int fused_p_occ_t() {
+    int o1 = 0, o2 = 0;
+    const size_t d1 = (size_t)S * M * M * BLOCK * 16;
+    cudaFuncSetAttribute(k_fused_p2<M, LAT, SYM, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused_p2<M, LAT, SYM, BLOCK, MINB, true>, BLOCK, d1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused_p2<M, LAT, SYM, BLOCK, MINB, false>, BLOCK, 0);
     return o1 < o2 ? o1 : o2;
 }
 
@@ -705,16 +1046,22 @@ static int fused_occ_t() {
 
 // M = 2: the lattice and general class maps give the same classes; the host uses LAT = false.
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
-    if (use_reg_variant(M, S, kind)) {
-#define X(M_, S_, B, V, MB)                                                                        \
-        if (M == M_ && S == S_) {                                                                  \
-            if (M_ == 2 && sym) return fused_r_t<M_, false, (M_ == 2), S_, B, MB>(a, ro, grid, s);  \
-            if (M_ > 2 && lattice) return fused_r_t<M_, (M_ > 2), false, S_, B, MB>(a, ro, grid, s); \
-            return fused_r_t<M_, false, false, S_, B, MB>(a, ro, grid, s);                          \
-        }
-        QP_FUSED_R_CFGS(X)
-#undef X
+#define X(M_, S_, B, V, MB, AS)                                                                   \
+    if (M == M_ && S == S_) {                                                                     \
+        if (M_ == 2 && sym) return fused_r_t<M_, false, (M_ == 2), S_, B, MB, AS>(a, ro, grid, s);\
+        if (M_ > 2 && lattice) return fused_r_t<M_, (M_ > 2), false, S_, B, MB, AS>(a, ro, grid, s); \
+        return fused_r_t<M_, false, false, S_, B, MB, AS>(a, ro, grid, s);                        \
     }
+    if (kind == 1) { QP_FUSED_R_CFGS(X) }
+    if (kind == 2) { QP_FUSED_A_CFGS(X) }
+#undef X
+#define X(M_, S_, B, V, MB, AS)                                                                   \
+    if (M == M_ && S == S_) {                                                                     \
+        if (M_ == 2 && sym) return fused_p_t<M_, false, (M_ == 2), S_, B, MB, AS>(a, ro, grid, s);\
+        return fused_p_t<M_, false, false, S_, B, MB, AS>(a, ro, grid, s);                        \
+    }
+    if (kind == 3) { QP_FUSED_P_CFGS(X) }
+#undef X
 #define X(M_, S_, B, V, TL, MB)                                                                   \
     if (M == M_ && S == S_) {                                                                     \
         if (M_ == 2 && sym) return fused_t<M_, false, (M_ == 2), S_, B, TL, MB>(a, ro, grid, s);   \
@@ -727,16 +1074,22 @@ cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const F
 }
 
 int fused_occupancy(int M, bool lattice, bool sym, int kind, int S) {
-    if (use_reg_variant(M, S, kind)) {
-#define X(M_, S_, B, V, MB)                                                             \
-        if (M == M_ && S == S_) {                                                       \
-            if (M_ == 2 && sym) return fused_r_occ_t<M_, false, (M_ == 2), S_, B, MB>();  \
-            if (M_ > 2 && lattice) return fused_r_occ_t<M_, (M_ > 2), false, S_, B, MB>(); \
-            return fused_r_occ_t<M_, false, false, S_, B, MB>();                          \
-        }
-        QP_FUSED_R_CFGS(X)
-#undef X
+#define X(M_, S_, B, V, MB, AS)                                                             \
+    if (M == M_ && S == S_) {                                                               \
+        if (M_ == 2 && sym) return fused_r_occ_t<M_, false, (M_ == 2), S_, B, MB, AS>();     \
+        if (M_ > 2 && lattice) return fused_r_occ_t<M_, (M_ > 2), false, S_, B, MB, AS>();   \
+        return fused_r_occ_t<M_, false, false, S_, B, MB, AS>();                             \
     }
+    if (kind == 1) { QP_FUSED_R_CFGS(X) }
+    if (kind == 2) { QP_FUSED_A_CFGS(X) }
+#undef X
+#define X(M_, S_, B, V, MB, AS)                                                             \
+    if (M == M_ && S == S_) {                                                               \
+        if (M_ == 2 && sym) return fused_p_occ_t<M_, false, (M_ == 2), S_, B, MB, AS>();     \
+        return fused_p_occ_t<M_, false, false, S_, B, MB, AS>();                             \
+    }
+    if (kind == 3) { QP_FUSED_P_CFGS(X) }
+#undef X
 #define X(M_, S_, B, V, TL, MB)                                                         \
     if (M == M_ && S == S_) {                                                           \
         if (M_ == 2 && sym) return fused_occ_t<M_, false, (M_ == 2), S_, B, TL, MB>();   \

@@ -106,8 +106,9 @@ struct GrowArgs {
 };
 
 FusedShape fused_shape(int M);
-// kind: 0 = warp-mapped k_fused, 1 = register k_fused_r (where a config exists for (M, S))
-bool has_reg_variant(int M, int S);
+// kind: 0 = warp-mapped k_fused, 1 = register k_fused_r, 2 = k_fused_r with cp.async staging
+// (kinds 1/2 where a config exists for (M, S), else the warp-mapped kernel)
+bool has_reg_variant(int M, int S, int kind);
 int fused_tile_digits(int M, int S, int kind);  // v: T = N^v outer fibres per tile
 int fused_block(int M, int S, int kind);
 // Launchers (kernels.cu).  Return cudaError_t of the launch.

@@ -178,7 +178,7 @@ def test_sigma_x_symmetry_full_size():
     assert np.abs(b - X @ a @ X).max() < 1e-12
 
 
-@pytest.mark.parametrize("kind", ["reg", "warp"])
+@pytest.mark.parametrize("kind", ["reg", "warp", "async", "split"])
 @pytest.mark.parametrize("nosym", [False, True])
 @pytest.mark.parametrize("fuse", [1, 2])
 @pytest.mark.parametrize("M,L,n", [(2, 2, 9), (2, 3, 12), (2, 5, 17), (2, 7, 20), (2, 8, 23), (3, 4, 11), (4, 3, 8)])
