@@ -38,12 +38,14 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def _ncu_traffic():
-    """Per-launch DRAM bytes of the slide kernel from the committed ncu --set full summary."""
+def _ncu_traffic(cfg: int):
+    """Per-launch DRAM bytes of the slide kernel from the committed ncu --set full summary
+    (profiles/ncu_slide_summary.json, captured on config 3); None for other workloads."""
     path = os.path.join(ROOT, "profiles", "ncu_slide_summary.json")
     try:
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch") if int(d.get("cfg", 3)) == cfg else None
     except Exception:
         return None
 
@@ -252,7 +254,7 @@ def main():
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "frac_of_8TBs": achieved / 8000.0,
-                         "traffic": _ncu_traffic(), "algorithmic_bytes_per_launch": bytes_launch,
+                         "traffic": _ncu_traffic(args.cfg), "algorithmic_bytes_per_launch": bytes_launch,
                          "steps_per_launch": K / max(1, launches)},
             "clocks": clk.summary(),
             "max_abs_trace_err": tr_err,
