@@ -592,8 +592,11 @@ void build_tables(qp_plan &P) {
     // ---- fused launch sets: for every start slot p0 and fusion depth S, the super-fibres of the
     //      inner slots p0..p0+S-1 and the factor / address tables of the L-S outer slots
     P.shape = qp::fused_shape(M);
+    // default: three fused steps per pass for M = 2 (k_fused3), else the register kernel
+    P.kind = (M == 2) ? 4 : 1;
+    if (const char *ek = std::getenv("QUAPI_FUSED_KIND")) P.kind = (ek[0] == 'w') ? 0 : (ek[0] == 'a' ? 2 : (ek[0] == 's' ? 3 : (ek[0] == '3' ? 4 : 1)));
     P.Smax = std::max(1, std::min(P.shape.S, L - 1));
-    if (const char *ek = std::getenv("QUAPI_FUSED_KIND")) P.kind = (ek[0] == 'w') ? 0 : (ek[0] == 'a' ? 2 : (ek[0] == 's' ? 3 : 1));
+    if (P.kind == 4 && M == 2) P.Smax = std::max(1, std::min(3, L - 1));
     if (const char *ev = std::getenv("QUAPI_FUSE_S")) P.Smax = std::max(1, std::min(P.Smax, std::atoi(ev)));
     P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
     for (int p0 = 0; p0 < L; ++p0)

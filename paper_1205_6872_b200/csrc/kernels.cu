@@ -843,6 +843,223 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_p2(const __grid_constant_
 }
 
 // --------------------------------------------------------------------------------------------
+// Three fused steps per HBM pass (M = 2, S = 3): the 64-entry super-fibre of an outer fibre is
+// held by 4 lanes of a warp (part j = lane >> 3 holds inner digit 2 = j: 16 entries), so sub-steps
+// 0 and 1 (fibres along digits 0 and 1) are lane-local; before sub-step 2 the four lanes transpose
+// digit 0 <-> digit 2 through a per-warp shared-memory buffer (two halves of 4 KB) and then hold
+// the fibres along digit 2.  Lane l works on outer fibre (l & 7) of the warp's 8; a CTA sweeps a
+// tile of T outer fibres in rounds of 8 * W.  Factor tables KU are CTA-wide per tile.
+// HBM traffic per step: 32/3 B per ARDM entry.
+// --------------------------------------------------------------------------------------------
+template <bool SYM, int BLOCK, int MINB, bool RO>
+__global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ FusedArgs a) {
+    constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2;
+    constexpr int NK = RO ? 2 : 1;
+    constexpr int W = BLOCK / 32;
+    constexpr bool LAT = false;
+    const SmallLayout lay{N, D, 0};
+    __shared__ double2 sK[2][N][N];
+    __shared__ double2 sIn[S][S][2][D][N];
+    __shared__ double2 KU[S][NK][Q][N][N];
+    __shared__ double2 sEhi[S][NK][D];
+    __shared__ long long sBase;
+    __shared__ int sLast;
+    // dynamic: per-warp exchange buffer [W][16][8] (a quarter of the super-fibre entries x 8 outer
+    // fibres), then the readout accumulators [S][N][BLOCK] (RO only)
+    extern __shared__ double2 dyn_smem[];
+    auto xch = reinterpret_cast<double2(*)[16][8]>(dyn_smem);
+    auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem + W * 16 * 8);
+    for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
+    for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
+    if constexpr (RO)
+        for (int s = 0; s < S; ++s)
+            for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane >> 3, t8 = lane & 7;
+    const int per = a.n_tiles / (int)gridDim.x, rem = a.n_tiles % (int)gridDim.x;
+    const int t_begin = (int)blockIdx.x * per + min((int)blockIdx.x, rem);
+    const int t_end = t_begin + per + ((int)blockIdx.x < rem ? 1 : 0);
+    constexpr int NKU = S * NK * Q * N * N;
+    const int rounds = (a.T + 8 * W - 1) / (8 * W);
+
+    // one fibre: xf holds the N old values; on return the N new values.  r = inner combination,
+    // last = value of the previous time point's slot.  acc: readout of this sub-step.
+    auto fibre = [&](double2 (&xf)[N], int s, int r, int last, bool ro, const double2 (&E0)[NK][D],
+                     double2 (&acc)[RO ? N : 1]) {
+        double2 S0, m[NK][D];
+        if constexpr (SYM) {
+            const double2 uu = cadd(xf[0], xf[3]), w = make_double2(xf[0].x - xf[3].x, xf[0].y - xf[3].y);
+            const double2 p = cadd(xf[1], xf[2]), q = make_double2(xf[1].x - xf[2].x, xf[1].y - xf[2].y);
+            S0 = cadd(uu, p);
+#pragma unroll
+            for (int kap = 0; kap < NK; ++kap) {
+                if (kap == 1 && !ro) break;
+                const double cr = a.sym[s][kap][0], ci = a.sym[s][kap][1], ch = a.sym[s][kap][2], sh = a.sym[s][kap][3];
+                const double2 A = make_double2(fma(cr, uu.x, ch * p.x), fma(cr, uu.y, ch * p.y));
+                const double2 Bv = make_double2(fma(-ci, w.y, sh * q.x), fma(ci, w.x, sh * q.y));
+                m[kap][0] = cadd(A, Bv);
+                m[kap][1] = make_double2(A.x - Bv.x, A.y - Bv.y);
+            }
+        } else {
+            S0 = cadd(cadd(xf[0], xf[1]), cadd(xf[2], xf[3]));
+#pragma unroll
+            for (int kap = 0; kap < NK; ++kap) {
+                if (kap == 1 && !ro) break;
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
+#pragma unroll
+                    for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                    m[kap][d] = mm;
+                }
+            }
+        }
+        const double2(&ku)[NK][Q][N][N] = KU[s];
+        if (ro) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const double2 pt = cmul(E0[NK - 1][d], m[NK - 1][d]);
+#pragma unroll
+                for (int nw = 0; nw < N; ++nw)
+                    if (class_of(M, LAT, nw / M, nw % M) == d + 1)
+                        acc[RO ? nw : 0] = cfma(ku[NK - 1][r][nw][last], pt, acc[RO ? nw : 0]);
+            }
+        }
+        double2 P[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) P[d] = cmul(E0[0][d], m[0][d]);
+#pragma unroll
+        for (int nw = 0; nw < N; ++nw) {
+            const int c = class_of(M, LAT, nw / M, nw % M);
+            const double2 o = cmul(ku[0][r][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
+            xf[nw] = o;
+            if (ro && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
+        }
+    };
+
+    for (int tau = t_begin; tau < t_end; ++tau) {
+        __syncthreads();  // previous tile's KU no longer in use
+        if ((int)threadIdx.x < S * NK * D) {
+            const int s = threadIdx.x / (NK * D), kap = (threadIdx.x / D) % NK, d = threadIdx.x % D;
+            double2 e = make_double2(1.0, 0.0);
+            for (int g = 1; g < a.G; ++g)
+                e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
+            sEhi[s][kap][d] = cmul(e, a.fixfac[s][kap][d]);
+        }
+        if ((int)threadIdx.x == BLOCK - 1) {
+            long long b = 0;
+            for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+            sBase = b;
+            sLast = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
+        }
+        __syncthreads();
+        for (int jj = threadIdx.x; jj < NKU; jj += BLOCK) {
+            const int last = jj % N, nw = (jj / N) % N, rr = (jj / (N * N)) % Q, kap = (jj / (N * N * Q)) % NK,
+                      s = jj / (N * N * Q * NK);
+            const int c = class_of(M, LAT, nw / M, nw % M);
+            double2 e = sK[kap][nw][last];
+            if (c > 0) {
+                e = cmul(e, sEhi[s][kap][c - 1]);
+                for (int i = 0; i < S; ++i)
+                    if (i != s) e = cmul(e, sIn[s][i][kap][c - 1][fib_digit<N, S>(s, rr, i)]);
+            }
+            KU[s][kap][rr][nw][last] = e;
+        }
+        __syncthreads();
+        const long long tbase = sBase;
+        const int last_t = sLast;
+        for (int rd = 0; rd < rounds; ++rd) {
+            const int t = rd * 8 * W + warp * 8 + t8;
+            const bool valid = t < a.T;
+            const int2 lo = valid ? __ldg(&a.lofs[t]) : make_int2(0, 0);
+            const long long base = tbase + lo.x;
+            double2 X[N][N];  // X[d1][d0], d2 = j
+            if (valid) {
+#pragma unroll
+                for (int d1 = 0; d1 < N; ++d1)
+#pragma unroll
+                    for (int d0 = 0; d0 < N; ++d0)
+                        X[d1][d0] = __ldcs(a.A + base + (long long)d0 * a.pw_in[0] + (long long)d1 * a.pw_in[1] +
+                                           (long long)j * a.pw_in[2]);
+            }
+            const int last0 = lo.y >= 0 ? lo.y : last_t;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s == 2) {  // transpose digit 0 <-> digit 2 among the 4 lanes of an outer fibre
+#pragma unroll
+                    for (int d1 = 0; d1 < N; ++d1) {  // one digit-1 value at a time (16 entries)
+                        if (valid) {
+#pragma unroll
+                            for (int d0 = 0; d0 < N; ++d0) xch[warp][d0 + 4 * j][t8] = X[d1][d0];
+                        }
+                        __syncwarp();
+                        if (valid) {  // X[d1][d2] := (digit0 = j, digit1 = d1, digit2 = d2)
+#pragma unroll
+                            for (int d2 = 0; d2 < N; ++d2) X[d1][d2] = xch[warp][j + 4 * d2][t8];
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (!valid) continue;
+                const bool ro = RO && a.rho[s] != nullptr;
+                double2 E0[NK][D];
+#pragma unroll
+                for (int kap = 0; kap < NK; ++kap)
+#pragma unroll
+                    for (int d = 0; d < D; ++d)
+                        E0[kap][d] = (kap == 0 || ro) ? __ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t])
+                                                      : make_double2(0.0, 0.0);
+                double2 acc[RO ? N : 1];
+#pragma unroll
+                for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
+                if (s == 0) {  // fibres along digit 0: X[d1][.], other digits (d1, d2 = j)
+#pragma unroll
+                    for (int d1 = 0; d1 < N; ++d1) fibre(X[d1], 0, d1 + 4 * j, last0, ro, E0, acc);
+                } else if (s == 1) {  // along digit 1: X[.][d0], other digits (d0, d2 = j); last = d0
+#pragma unroll
+                    for (int d0 = 0; d0 < N; ++d0) {
+                        double2 xf[N];
+#pragma unroll
+                        for (int v = 0; v < N; ++v) xf[v] = X[v][d0];
+                        fibre(xf, 1, d0 + 4 * j, d0, ro, E0, acc);
+#pragma unroll
+                        for (int v = 0; v < N; ++v) X[v][d0] = xf[v];
+                    }
+                } else {  // along digit 2: X[d1][.], other digits (d0 = j, d1); last = d1
+#pragma unroll
+                    for (int d1 = 0; d1 < N; ++d1) fibre(X[d1], 2, j + 4 * d1, d1, ro, E0, acc);
+                }
+                if (ro) {
+#pragma unroll
+                    for (int n = 0; n < N; ++n)
+                        accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0] =
+                            cadd(accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0], acc[RO ? n : 0]);
+                }
+            }
+            if (valid) {  // X[d1][d2] with digit 0 = j
+#pragma unroll
+                for (int d1 = 0; d1 < N; ++d1)
+#pragma unroll
+                    for (int d2 = 0; d2 < N; ++d2)
+                        __stcs(a.A + base + (long long)j * a.pw_in[0] + (long long)d1 * a.pw_in[1] + (long long)d2 * a.pw_in[2],
+                               X[d1][d2]);
+            }
+        }
+    }
+    if constexpr (RO) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (a.rho[s] != nullptr) {
+                double2 tt[N];
+#pragma unroll
+                for (int n = 0; n < N; ++n) tt[n] = accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0];
+                reduce_finalize<N, BLOCK>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
+                                          a.rho_accumulate != 0);
+            }
+    }
+}
+
+// --------------------------------------------------------------------------------------------
 // Growth step 1 <= k < L: A_{k-1} (digits 0..k-1) -> A_k (digits 0..k), in place:
 //   A_k[x + v N^k] = K'(v, d_{k-1}(x)) exp(Ds(v) Psi_k(x)) A_{k-1}[x],
 //   Psi_k(x) = sum_{j=1..k} psi_{k,j}(d_{k-j}(x)),   classes eta_j (j<k), E_k (j=k, partner sigma_0).
@@ -935,7 +1152,12 @@ FusedShape fused_shape(int M) {
 }
 
 // kind: 0 = warp-mapped k_fused, 1 = register k_fused_r, 2 = register k_fused_r with cp.async staging
+// kind 4: three fused steps per pass (k_fused3, M = 2); S < 3 launches of such a plan use kind 1
+static int eff_kind(int M, int S, int kind) { return kind == 4 ? ((M == 2 && S == 3) ? 4 : 1) : kind; }
+
 bool has_reg_variant(int M, int S, int kind) {
+    kind = eff_kind(M, S, kind);
+    if (kind == 4) return true;
     if (kind == 3) {
 #define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return true;
         QP_FUSED_P_CFGS(X)
@@ -955,6 +1177,8 @@ bool has_reg_variant(int M, int S, int kind) {
 }
 
 int fused_tile_digits(int M, int S, int kind) {
+    kind = eff_kind(M, S, kind);
+    if (kind == 4) return 5;
 #define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return V;
     if (kind == 1 && has_reg_variant(M, S, 1)) { QP_FUSED_R_CFGS(X) }
     if (kind == 2 && has_reg_variant(M, S, 2)) { QP_FUSED_A_CFGS(X) }
@@ -967,6 +1191,8 @@ int fused_tile_digits(int M, int S, int kind) {
 }
 
 int fused_block(int M, int S, int kind) {
+    kind = eff_kind(M, S, kind);
+    if (kind == 4) return 256;
 #define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return B;
     if (kind == 1 && has_reg_variant(M, S, 1)) { QP_FUSED_R_CFGS(X) }
     if (kind == 2 && has_reg_variant(M, S, 2)) { QP_FUSED_A_CFGS(X) }
@@ -1045,7 +1271,35 @@ static int fused_occ_t() {
 }
 
 // M = 2: the lattice and general class maps give the same classes; the host uses LAT = false.
+static size_t fused3_dyn(int block, bool ro) { return ((size_t)(block / 32) * 16 * 8 + (ro ? (size_t)3 * 4 * block : 0)) * 16; }
+
+template <bool SYM, int BLOCK, int MINB>
+static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    const size_t dyn = fused3_dyn(BLOCK, ro);
+    if (ro) {
+        cudaFuncSetAttribute(k_fused3<SYM, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        k_fused3<SYM, BLOCK, MINB, true><<<grid, BLOCK, dyn, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_fused3<SYM, BLOCK, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        k_fused3<SYM, BLOCK, MINB, false><<<grid, BLOCK, dyn, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+template <bool SYM, int BLOCK, int MINB>
+static int fused3_occ_t() {
+    int o1 = 0, o2 = 0;
+    const size_t d1 = fused3_dyn(BLOCK, true), d2 = fused3_dyn(BLOCK, false);
+    cudaFuncSetAttribute(k_fused3<SYM, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d1);
+    cudaFuncSetAttribute(k_fused3<SYM, BLOCK, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d2);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused3<SYM, BLOCK, MINB, true>, BLOCK, d1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused3<SYM, BLOCK, MINB, false>, BLOCK, d2);
+    return o1 < o2 ? o1 : o2;
+}
+
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    kind = eff_kind(M, S, kind);
+    if (kind == 4) return sym ? fused3_t<true, 256, 2>(a, ro, grid, s) : fused3_t<false, 256, 2>(a, ro, grid, s);
 #define X(M_, S_, B, V, MB, AS)                                                                   \
     if (M == M_ && S == S_) {                                                                     \
         if (M_ == 2 && sym) return fused_r_t<M_, false, (M_ == 2), S_, B, MB, AS>(a, ro, grid, s);\
@@ -1074,6 +1328,8 @@ cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const F
 }
 
 int fused_occupancy(int M, bool lattice, bool sym, int kind, int S) {
+    kind = eff_kind(M, S, kind);
+    if (kind == 4) return sym ? fused3_occ_t<true, 256, 2>() : fused3_occ_t<false, 256, 2>();
 #define X(M_, S_, B, V, MB, AS)                                                             \
     if (M == M_ && S == S_) {                                                               \
         if (M_ == 2 && sym) return fused_r_occ_t<M_, false, (M_ == 2), S_, B, MB, AS>();     \

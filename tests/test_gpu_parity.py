@@ -178,9 +178,9 @@ def test_sigma_x_symmetry_full_size():
     assert np.abs(b - X @ a @ X).max() < 1e-12
 
 
-@pytest.mark.parametrize("kind", ["reg", "warp", "async", "split"])
+@pytest.mark.parametrize("kind", ["reg", "warp", "async", "split", "3"])
 @pytest.mark.parametrize("nosym", [False, True])
-@pytest.mark.parametrize("fuse", [1, 2])
+@pytest.mark.parametrize("fuse", [1, 2, 3])
 @pytest.mark.parametrize("M,L,n", [(2, 2, 9), (2, 3, 12), (2, 5, 17), (2, 7, 20), (2, 8, 23), (3, 4, 11), (4, 3, 8)])
 def test_fusion_depths(fuse, M, L, n, nosym, kind, monkeypatch):
     """k_fused with 1 and 2 time steps per HBM pass (QUAPI_FUSE_S caps the depth) against the oracle;
@@ -195,7 +195,8 @@ def test_fusion_depths(fuse, M, L, n, nosym, kind, monkeypatch):
     for lat in (True, False) if M > 2 else (True,):
         w = W.random_problem(300 + 10 * M + L, M, L, n, kind=W.J_DEBYE, lattice_s=lat)
         rg, plan, _ = gpu_run(w)
-        assert plan.sizes.fuse_steps == (min(fuse, L - 1) if M == 2 else 1)
+        assert plan.sizes.fuse_steps == (min(fuse, L - 1, 3 if kind == "3" else 2) if M == 2 else 1)
+    # default plan (no QUAPI_FUSED_KIND): three fused steps per pass for M = 2
         check(rg, O.run(P(w)))
 
 
