@@ -851,6 +851,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_p2(const __grid_constant_
 // tile of T outer fibres in rounds of 8 * W.  Factor tables KU are CTA-wide per tile.
 // HBM traffic per step: 32/3 B per ARDM entry.
 // --------------------------------------------------------------------------------------------
+#ifndef QP_F3_PREFETCH
+#define QP_F3_PREFETCH 0
+#endif
+constexpr bool kF3Prefetch = QP_F3_PREFETCH;
+
 template <bool SYM, int BLOCK, int MINB, bool RO>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ FusedArgs a) {
     constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2;
@@ -981,6 +986,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                     for (int d0 = 0; d0 < N; ++d0)
                         X[d1][d0] = __ldcs(a.A + base + (long long)d0 * a.pw_in[0] + (long long)d1 * a.pw_in[1] +
                                            (long long)j * a.pw_in[2]);
+            }
+            if (kF3Prefetch && rd + 1 < rounds) {  // pull the next round of this tile into L2
+                const int tn = t + 8 * W;
+                if (tn < a.T) {
+                    const long long bn = tbase + __ldg(&a.lofs[tn]).x + (long long)j * a.pw_in[2];
+#pragma unroll
+                    for (int d1 = 0; d1 < N; ++d1)
+#pragma unroll
+                        for (int d0 = 0; d0 < N; ++d0)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.A + bn + (long long)d0 * a.pw_in[0] +
+                                                                        (long long)d1 * a.pw_in[1]));
+                }
             }
             const int last0 = lo.y >= 0 ? lo.y : last_t;
 #pragma unroll
