@@ -457,7 +457,12 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     for (int q = 0; q < L; ++q)
         if (pos[q] >= 0 && std::find(inner.begin(), inner.end(), q) == inner.end()) outer.push_back(q);  // ascending
     const int nout = (int)outer.size();
-    const int v = std::min(qp::fused_tile_digits(M, S, P.kind), nout), w = std::max(1, P.shape.w);
+    // tile digits: the kernel's preferred v, lowered (not below its minimum) so that small problems
+    // still have >= ~2 tiles per SM of a 148-SM B200 to spread over the persistent grid
+    int v = std::min(qp::fused_tile_digits(M, S, P.kind), nout);
+    const int vmin = std::min(qp::fused_tile_digits_min(M, S, P.kind), nout);
+    while (v > vmin && std::pow((double)N, nout - v) < 2.0 * 148) --v;
+    const int w = std::max(1, P.shape.w);
     const int hi = nout - v;
     const int G = 1 + (hi + w - 1) / w;
     const int T = (int)ipow(N, v);
@@ -846,14 +851,11 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
                 ro |= slot >= 0;
                 const int var = (k + st == P->L) ? 1 : 0;
                 const qp::SmallLayout lay{P->N, P->D, P->L};
-                for (int kap = 0; kap < 2; ++kap)
-                    for (int d = 0; d < P->D; ++d)
-                        for (int old = 0; old < P->N; ++old)
-                            a.beta[st][kap][d][old] = P->small[lay.beta(var, kap) + d * P->N + old];
+                a.var[st] = var;
                 if (P->sym) {  // class 1 = (0,1): beta_1 = (c, rho, 1/rho, conj c)
                     for (int kap = 0; kap < 2; ++kap) {
-                        const double2 c = a.beta[st][kap][0][0];
-                        const double rho = a.beta[st][kap][0][1].x;
+                        const double2 c = P->small[lay.beta(var, kap) + 0];
+                        const double rho = P->small[lay.beta(var, kap) + 1].x;
                         a.sym[st][kap][0] = c.x;
                         a.sym[st][kap][1] = c.y;
                         a.sym[st][kap][2] = 0.5 * (rho + 1.0 / rho);
@@ -1125,14 +1127,11 @@ qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_loc
                 a.rho[st] = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * N : nullptr;
                 ro |= slot >= 0;
                 const int var = (k + st == L) ? 1 : 0;
-                for (int kap = 0; kap < 2; ++kap)
-                    for (int d = 0; d < P->D; ++d)
-                        for (int old = 0; old < N; ++old)
-                            a.beta[st][kap][d][old] = P->small[lay.beta(var, kap) + d * N + old];
+                a.var[st] = var;
                 if (P->sym)
                     for (int kap = 0; kap < 2; ++kap) {
-                        const double2 c = a.beta[st][kap][0][0];
-                        const double rho = a.beta[st][kap][0][1].x;
+                        const double2 c = P->small[lay.beta(var, kap) + 0];
+                        const double rho = P->small[lay.beta(var, kap) + 1].x;
                         a.sym[st][kap][0] = c.x;
                         a.sym[st][kap][1] = c.y;
                         a.sym[st][kap][2] = 0.5 * (rho + 1.0 / rho);

@@ -147,6 +147,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
     __shared__ double2 xch[S > 1 ? cpow(N, S) * TILE : 1];  // [entry][outer fibre] exchange buffer
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
+    __shared__ double2 sBeta[S][2][D][N];  // beta_d(old) of each sub-step (first slide: initial-edge classes)
+    for (int i = threadIdx.x; i < S * 2 * D * N; i += BLOCK) {
+        const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
+        (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
+    }
 
     const int r = threadIdx.x / TILE, t = threadIdx.x % TILE;
     const bool valid = t < a.T && r < Q;
@@ -173,7 +178,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
     //   stage B (tile i+1): KU[s][kap][r][new][last] = KI * Ehi[s][kap][class(new)]
     // so KU holds every factor of output row `new` except the per-fibre outer group 0.
     constexpr int NKU = S * NK * Q * N * N;
-    __shared__ double2 KI[S][NK][Q][N][N];
+    // (for S = 1 there is no inner slot: KI would equal K', so it is not stored)
+    __shared__ double2 KI[S > 1 ? S : 1][S > 1 ? NK : 1][S > 1 ? Q : 1][S > 1 ? N : 1][S > 1 ? N : 1];
     __shared__ double2 KU[3][S][NK][Q][N][N];
     __shared__ double2 sEhi[4][S][NK][D];
     __shared__ long long sBase[4];
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
         if (c > 0)
             for (int i = 0; i < S; ++i)
                 if (i != s) e = cmul(e, sIn[s][i][kap][c - 1][fib_digit<N, S>(s, rr, i)]);
-        KI[s][kap][rr][nw][last] = e;
+        if constexpr (S > 1) KI[S > 1 ? s : 0][S > 1 ? kap : 0][S > 1 ? rr : 0][S > 1 ? nw : 0][S > 1 ? last : 0] = e;
     }
     auto stage_a = [&](int tau, int slot) {
         if ((int)threadIdx.x < S * NK * D) {
@@ -209,7 +215,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
             const int last = j % N, nw = (j / N) % N, rr = (j / (N * N)) % Q, kap = (j / (N * N * Q)) % NK,
                       s = j / (N * N * Q * NK);
             const int c = class_of(M, LAT, nw / M, nw % M);
-            const double2 e = KI[s][kap][rr][nw][last];
+            double2 e;
+            if constexpr (S > 1) e = KI[S > 1 ? s : 0][S > 1 ? kap : 0][S > 1 ? rr : 0][S > 1 ? nw : 0][S > 1 ? last : 0];
+            else e = sK[kap][nw][last];
             KU[kslot][s][kap][rr][nw][last] = c > 0 ? cmul(e, sEhi[aslot][s][kap][c - 1]) : e;
         }
     };
@@ -285,9 +293,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused(const __grid_constant__ F
                     if (kap == 1 && !ro) break;
 #pragma unroll
                     for (int d = 0; d < D; ++d) {
-                        double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
+                        double2 mm = cmul(sBeta[s][kap][d][0], xf[0]);
 #pragma unroll
-                        for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                        for (int v = 1; v < N; ++v) mm = cfma(sBeta[s][kap][d][v], xf[v], mm);
                         m[kap][d] = mm;
                     }
                 }
@@ -374,6 +382,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
+    __shared__ double2 sBeta[S][2][D][N];  // beta_d(old) of each sub-step (first slide: initial-edge classes)
+    for (int i = threadIdx.x; i < S * 2 * D * N; i += BLOCK) {
+        const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
+        (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
+    }
     if constexpr (RO)
         for (int s = 0; s < S; ++s)
             for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
@@ -543,9 +556,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__
                             if (kap == 1 && !ro) break;
 #pragma unroll
                             for (int d = 0; d < D; ++d) {
-                                double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
+                                double2 mm = cmul(sBeta[s][kap][d][0], xf[0]);
 #pragma unroll
-                                for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                                for (int v = 1; v < N; ++v) mm = cfma(sBeta[s][kap][d][v], xf[v], mm);
                                 m[kap][d] = mm;
                             }
                         }
@@ -633,6 +646,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_p2(const __grid_constant_
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
+    __shared__ double2 sBeta[S][2][D][N];  // beta_d(old) of each sub-step (first slide: initial-edge classes)
+    for (int i = threadIdx.x; i < S * 2 * D * N; i += BLOCK) {
+        const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
+        (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
+    }
     if constexpr (RO)
         for (int s = 0; s < S; ++s)
             for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
@@ -781,9 +799,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_p2(const __grid_constant_
                         if (kap == 1 && !ro) break;
 #pragma unroll
                         for (int d = 0; d < D; ++d) {
-                            double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
+                            double2 mm = cmul(sBeta[s][kap][d][0], xf[0]);
 #pragma unroll
-                            for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                            for (int v = 1; v < N; ++v) mm = cfma(sBeta[s][kap][d][v], xf[v], mm);
                             m[kap][d] = mm;
                         }
                     }
@@ -876,6 +894,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem + W * 16 * 8);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
+    __shared__ double2 sBeta[S][2][D][N];  // beta_d(old) of each sub-step (first slide: initial-edge classes)
+    for (int i = threadIdx.x; i < S * 2 * D * N; i += BLOCK) {
+        const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
+        (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
+    }
     if constexpr (RO)
         for (int s = 0; s < S; ++s)
             for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
@@ -912,9 +935,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 if (kap == 1 && !ro) break;
 #pragma unroll
                 for (int d = 0; d < D; ++d) {
-                    double2 mm = cmul(a.beta[s][kap][d][0], xf[0]);
+                    double2 mm = cmul(sBeta[s][kap][d][0], xf[0]);
 #pragma unroll
-                    for (int v = 1; v < N; ++v) mm = cfma(a.beta[s][kap][d][v], xf[v], mm);
+                    for (int v = 1; v < N; ++v) mm = cfma(sBeta[s][kap][d][v], xf[v], mm);
                     m[kap][d] = mm;
                 }
             }
@@ -1205,6 +1228,15 @@ int fused_tile_digits(int M, int S, int kind) {
     QP_FUSED_CFGS(X)
 #undef X
     return -1;
+}
+
+int fused_tile_digits_min(int M, int S, int kind) {
+    kind = eff_kind(M, S, kind);
+    const int N = M * M;
+    if (kind == 4) return 3;                   // k_fused3: a round is 8 warps x 8 outer fibres = 64
+    if (kind == 0) return fused_tile_digits(M, S, kind);  // k_fused: compile-time TILE
+    if (kind == 3) return N >= 16 ? 1 : 2;     // k_fused_p2: chunks of 16 outer fibres
+    return N >= 9 ? 2 : 3;                     // k_fused_r (+async): chunks of 32 outer fibres
 }
 
 int fused_block(int M, int S, int kind) {

@@ -61,10 +61,8 @@ struct FusedArgs {
     int last_div;            // sub-step 0 'last' digit is a tile digit: (tau / last_div) % N; else -1
     int fixed_last;          // sub-step 0 'last' slot is a (fixed) shard slot: its value; else -1
     int rho_accumulate;      // 1: rho[n] += sum (several shard blocks contribute to one step)
-    // beta_d(old) = exp(delta_d psi_L(old)) of each sub-step (kernel-parameter constant bank):
-    // [sub-step][0 propagate / 1 terminal][class][old]; the first slide step k == L uses the
-    // initial-edge classes (partner sigma_0)
-    double2 beta[kMaxS][2][kMaxD][kMaxN];
+    int var[kMaxS];          // beta variant per sub-step: 1 for the first slide step k == L (initial-edge
+                             // classes of the partner sigma_0), else 0 (SmallLayout::beta)
     // M = 2, s = (+s, -s): beta_1 = (c, rho, 1/rho, conj c); {Re c, Im c, (rho+1/rho)/2, (rho-1/rho)/2}
     double sym[kMaxS][2][4];
     // sharded layouts: factor of the fixed shard-slot digits of this block, per sub-step / kind / class
@@ -109,7 +107,8 @@ FusedShape fused_shape(int M);
 // kind: 0 = warp-mapped k_fused, 1 = register k_fused_r, 2 = k_fused_r with cp.async staging
 // (kinds 1/2 where a config exists for (M, S), else the warp-mapped kernel)
 bool has_reg_variant(int M, int S, int kind);
-int fused_tile_digits(int M, int S, int kind);  // v: T = N^v outer fibres per tile
+int fused_tile_digits(int M, int S, int kind);      // preferred v: T = N^v outer fibres per tile
+int fused_tile_digits_min(int M, int S, int kind);  // smallest v the kernel supports
 int fused_block(int M, int S, int kind);
 // Launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool readout, int grid, cudaStream_t s);
