@@ -336,6 +336,7 @@ struct qp_plan {
     size_t off_small = 0, off_part = 0, off_rho = 0, off_cnt = 0, tables_end = 0, work_bytes = 0;
     int64_t ardm_entries = 0;
     int grid[qp::kMaxS + 1] = {0};
+    int occ[qp::kMaxS + 1][2] = {};    // resident CTAs per SM of the fused kernel per (S, lane map)
     int sms = 0;
     int64_t next_k = 1;
     bool inited = false;
@@ -441,6 +442,14 @@ qp_status compute_eta(qp_plan &P, const qp_problem &pr) {
     return QP_OK;
 }
 
+// Persistent grid of one fused launch: fixed per (plan, launch set, device type), so the readout
+// order (block partials) is deterministic.
+static int launch_grid(qp_plan *P, int S, const qp::FusedArgs &a) {
+    int &o = P->occ[S][a.lane_map & 1];
+    if (o == 0) o = std::max(1, qp::fused_occupancy(P->M, P->lattice, P->sym, P->kind, S, a.lane_map));
+    return std::max(1, std::min<int>({a.n_tiles, P->sms * o, qp::kPartialsMax}));
+}
+
 // Tables of one fused launch over inner slots p0..p0+S-1 (mod L) of a local layout from which the
 // shard slots `removed` are absent (empty for an unsharded plan).
 void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &removed, qp_plan::LaunchSet &ls) {
@@ -535,6 +544,9 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     }
     a.last_div = (ilast >= v && ilast < nout) ? (int)ipow(N, ilast - v) : -1;
     a.fixed_last = -1;  // set per launch when sub-step 0's 'last' slot is a shard slot
+    // k_fused3 lane map 1 (32 consecutive fibres per warp load) when fibres t, t+1 are adjacent
+    a.lane_map = (T >= 64 && ls.lofs[1].x == 1) ? 1 : 0;
+    if (const char *e = std::getenv("QUAPI_F3MAP")) a.lane_map = (e[0] == '1' && T >= 64) ? 1 : 0;
     for (int st = 0; st < qp::kMaxS; ++st)
         for (int kap = 0; kap < 2; ++kap)
             for (int d = 0; d < qp::kMaxD; ++d) a.fixfac[st][kap][d] = make_double2(1.0, 0.0);
@@ -863,7 +875,7 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
                     }
                 }
             }
-            e = qp::launch_fused(P->M, P->lattice, P->sym, P->kind, S, a, ro, P->grid[S], s);
+            e = qp::launch_fused(P->M, P->lattice, P->sym, P->kind, S, a, ro, launch_grid(P, S, a), s);
             adv = S;
         }
         if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
@@ -1151,7 +1163,7 @@ qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_loc
             a.fixed_last = -1;
             for (int i = 0; i < sh.z; ++i)
                 if (Z[i] == qlast) a.fixed_last = dig[i];
-            const cudaError_t e = qp::launch_fused(P->M, P->lattice, P->sym, P->kind, S, a, ro, P->grid[S], s);
+            const cudaError_t e = qp::launch_fused(P->M, P->lattice, P->sym, P->kind, S, a, ro, launch_grid(P, S, a), s);
             if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: shard launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
             ++launched;
         }

@@ -869,12 +869,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused_p2(const __grid_constant_
 // tile of T outer fibres in rounds of 8 * W.  Factor tables KU are CTA-wide per tile.
 // HBM traffic per step: 32/3 B per ARDM entry.
 // --------------------------------------------------------------------------------------------
-#ifndef QP_F3_PREFETCH
-#define QP_F3_PREFETCH 0
-#endif
-constexpr bool kF3Prefetch = QP_F3_PREFETCH;
 
-template <bool SYM, int BLOCK, int MINB, bool RO>
+// KU row swizzle: the 16 entries (new, last) of KU row r are stored at (4 new + last) ^ f(r).  The
+// lanes of a warp read rows r = d + 4j (sub-steps 0, 1) or j + 4d (sub-step 2) for their digit-2
+// value j; rows are 256 B apart (same banks), so without the swizzle the 4 rows conflict 4-way.
+// f(r) = g(r / 4) ^ g(r % 4), g(x) = 4 (x & 1) + x / 2: distinct 16-B bank groups for the 4 rows,
+// and at most 2-way for sub-step 0 whose 'last' also varies across lanes.
+__device__ __forceinline__ int f3_swizzle(int r) {
+    const int hi = r >> 2, lo = r & 3;
+    return (((hi & 1) << 2) | (hi >> 1)) ^ (((lo & 1) << 2) | (lo >> 1));
+}
+
+template <bool SYM, int MAP, int BLOCK, int MINB, bool PF, bool RO>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ FusedArgs a) {
     constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2;
     constexpr int NK = RO ? 2 : 1;
@@ -890,7 +896,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     // dynamic: per-warp exchange buffer [W][16][8] (a quarter of the super-fibre entries x 8 outer
     // fibres), then the readout accumulators [S][N][BLOCK] (RO only)
     extern __shared__ double2 dyn_smem[];
-    auto xch = reinterpret_cast<double2(*)[16][8]>(dyn_smem);
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem + W * 16 * 8);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
@@ -902,8 +907,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     if constexpr (RO)
         for (int s = 0; s < S; ++s)
             for (int n = 0; n < N; ++n) accS[s][n][threadIdx.x] = make_double2(0.0, 0.0);
+    static_assert(MAP == 0 || W % 4 == 0, "lane map 1: groups of 4 warps (one per digit-2 value)");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int j = lane >> 3, t8 = lane & 7;
+    // lane map 0: lane = (j, t8), 8 outer fibres per warp, the 4 quarters of a super-fibre in one warp
+    // lane map 1: lane = one of 32 consecutive outer fibres, warp -> j (512 contiguous bytes per load
+    //             when the lowest ARDM digit is an outer digit); quarters exchanged across 4 warps
+    const int j = MAP == 0 ? lane >> 3 : warp & 3;
+    const int fib = MAP == 0 ? warp * 8 + (lane & 7) : (warp >> 2) * 32 + lane;  // fibre within a round
+    // map 0: [W][16][8] per warp; map 1: [16][8 W] (same size)
+    auto xch_at = [&](int e) -> double2 & {
+        return MAP == 0 ? dyn_smem[(warp * 16 + e) * 8 + (lane & 7)] : dyn_smem[e * 8 * W + fib];
+    };
     const int per = a.n_tiles / (int)gridDim.x, rem = a.n_tiles % (int)gridDim.x;
     const int t_begin = (int)blockIdx.x * per + min((int)blockIdx.x, rem);
     const int t_end = t_begin + per + ((int)blockIdx.x < rem ? 1 : 0);
@@ -942,16 +956,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 }
             }
         }
-        const double2(&ku)[NK][Q][N][N] = KU[s];
-        if (ro) {
+        const int sw = MAP == 0 ? f3_swizzle(r) : 0;
+        const double2 *ku0 = &KU[s][0][r][0][0], *ku1 = &KU[s][NK - 1][r][0][0];
+        if (ro) {  // off-diagonal readout without the outer factor E0 (applied once per step below)
 #pragma unroll
-            for (int d = 0; d < D; ++d) {
-                const double2 pt = cmul(E0[NK - 1][d], m[NK - 1][d]);
+            for (int d = 0; d < D; ++d)
 #pragma unroll
                 for (int nw = 0; nw < N; ++nw)
                     if (class_of(M, LAT, nw / M, nw % M) == d + 1)
-                        acc[RO ? nw : 0] = cfma(ku[NK - 1][r][nw][last], pt, acc[RO ? nw : 0]);
-            }
+                        acc[RO ? nw : 0] = cfma(ku1[(nw * N + last) ^ sw], m[NK - 1][d], acc[RO ? nw : 0]);
         }
         double2 P[D];
 #pragma unroll
@@ -959,11 +972,37 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
 #pragma unroll
         for (int nw = 0; nw < N; ++nw) {
             const int c = class_of(M, LAT, nw / M, nw % M);
-            const double2 o = cmul(ku[0][r][nw][last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
+            const double2 o = cmul(ku0[(nw * N + last) ^ sw], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
             xf[nw] = o;
             if (ro && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
         }
     };
+
+    // tile base offset (outer digit groups >= 1) and one unit's loads: unit = (tile tau, round rd),
+    // lane -> outer fibre t = rd 8W + 8 warp + t8 and digit-2 value j; X[d1][d0]
+    auto tile_base = [&](int tau) {
+        long long b = 0;
+        for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+        return b;
+    };
+    auto load_unit = [&](int tau, int rd, double2 (&Y)[N][N], int2 &lo) {
+        const int t = rd * 8 * W + fib;
+        if (t < a.T) {
+            lo = __ldg(&a.lofs[t]);
+            const long long base = tile_base(tau) + lo.x + (long long)j * a.pw_in[2];
+#pragma unroll
+            for (int d1 = 0; d1 < N; ++d1)
+#pragma unroll
+                for (int d0 = 0; d0 < N; ++d0)
+                    Y[d1][d0] = __ldcs(a.A + base + (long long)d0 * a.pw_in[0] + (long long)d1 * a.pw_in[1]);
+        } else {
+            lo = make_int2(0, 0);
+        }
+    };
+    double2 Xn[PF ? N : 1][PF ? N : 1];  // PF: the next unit's super-fibre quarter, in flight
+    int2 lon = make_int2(0, 0);
+    if constexpr (PF)
+        if (t_begin < t_end) load_unit(t_begin, 0, Xn, lon);
 
     for (int tau = t_begin; tau < t_end; ++tau) {
         __syncthreads();  // previous tile's KU no longer in use
@@ -991,37 +1030,28 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 for (int i = 0; i < S; ++i)
                     if (i != s) e = cmul(e, sIn[s][i][kap][c - 1][fib_digit<N, S>(s, rr, i)]);
             }
-            KU[s][kap][rr][nw][last] = e;
+            (&KU[s][kap][rr][0][0])[(nw * N + last) ^ (MAP == 0 ? f3_swizzle(rr) : 0)] = e;
         }
         __syncthreads();
         const long long tbase = sBase;
         const int last_t = sLast;
         for (int rd = 0; rd < rounds; ++rd) {
-            const int t = rd * 8 * W + warp * 8 + t8;
+            const int t = rd * 8 * W + fib;
             const bool valid = t < a.T;
-            const int2 lo = valid ? __ldg(&a.lofs[t]) : make_int2(0, 0);
-            const long long base = tbase + lo.x;
+            int2 lo;
             double2 X[N][N];  // X[d1][d0], d2 = j
-            if (valid) {
+            if constexpr (PF) {  // this unit was loaded one unit ago; issue the next unit's loads now
 #pragma unroll
                 for (int d1 = 0; d1 < N; ++d1)
 #pragma unroll
-                    for (int d0 = 0; d0 < N; ++d0)
-                        X[d1][d0] = __ldcs(a.A + base + (long long)d0 * a.pw_in[0] + (long long)d1 * a.pw_in[1] +
-                                           (long long)j * a.pw_in[2]);
+                    for (int d0 = 0; d0 < N; ++d0) X[d1][d0] = Xn[d1][d0];
+                lo = lon;
+                const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
+                if (taun < t_end) load_unit(taun, rn, Xn, lon);
+            } else {
+                load_unit(tau, rd, X, lo);
             }
-            if (kF3Prefetch && rd + 1 < rounds) {  // pull the next round of this tile into L2
-                const int tn = t + 8 * W;
-                if (tn < a.T) {
-                    const long long bn = tbase + __ldg(&a.lofs[tn]).x + (long long)j * a.pw_in[2];
-#pragma unroll
-                    for (int d1 = 0; d1 < N; ++d1)
-#pragma unroll
-                        for (int d0 = 0; d0 < N; ++d0)
-                            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.A + bn + (long long)d0 * a.pw_in[0] +
-                                                                        (long long)d1 * a.pw_in[1]));
-                }
-            }
+            const long long base = tbase + lo.x;
             const int last0 = lo.y >= 0 ? lo.y : last_t;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
@@ -1030,25 +1060,24 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                     for (int d1 = 0; d1 < N; ++d1) {  // one digit-1 value at a time (16 entries)
                         if (valid) {
 #pragma unroll
-                            for (int d0 = 0; d0 < N; ++d0) xch[warp][d0 + 4 * j][t8] = X[d1][d0];
+                            for (int d0 = 0; d0 < N; ++d0) xch_at(d0 + 4 * j) = X[d1][d0];
                         }
-                        __syncwarp();
+                        if constexpr (MAP == 0) __syncwarp(); else __syncthreads();
                         if (valid) {  // X[d1][d2] := (digit0 = j, digit1 = d1, digit2 = d2)
 #pragma unroll
-                            for (int d2 = 0; d2 < N; ++d2) X[d1][d2] = xch[warp][j + 4 * d2][t8];
+                            for (int d2 = 0; d2 < N; ++d2) X[d1][d2] = xch_at(j + 4 * d2);
                         }
-                        __syncwarp();
+                        if constexpr (MAP == 0) __syncwarp(); else __syncthreads();
                     }
                 }
                 if (!valid) continue;
                 const bool ro = RO && a.rho[s] != nullptr;
-                double2 E0[NK][D];
+                double2 E0[NK][D];  // outer group-0 factor (kap = 1, readout: loaded at the end of the step)
 #pragma unroll
-                for (int kap = 0; kap < NK; ++kap)
-#pragma unroll
-                    for (int d = 0; d < D; ++d)
-                        E0[kap][d] = (kap == 0 || ro) ? __ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t])
-                                                      : make_double2(0.0, 0.0);
+                for (int d = 0; d < D; ++d) {
+                    E0[0][d] = __ldg(&a.Etab[((size_t)s * 2 * a.G * D + d) * a.X + t]);
+                    E0[NK - 1][d] = E0[0][d];
+                }
                 double2 acc[RO ? N : 1];
 #pragma unroll
                 for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
@@ -1070,6 +1099,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                     for (int d1 = 0; d1 < N; ++d1) fibre(X[d1], 2, j + 4 * d1, d1, ro, E0, acc);
                 }
                 if (ro) {
+                    // the outer factor E0 (fixed for this thread's outer fibre) of the off-diagonal
+                    // readout rows, factored out of the sum over its four fibres
+#pragma unroll
+                    for (int n = 0; n < N; ++n) {
+                        const int c = class_of(M, LAT, n / M, n % M);
+                        if (c > 0)
+                            acc[RO ? n : 0] = cmul(__ldg(&a.Etab[(((size_t)s * 2 + 1) * a.G * D + (c > 0 ? c - 1 : 0)) * a.X + t]),
+                                                   acc[RO ? n : 0]);
+                    }
 #pragma unroll
                     for (int n = 0; n < N; ++n)
                         accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0] =
@@ -1195,6 +1233,23 @@ FusedShape fused_shape(int M) {
 // kind 4: three fused steps per pass (k_fused3, M = 2); S < 3 launches of such a plan use kind 1
 static int eff_kind(int M, int S, int kind) { return kind == 4 ? ((M == 2 && S == 3) ? 4 : 1) : kind; }
 
+// k_fused3 launch variants (index, lane map, BLOCK, MINB, PF = register prefetch of the next unit).
+// The lane map is fixed per launch set (FusedArgs::lane_map); QUAPI_F3 = index selects a variant of
+// that map for tuning, else the map's default (no register spills at 168 registers).
+#define QP_F3_CFGS(X)                                                                             \
+    X(0, 0, 256, 2, false) X(1, 0, 192, 2, false) X(2, 0, 128, 3, false) X(3, 1, 128, 3, false)   \
+    X(4, 1, 256, 1, false) X(5, 1, 384, 1, false) X(6, 1, 128, 2, true)
+static int f3_variant(int map) {
+    const int def = map == 0 ? 1 : 3;
+    const char *e = std::getenv("QUAPI_F3");
+    if (!e) return def;
+    const int v = std::atoi(e);
+#define X(I, MP, B, MB, PF) if (v == I) return MP == map ? I : def;
+    QP_F3_CFGS(X)
+#undef X
+    return def;
+}
+
 bool has_reg_variant(int M, int S, int kind) {
     kind = eff_kind(M, S, kind);
     if (kind == 4) return true;
@@ -1241,7 +1296,11 @@ int fused_tile_digits_min(int M, int S, int kind) {
 
 int fused_block(int M, int S, int kind) {
     kind = eff_kind(M, S, kind);
-    if (kind == 4) return 256;
+    if (kind == 4) {
+#define X(I, MP, B, MB, PF) if (f3_variant(0) == I) return B;
+        QP_F3_CFGS(X)
+#undef X
+    }
 #define X(M_, S_, B, V, MB, AS) if (M == M_ && S == S_) return B;
     if (kind == 1 && has_reg_variant(M, S, 1)) { QP_FUSED_R_CFGS(X) }
     if (kind == 2 && has_reg_variant(M, S, 2)) { QP_FUSED_A_CFGS(X) }
@@ -1322,33 +1381,39 @@ static int fused_occ_t() {
 // M = 2: the lattice and general class maps give the same classes; the host uses LAT = false.
 static size_t fused3_dyn(int block, bool ro) { return ((size_t)(block / 32) * 16 * 8 + (ro ? (size_t)3 * 4 * block : 0)) * 16; }
 
-template <bool SYM, int BLOCK, int MINB>
+template <bool SYM, int MAP, int BLOCK, int MINB, bool PF>
 static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
     const size_t dyn = fused3_dyn(BLOCK, ro);
     if (ro) {
-        cudaFuncSetAttribute(k_fused3<SYM, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        k_fused3<SYM, BLOCK, MINB, true><<<grid, BLOCK, dyn, s>>>(a);
+        cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        k_fused3<SYM, MAP, BLOCK, MINB, PF, true><<<grid, BLOCK, dyn, s>>>(a);
     } else {
-        cudaFuncSetAttribute(k_fused3<SYM, BLOCK, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        k_fused3<SYM, BLOCK, MINB, false><<<grid, BLOCK, dyn, s>>>(a);
+        cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        k_fused3<SYM, MAP, BLOCK, MINB, PF, false><<<grid, BLOCK, dyn, s>>>(a);
     }
     return cudaGetLastError();
 }
 
-template <bool SYM, int BLOCK, int MINB>
+template <bool SYM, int MAP, int BLOCK, int MINB, bool PF>
 static int fused3_occ_t() {
     int o1 = 0, o2 = 0;
     const size_t d1 = fused3_dyn(BLOCK, true), d2 = fused3_dyn(BLOCK, false);
-    cudaFuncSetAttribute(k_fused3<SYM, BLOCK, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d1);
-    cudaFuncSetAttribute(k_fused3<SYM, BLOCK, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d2);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused3<SYM, BLOCK, MINB, true>, BLOCK, d1);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused3<SYM, BLOCK, MINB, false>, BLOCK, d2);
+    cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d1);
+    cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d2);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, BLOCK, d1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused3<SYM, MAP, BLOCK, MINB, PF, false>, BLOCK, d2);
     return o1 < o2 ? o1 : o2;
 }
 
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
     kind = eff_kind(M, S, kind);
-    if (kind == 4) return sym ? fused3_t<true, 256, 2>(a, ro, grid, s) : fused3_t<false, 256, 2>(a, ro, grid, s);
+    if (kind == 4) {
+#define X(I, MP, B, MB, PF)                                                                          \
+        if (f3_variant(a.lane_map) == I)                                                                 \
+            return sym ? fused3_t<true, MP, B, MB, PF>(a, ro, grid, s) : fused3_t<false, MP, B, MB, PF>(a, ro, grid, s);
+        QP_F3_CFGS(X)
+#undef X
+    }
 #define X(M_, S_, B, V, MB, AS)                                                                   \
     if (M == M_ && S == S_) {                                                                     \
         if (M_ == 2 && sym) return fused_r_t<M_, false, (M_ == 2), S_, B, MB, AS>(a, ro, grid, s);\
@@ -1376,9 +1441,14 @@ cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const F
     return cudaErrorInvalidValue;
 }
 
-int fused_occupancy(int M, bool lattice, bool sym, int kind, int S) {
+int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int lane_map) {
     kind = eff_kind(M, S, kind);
-    if (kind == 4) return sym ? fused3_occ_t<true, 256, 2>() : fused3_occ_t<false, 256, 2>();
+    if (kind == 4) {
+#define X(I, MP, B, MB, PF) \
+        if (f3_variant(lane_map) == I) return sym ? fused3_occ_t<true, MP, B, MB, PF>() : fused3_occ_t<false, MP, B, MB, PF>();
+        QP_F3_CFGS(X)
+#undef X
+    }
 #define X(M_, S_, B, V, MB, AS)                                                             \
     if (M == M_ && S == S_) {                                                               \
         if (M_ == 2 && sym) return fused_r_occ_t<M_, false, (M_ == 2), S_, B, MB, AS>();     \

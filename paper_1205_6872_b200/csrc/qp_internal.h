@@ -61,6 +61,7 @@ struct FusedArgs {
     int last_div;            // sub-step 0 'last' digit is a tile digit: (tau / last_div) % N; else -1
     int fixed_last;          // sub-step 0 'last' slot is a (fixed) shard slot: its value; else -1
     int rho_accumulate;      // 1: rho[n] += sum (several shard blocks contribute to one step)
+    int lane_map;            // k_fused3 lane map (kernels.cu): 1 when tile fibres t, t+1 are adjacent in HBM
     int var[kMaxS];          // beta variant per sub-step: 1 for the first slide step k == L (initial-edge
                              // classes of the partner sigma_0), else 0 (SmallLayout::beta)
     // M = 2, s = (+s, -s): beta_1 = (c, rho, 1/rho, conj c); {Re c, Im c, (rho+1/rho)/2, (rho-1/rho)/2}
@@ -112,7 +113,7 @@ int fused_tile_digits_min(int M, int S, int kind);  // smallest v the kernel sup
 int fused_block(int M, int S, int kind);
 // Launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool readout, int grid, cudaStream_t s);
-int fused_occupancy(int M, bool lattice, bool sym, int kind, int S);  // resident CTAs per SM (needs a device)
+int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int lane_map = 0);  // resident CTAs per SM (needs a device)
 cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaStream_t s);
 
 }  // namespace qp
