@@ -329,6 +329,9 @@ struct qp_plan {
         std::vector<int2> lofs;        // [T]
         size_t off_inner = 0, off_E = 0, off_goff = 0, off_lofs = 0;
         qp::FusedArgs args{};          // table pointers filled in qp_steps
+        int tma_a = -1, tma_b = 0;     // k_fused3 TMA view: run A = slots 0..tma_a-1, run B = tma_b slots
+        mutable const void *tma_A = nullptr;  // ARDM pointer the cached tensor map was encoded for
+        mutable CUtensorMap tmap{};
     };
     qp::FusedShape shape{};
     int Smax = 1;
@@ -336,7 +339,7 @@ struct qp_plan {
     size_t off_small = 0, off_part = 0, off_rho = 0, off_cnt = 0, tables_end = 0, work_bytes = 0;
     int64_t ardm_entries = 0;
     int grid[qp::kMaxS + 1] = {0};
-    int occ[qp::kMaxS + 1][2] = {};    // resident CTAs per SM of the fused kernel per (S, lane map)
+    int occ[qp::kMaxS + 1][4] = {};    // resident CTAs per SM of the fused kernel per (S, k_fused3 mode)
     int sms = 0;
     int64_t next_k = 1;
     bool inited = false;
@@ -442,11 +445,51 @@ qp_status compute_eta(qp_plan &P, const qp_problem &pr) {
     return QP_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static const EncodeTiledFn fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return (EncodeTiledFn)f;
+    }();
+    return fn;
+}
+
+// k_fused3's TMA view of the ARDM for launch set ls: 5-D tensor of FP64 (run A as 2 x N^a doubles,
+// run B, inner d0, d1, d2), box = one round of F outer fibres x N^3 inner entries.  Returns false
+// (the kernel then loads with plain LDG) if the driver cannot encode it.
+static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, double2 *A, int F) {
+    if (ls.tma_A == A) return true;
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const int p0 = ls.p0;
+    const cuuint64_t nA = (cuuint64_t)ipow(P.N, ls.tma_a), nB = (cuuint64_t)ipow(P.N, ls.tma_b);
+    const cuuint64_t boxA = std::min<cuuint64_t>(nA, (cuuint64_t)F);
+    if (nA * nB < (cuuint64_t)F || (cuuint64_t)F % boxA) return false;
+    const cuuint64_t gdim[5] = {2 * nA, nB, 4, 4, 4};
+    const cuuint64_t gstr[4] = {16ull * ipow(P.N, p0 + 3), 16ull * ipow(P.N, p0), 16ull * ipow(P.N, p0 + 1),
+                                16ull * ipow(P.N, p0 + 2)};
+    const cuuint32_t box[5] = {(cuuint32_t)(2 * boxA), (cuuint32_t)(F / boxA), 4, 4, 4};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (enc(&ls.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)A, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    ls.tma_A = A;
+    return true;
+}
+
 // Persistent grid of one fused launch: fixed per (plan, launch set, device type), so the readout
 // order (block partials) is deterministic.
 static int launch_grid(qp_plan *P, int S, const qp::FusedArgs &a) {
-    int &o = P->occ[S][a.lane_map & 1];
-    if (o == 0) o = std::max(1, qp::fused_occupancy(P->M, P->lattice, P->sym, P->kind, S, a.lane_map));
+    const int mode = (a.lane_map & 1) + (a.use_tma ? 2 : 0);
+    int &o = P->occ[S][mode];
+    if (o == 0) o = std::max(1, qp::fused_occupancy(P->M, P->lattice, P->sym, P->kind, S, mode));
     return std::max(1, std::min<int>({a.n_tiles, P->sms * o, qp::kPartialsMax}));
 }
 
@@ -547,6 +590,12 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     // k_fused3 lane map 1 (32 consecutive fibres per warp load) when fibres t, t+1 are adjacent
     a.lane_map = (T >= 64 && ls.lofs[1].x == 1) ? 1 : 0;
     if (const char *e = std::getenv("QUAPI_F3MAP")) a.lane_map = (e[0] == '1' && T >= 64) ? 1 : 0;
+    // TMA staging (k_fused3, unsharded, lane map 1 with slot 0 the lowest outer slot): the outer
+    // slots are two runs of consecutive slots, A = 0 .. p0-1 and B = p0+3 .. L-1
+    ls.tma_a = -1;
+    if (P.kind == 4 && M == 2 && S == 3 && removed.empty() && a.lane_map == 1 && p0 >= 1 && p0 + S <= L &&
+        !std::getenv("QUAPI_NO_TMA"))
+        ls.tma_a = p0, ls.tma_b = L - p0 - S;
     for (int st = 0; st < qp::kMaxS; ++st)
         for (int kap = 0; kap < 2; ++kap)
             for (int d = 0; d < qp::kMaxD; ++d) a.fixfac[st][kap][d] = make_double2(1.0, 0.0);
@@ -850,6 +899,13 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             qp::FusedArgs a = ls.args;
             a.A = A;
             a.small = small;
+            a.use_tma = 0;
+            if (ls.tma_a >= 0 && P->kind == 4 && S == 3 &&
+                encode_f3_tmap(*P, ls, A, qp::fused3_round_fibres(qp::F3_MODE_TMA))) {
+                a.use_tma = 1;
+                a.tmap = ls.tmap;
+                a.tma_nA = ipow(P->N, ls.tma_a);
+            }
             a.inner = (const double2 *)(w + ls.off_inner);
             a.Etab = (const double2 *)(w + ls.off_E);
             a.goff = (const long long *)(w + ls.off_goff);

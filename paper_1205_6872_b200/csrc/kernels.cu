@@ -880,9 +880,39 @@ __device__ __forceinline__ int f3_swizzle(int r) {
     return (((hi & 1) << 2) | (hi >> 1)) ^ (((lo & 1) << 2) | (lo >> 1));
 }
 
-template <bool SYM, int MAP, int BLOCK, int MINB, bool PF, bool RO>
+// TMA (cp.async.bulk.tensor) + mbarrier helpers for k_fused3's staged loads
+__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra WAIT_%=;\n}\n" ::"r"(smem_addr(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void *dst, const void *tmap, unsigned long long *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %4, %4}], [%5];"
+        ::"r"(smem_addr(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(0), "r"(smem_addr(bar)) : "memory");
+}
+
+// PFM (next-round prefetch): 0 none, 1 registers, 2 TMA box into a shared-memory stage (lane map 1,
+// unsharded layouts: FusedArgs::tmap, dims (run A, run B, d0, d1, d2), see host.cpp)
+template <bool SYM, int MAP, int BLOCK, int MINB, int PFM, bool RO>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ FusedArgs a) {
     constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2;
+    constexpr bool PF = PFM == 1, TM = PFM == 2;
+    static_assert(!TM || MAP == 1, "TMA staging uses lane map 1");
+    constexpr int F = 8 * (BLOCK / 32);  // outer fibres per round
     constexpr int NK = RO ? 2 : 1;
     constexpr int W = BLOCK / 32;
     constexpr bool LAT = false;
@@ -893,9 +923,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     __shared__ double2 sEhi[S][NK][D];
     __shared__ long long sBase;
     __shared__ int sLast;
-    // dynamic: per-warp exchange buffer [W][16][8] (a quarter of the super-fibre entries x 8 outer
-    // fibres), then the readout accumulators [S][N][BLOCK] (RO only)
-    extern __shared__ double2 dyn_smem[];
+    // dynamic: (TM) the round's TMA stage [d2][d1][d0][F], then the exchange buffer (W x 16 x 8
+    // entries: a quarter of the super-fibre entries of the round's fibres), then the readout
+    // accumulators [S][N][BLOCK] (RO only)
+    extern __shared__ __align__(1024) double2 dyn_smem_raw[];
+    double2 *stage = dyn_smem_raw;
+    // TM: per-round outer factors E0 [2 buffers][S][2][D][F] and tile-local offsets [2][F] (bulk copies
+    // on the same mbarrier, double-buffered: read during the round while the next one lands)
+    double2 *sE0 = dyn_smem_raw + (TM ? F * 64 : 0);
+    int2 *sLo = reinterpret_cast<int2 *>(sE0 + (TM ? 2 * S * 2 * D * F : 0));
+    double2 *dyn_smem = sE0 + (TM ? 2 * S * 2 * D * F + F : 0);
+    __shared__ __align__(8) unsigned long long sFull;
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem + W * 16 * 8);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
@@ -1003,6 +1041,28 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     int2 lon = make_int2(0, 0);
     if constexpr (PF)
         if (t_begin < t_end) load_unit(t_begin, 0, Xn, lon);
+    // TM: one stage; thread 0 issues the TMA box of unit (tau, rd): outer fibres G = tau T + rd F
+    auto tma_issue = [&](int tau, int rd, int buf) {
+        const long long G = (long long)tau * a.T + (long long)rd * F;
+        fence_proxy_async();
+        mbar_expect_tx(&sFull, F * 64 * 16 + S * 2 * D * F * 16 + F * 8);
+        tma_load_5d(stage, &a.tmap, &sFull, (int)(2 * (G % a.tma_nA)), (int)(G / a.tma_nA));
+        for (int q = 0; q < S * 2 * D; ++q) {  // q = (s, kap, d): Etab[s][kap][g = 0][d][t0 ..]
+            const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
+            bulk_g2s(sE0 + ((size_t)buf * S * 2 * D + q) * F,
+                     a.Etab + ((((size_t)st * 2 + kap) * a.G) * D + d) * a.X + rd * F, F * 16, &sFull);
+        }
+        bulk_g2s(sLo + buf * F, a.lofs + rd * F, F * 8, &sFull);
+    };
+    unsigned phase = 0, cur = 0;
+    if constexpr (TM) {
+        if (threadIdx.x == 0) {
+            mbar_init(&sFull, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && t_begin < t_end) tma_issue(t_begin, 0, 0);
+    }
 
     for (int tau = t_begin; tau < t_end; ++tau) {
         __syncthreads();  // previous tile's KU no longer in use
@@ -1040,7 +1100,19 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
             const bool valid = t < a.T;
             int2 lo;
             double2 X[N][N];  // X[d1][d0], d2 = j
-            if constexpr (PF) {  // this unit was loaded one unit ago; issue the next unit's loads now
+            if constexpr (TM) {  // the stage holds this unit (issued one unit ago)
+                mbar_wait(&sFull, phase);
+                cur = phase;
+                phase ^= 1;
+                lo = sLo[cur * F + fib];
+#pragma unroll
+                for (int d1 = 0; d1 < N; ++d1)
+#pragma unroll
+                    for (int d0 = 0; d0 < N; ++d0) X[d1][d0] = stage[((j * N + d1) * N + d0) * F + fib];
+                __syncthreads();  // stage free: refill it with the next unit
+                const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
+                if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
+            } else if constexpr (PF) {  // this unit was loaded one unit ago; issue the next unit's loads now
 #pragma unroll
                 for (int d1 = 0; d1 < N; ++d1)
 #pragma unroll
@@ -1075,7 +1147,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 double2 E0[NK][D];  // outer group-0 factor (kap = 1, readout: loaded at the end of the step)
 #pragma unroll
                 for (int d = 0; d < D; ++d) {
-                    E0[0][d] = __ldg(&a.Etab[((size_t)s * 2 * a.G * D + d) * a.X + t]);
+                    E0[0][d] = TM ? sE0[((cur * S + s) * 2 * D + d) * F + fib]
+                                  : __ldg(&a.Etab[((size_t)s * 2 * a.G * D + d) * a.X + t]);
                     E0[NK - 1][d] = E0[0][d];
                 }
                 double2 acc[RO ? N : 1];
@@ -1105,8 +1178,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                     for (int n = 0; n < N; ++n) {
                         const int c = class_of(M, LAT, n / M, n % M);
                         if (c > 0)
-                            acc[RO ? n : 0] = cmul(__ldg(&a.Etab[(((size_t)s * 2 + 1) * a.G * D + (c > 0 ? c - 1 : 0)) * a.X + t]),
-                                                   acc[RO ? n : 0]);
+                            acc[RO ? n : 0] =
+                                cmul(TM ? sE0[((cur * S + s) * 2 * D + D + (c > 0 ? c - 1 : 0)) * F + fib]
+                                        : __ldg(&a.Etab[(((size_t)s * 2 + 1) * a.G * D + (c > 0 ? c - 1 : 0)) * a.X + t]),
+                                     acc[RO ? n : 0]);
                     }
 #pragma unroll
                     for (int n = 0; n < N; ++n)
@@ -1233,21 +1308,29 @@ FusedShape fused_shape(int M) {
 // kind 4: three fused steps per pass (k_fused3, M = 2); S < 3 launches of such a plan use kind 1
 static int eff_kind(int M, int S, int kind) { return kind == 4 ? ((M == 2 && S == 3) ? 4 : 1) : kind; }
 
-// k_fused3 launch variants (index, lane map, BLOCK, MINB, PF = register prefetch of the next unit).
-// The lane map is fixed per launch set (FusedArgs::lane_map); QUAPI_F3 = index selects a variant of
-// that map for tuning, else the map's default (no register spills at 168 registers).
-#define QP_F3_CFGS(X)                                                                             \
-    X(0, 0, 256, 2, false) X(1, 0, 192, 2, false) X(2, 0, 128, 3, false) X(3, 1, 128, 3, false)   \
-    X(4, 1, 256, 1, false) X(5, 1, 384, 1, false) X(6, 1, 128, 2, true)
-static int f3_variant(int map) {
-    const int def = map == 0 ? 1 : 3;
+// k_fused3 launch variants (index, mode, BLOCK, MINB, PFM).  mode = lane map + 2 x TMA staging,
+// fixed per launch (FusedArgs::lane_map, use_tma); QUAPI_F3 = index selects a variant of that mode
+// for tuning, else the mode's default (no register spills at <= 168 registers).
+#define QP_F3_CFGS(X)                                                                              \
+    X(0, 0, 256, 2, 0) X(1, 0, 192, 2, 0) X(2, 0, 128, 3, 0) X(3, 1, 128, 3, 0) X(4, 1, 256, 1, 0) \
+    X(5, 1, 384, 1, 0) X(6, 1, 128, 2, 1) X(7, 3, 128, 2, 2) X(8, 3, 256, 1, 2)
+static int f3_mode(const FusedArgs &a) { return (a.lane_map & 1) + (a.use_tma ? 2 : 0); }
+static int f3_variant(int mode) {
+    const int def = mode == 0 ? 1 : (mode == 1 ? 3 : 7);
     const char *e = std::getenv("QUAPI_F3");
     if (!e) return def;
     const int v = std::atoi(e);
-#define X(I, MP, B, MB, PF) if (v == I) return MP == map ? I : def;
+#define X(I, MD, B, MB, PM) if (v == I) return MD == mode ? I : def;
     QP_F3_CFGS(X)
 #undef X
     return def;
+}
+int fused3_round_fibres(int mode) {
+    const int v = f3_variant(mode);
+#define X(I, MD, B, MB, PM) if (v == I) return B / 4;
+    QP_F3_CFGS(X)
+#undef X
+    return 32;
 }
 
 bool has_reg_variant(int M, int S, int kind) {
@@ -1297,7 +1380,7 @@ int fused_tile_digits_min(int M, int S, int kind) {
 int fused_block(int M, int S, int kind) {
     kind = eff_kind(M, S, kind);
     if (kind == 4) {
-#define X(I, MP, B, MB, PF) if (f3_variant(0) == I) return B;
+#define X(I, MD, B, MB, PM) if (f3_variant(0) == I) return B;
         QP_F3_CFGS(X)
 #undef X
     }
@@ -1379,11 +1462,14 @@ static int fused_occ_t() {
 }
 
 // M = 2: the lattice and general class maps give the same classes; the host uses LAT = false.
-static size_t fused3_dyn(int block, bool ro) { return ((size_t)(block / 32) * 16 * 8 + (ro ? (size_t)3 * 4 * block : 0)) * 16; }
+static size_t fused3_dyn(int block, bool ro, int pfm) {
+    const size_t F = block / 4;
+    return ((pfm == 2 ? F * 64 + 2 * 3 * 2 * 2 * F + F : 0) + (size_t)(block / 32) * 16 * 8 + (ro ? (size_t)3 * 4 * block : 0)) * 16;
+}
 
-template <bool SYM, int MAP, int BLOCK, int MINB, bool PF>
+template <bool SYM, int MAP, int BLOCK, int MINB, int PF>
 static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
-    const size_t dyn = fused3_dyn(BLOCK, ro);
+    const size_t dyn = fused3_dyn(BLOCK, ro, PF);
     if (ro) {
         cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         k_fused3<SYM, MAP, BLOCK, MINB, PF, true><<<grid, BLOCK, dyn, s>>>(a);
@@ -1394,10 +1480,10 @@ static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t 
     return cudaGetLastError();
 }
 
-template <bool SYM, int MAP, int BLOCK, int MINB, bool PF>
+template <bool SYM, int MAP, int BLOCK, int MINB, int PF>
 static int fused3_occ_t() {
     int o1 = 0, o2 = 0;
-    const size_t d1 = fused3_dyn(BLOCK, true), d2 = fused3_dyn(BLOCK, false);
+    const size_t d1 = fused3_dyn(BLOCK, true, PF), d2 = fused3_dyn(BLOCK, false, PF);
     cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d1);
     cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d2);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, BLOCK, d1);
@@ -1408,9 +1494,9 @@ static int fused3_occ_t() {
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
     kind = eff_kind(M, S, kind);
     if (kind == 4) {
-#define X(I, MP, B, MB, PF)                                                                          \
-        if (f3_variant(a.lane_map) == I)                                                                 \
-            return sym ? fused3_t<true, MP, B, MB, PF>(a, ro, grid, s) : fused3_t<false, MP, B, MB, PF>(a, ro, grid, s);
+#define X(I, MD, B, MB, PF)                                                                          \
+        if (f3_variant(f3_mode(a)) == I)                                                                 \
+            return sym ? fused3_t<true, (MD & 1), B, MB, PF>(a, ro, grid, s) : fused3_t<false, (MD & 1), B, MB, PF>(a, ro, grid, s);
         QP_F3_CFGS(X)
 #undef X
     }
@@ -1441,11 +1527,11 @@ cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const F
     return cudaErrorInvalidValue;
 }
 
-int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int lane_map) {
+int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int mode) {
     kind = eff_kind(M, S, kind);
     if (kind == 4) {
-#define X(I, MP, B, MB, PF) \
-        if (f3_variant(lane_map) == I) return sym ? fused3_occ_t<true, MP, B, MB, PF>() : fused3_occ_t<false, MP, B, MB, PF>();
+#define X(I, MD, B, MB, PF) \
+        if (f3_variant(mode) == I) return sym ? fused3_occ_t<true, (MD & 1), B, MB, PF>() : fused3_occ_t<false, (MD & 1), B, MB, PF>();
         QP_F3_CFGS(X)
 #undef X
     }

@@ -1,6 +1,7 @@
 // qp_internal.h -- structures shared by the host setup (host.cpp) and the sm_100a kernels
 // (kernels.cu).  Not part of the public ABI (include/quapi.h).
 #pragma once
+#include <cuda.h>  // CUtensorMap (the encode entry point is fetched at run time; no -lcuda)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -62,6 +63,9 @@ struct FusedArgs {
     int fixed_last;          // sub-step 0 'last' slot is a (fixed) shard slot: its value; else -1
     int rho_accumulate;      // 1: rho[n] += sum (several shard blocks contribute to one step)
     int lane_map;            // k_fused3 lane map (kernels.cu): 1 when tile fibres t, t+1 are adjacent in HBM
+    int use_tma;             // k_fused3 (lane map 1, unsharded): rounds staged by TMA through `tmap`
+    long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view
+    alignas(64) CUtensorMap tmap;
     int var[kMaxS];          // beta variant per sub-step: 1 for the first slide step k == L (initial-edge
                              // classes of the partner sigma_0), else 0 (SmallLayout::beta)
     // M = 2, s = (+s, -s): beta_1 = (c, rho, 1/rho, conj c); {Re c, Im c, (rho+1/rho)/2, (rho-1/rho)/2}
@@ -113,7 +117,10 @@ int fused_tile_digits_min(int M, int S, int kind);  // smallest v the kernel sup
 int fused_block(int M, int S, int kind);
 // Launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool readout, int grid, cudaStream_t s);
-int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int lane_map = 0);  // resident CTAs per SM (needs a device)
+// mode (k_fused3): lane map + 2 x TMA staging
+constexpr int F3_MODE_TMA = 3;
+int fused3_round_fibres(int mode);  // outer fibres per round (BLOCK / 4) of the mode's k_fused3 variant
+int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int mode = 0);  // resident CTAs per SM (needs a device)
 cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaStream_t s);
 
 }  // namespace qp
