@@ -886,6 +886,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
+// 32-byte (256-bit) streaming load / store of two adjacent complex entries (p must be 32-B aligned)
+__device__ __forceinline__ void ld2_cs(const double2 *p, double2 &x, double2 &y) {
+    asm volatile("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(x.x), "=d"(x.y), "=d"(y.x), "=d"(y.y) : "l"(p));
+}
+__device__ __forceinline__ void st2_cs(double2 *p, double2 x, double2 y) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(x.x), "d"(x.y), "d"(y.x), "d"(y.y) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
@@ -911,7 +918,6 @@ template <bool SYM, int MAP, int BLOCK, int MINB, int PFM, bool RO>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ FusedArgs a) {
     constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2;
     constexpr bool PF = PFM == 1, TM = PFM == 2;
-    static_assert(!TM || MAP == 1, "TMA staging uses lane map 1");
     constexpr int F = 8 * (BLOCK / 32);  // outer fibres per round
     constexpr int NK = RO ? 2 : 1;
     constexpr int W = BLOCK / 32;
@@ -1028,11 +1034,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
         if (t < a.T) {
             lo = __ldg(&a.lofs[t]);
             const long long base = tile_base(tau) + lo.x + (long long)j * a.pw_in[2];
+            if (a.pw_in[0] == 1) {  // d0 is ring slot 0: entry pairs (d0, d0 + 1) are adjacent, 32-B loads
 #pragma unroll
-            for (int d1 = 0; d1 < N; ++d1)
+                for (int d1 = 0; d1 < N; ++d1)
 #pragma unroll
-                for (int d0 = 0; d0 < N; ++d0)
-                    Y[d1][d0] = __ldcs(a.A + base + (long long)d0 * a.pw_in[0] + (long long)d1 * a.pw_in[1]);
+                    for (int d0 = 0; d0 < N; d0 += 2) ld2_cs(a.A + base + d0 + (long long)d1 * a.pw_in[1], Y[d1][d0], Y[d1][d0 + 1]);
+            } else if (a.pw_in[1] == 1) {  // d1 is slot 0: pairs (d1, d1 + 1)
+#pragma unroll
+                for (int d1 = 0; d1 < N; d1 += 2)
+#pragma unroll
+                    for (int d0 = 0; d0 < N; ++d0) ld2_cs(a.A + base + (long long)d0 * a.pw_in[0] + d1, Y[d1][d0], Y[d1 + 1][d0]);
+            } else {
+#pragma unroll
+                for (int d1 = 0; d1 < N; ++d1)
+#pragma unroll
+                    for (int d0 = 0; d0 < N; ++d0)
+                        Y[d1][d0] = __ldcs(a.A + base + (long long)d0 * a.pw_in[0] + (long long)d1 * a.pw_in[1]);
+            }
         } else {
             lo = make_int2(0, 0);
         }
@@ -1046,7 +1064,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
         const long long G = (long long)tau * a.T + (long long)rd * F;
         fence_proxy_async();
         mbar_expect_tx(&sFull, F * 64 * 16 + S * 2 * D * F * 16 + F * 8);
-        tma_load_5d(stage, &a.tmap, &sFull, (int)(2 * (G % a.tma_nA)), (int)(G / a.tma_nA));
+        tma_load_5d(stage, &a.tmap, &sFull, (int)(a.tma_c0m * (G % a.tma_nA)), (int)(G / a.tma_nA));
         for (int q = 0; q < S * 2 * D; ++q) {  // q = (s, kap, d): Etab[s][kap][g = 0][d][t0 ..]
             const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
             bulk_g2s(sE0 + ((size_t)buf * S * 2 * D + q) * F,
@@ -1108,7 +1126,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
 #pragma unroll
                 for (int d1 = 0; d1 < N; ++d1)
 #pragma unroll
-                    for (int d0 = 0; d0 < N; ++d0) X[d1][d0] = stage[((j * N + d1) * N + d0) * F + fib];
+                    for (int d0 = 0; d0 < N; ++d0)
+                        X[d1][d0] = stage[fib * a.tma_sf + d0 * a.tma_s[0] + d1 * a.tma_s[1] + j * a.tma_s[2]];
                 __syncthreads();  // stage free: refill it with the next unit
                 const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
                 if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
@@ -1190,12 +1209,24 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 }
             }
             if (valid) {  // X[d1][d2] with digit 0 = j
+                const long long b0 = base + (long long)j * a.pw_in[0];
+                if (a.pw_in[2] == 1) {  // d2 is ring slot 0: 32-B stores of adjacent pairs
 #pragma unroll
-                for (int d1 = 0; d1 < N; ++d1)
+                    for (int d1 = 0; d1 < N; ++d1)
 #pragma unroll
-                    for (int d2 = 0; d2 < N; ++d2)
-                        __stcs(a.A + base + (long long)j * a.pw_in[0] + (long long)d1 * a.pw_in[1] + (long long)d2 * a.pw_in[2],
-                               X[d1][d2]);
+                        for (int d2 = 0; d2 < N; d2 += 2) st2_cs(a.A + b0 + (long long)d1 * a.pw_in[1] + d2, X[d1][d2], X[d1][d2 + 1]);
+                } else if (a.pw_in[1] == 1) {
+#pragma unroll
+                    for (int d1 = 0; d1 < N; d1 += 2)
+#pragma unroll
+                        for (int d2 = 0; d2 < N; ++d2) st2_cs(a.A + b0 + d1 + (long long)d2 * a.pw_in[2], X[d1][d2], X[d1 + 1][d2]);
+                } else {
+#pragma unroll
+                    for (int d1 = 0; d1 < N; ++d1)
+#pragma unroll
+                        for (int d2 = 0; d2 < N; ++d2)
+                            __stcs(a.A + b0 + (long long)d1 * a.pw_in[1] + (long long)d2 * a.pw_in[2], X[d1][d2]);
+                }
             }
         }
     }
@@ -1313,10 +1344,11 @@ static int eff_kind(int M, int S, int kind) { return kind == 4 ? ((M == 2 && S =
 // for tuning, else the mode's default (no register spills at <= 168 registers).
 #define QP_F3_CFGS(X)                                                                              \
     X(0, 0, 256, 2, 0) X(1, 0, 192, 2, 0) X(2, 0, 128, 3, 0) X(3, 1, 128, 3, 0) X(4, 1, 256, 1, 0) \
-    X(5, 1, 384, 1, 0) X(6, 1, 128, 2, 1) X(7, 3, 128, 2, 2) X(8, 3, 256, 1, 2)
+    X(5, 1, 384, 1, 0) X(6, 1, 128, 2, 1) X(7, 3, 128, 2, 2) X(8, 3, 256, 1, 2) X(9, 2, 128, 2, 2)              \
+    X(10, 2, 256, 1, 2)
 static int f3_mode(const FusedArgs &a) { return (a.lane_map & 1) + (a.use_tma ? 2 : 0); }
 static int f3_variant(int mode) {
-    const int def = mode == 0 ? 1 : (mode == 1 ? 3 : 7);
+    const int def = mode == 0 ? 1 : (mode == 1 ? 3 : (mode == 2 ? 9 : 7));
     const char *e = std::getenv("QUAPI_F3");
     if (!e) return def;
     const int v = std::atoi(e);
