@@ -243,9 +243,14 @@ def main():
             "scaling": "weak" if world > 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": base.name, "ardm_entries": sz.ardm_entries, "ardm_bytes": sz.ardm_bytes,
-                       "readout": "every step (allPoints), fused", "l2": "inputs larger than L2 (4.3 GB ARDM)",
+                       "readout": "every step (allPoints), fused",
+                       "l2": (f"inputs larger than L2 ({sz.ardm_bytes / 1e9:.1f} GB ARDM, 126 MB L2)"
+                              if sz.ardm_bytes > 2 * 126e6 else
+                              f"L2-resident ARDM ({sz.ardm_bytes / 1e6:.1f} MB): not flushed, not a roofline case"),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "grid": plan.sizes.grid, "block": sz.block, "tile_fibres": sz.tile_fibres,
+                       "kernel": ("k_fused3: 3 time steps per HBM pass, persistent grid, TMA-staged rounds "
+                                  "where the ring slot allows" if sz.fuse_steps == 3 else
+                                  f"k_fused_r: {sz.fuse_steps} time step(s) per HBM pass"),
                        "steps_per_launch": K / max(1, launches)},
             "achieved_gbs": achieved,
             "step_equivalent_gbs": step_equiv,

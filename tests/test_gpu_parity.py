@@ -212,3 +212,19 @@ def test_fusion_grouping_independent_of_segments():
     for k0, k1 in zip(cuts[:-1], cuts[1:]):
         plan.steps(k0, k1, ardm, work)
     assert np.array_equal(plan.read_rho(work), whole)
+
+
+@pytest.mark.parametrize("env", [{}, {"QUAPI_NO_TMA": "1"}, {"QUAPI_F3TMAP": "1"}, {"QUAPI_TMA_VIEWB": "1"},
+                                 {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "1"}, {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "0"},
+                                 {"QUAPI_F3": "0"}, {"QUAPI_F3": "2"}, {"QUAPI_F3": "6"}, {"QUAPI_F3": "10"}])
+@pytest.mark.parametrize("L,n", [(8, 37), (9, 30)])
+def test_fused3_load_paths(env, L, n, monkeypatch):
+    """k_fused3's load paths (TMA-staged rounds in views A and B, plain loads in lane maps 0 and 1,
+    32-byte loads/stores along ring slot 0, register prefetch) and launch variants against the
+    oracle; L >= 8 so that every start slot p0 (TMA views included) occurs."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = W.random_problem(500 + L, 2, L, n, kind=W.J_OHMIC_EXP)
+    rg, plan, _ = gpu_run(w)
+    assert plan.sizes.fuse_steps == 3
+    check(rg, O.run(P(w)))
