@@ -17,6 +17,15 @@ for kind in ("reg", "warp", "async", "split"):
         a, wk = pl.alloc()
         r = pl.run(a, wk)
         assert np.isfinite(r).all()
+os.environ["QUAPI_FUSED_KIND"] = "3"
+for env in ({}, {"QUAPI_NO_TMA": "1"}, {"QUAPI_F3TMAP": "1"}, {"QUAPI_TMA_VIEWB": "1"}, {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "1"}):
+    os.environ.update(env)
+    w = W.random_problem(7, 2, 8, 20)  # L = 8: TMA-staged, plain-load and 32-B-load ring slots all occur
+    pl = Q.Plan(w)
+    a, wk = pl.alloc()
+    assert np.isfinite(pl.run(a, wk)).all()
+    for k in env:
+        del os.environ[k]
 os.environ["QUAPI_FUSED_KIND"] = "reg"
 w = W.random_problem(6, 2, 6, 20)
 ranks = [SH.ShardRank(w, 2, i) for i in range(2)]
