@@ -333,6 +333,7 @@ struct qp_plan {
         // run B = the tma_b slots above the inner ones.  View B (p0 = L-2, tma_a = 0): inner digit 2 is
         // slot 0 and the outer slots 1..L-3 are one run.
         int tma_a = -1, tma_b = 0;
+        bool stg_ca = false;           // cp.async-staged rounds (p0 = 0, L-2, L-1; see build_launch_set)
         mutable const void *tma_A = nullptr;  // ARDM pointer the cached tensor map was encoded for
         mutable CUtensorMap tmap{};
     };
@@ -342,7 +343,7 @@ struct qp_plan {
     size_t off_small = 0, off_part = 0, off_rho = 0, off_cnt = 0, tables_end = 0, work_bytes = 0;
     int64_t ardm_entries = 0;
     int grid[qp::kMaxS + 1] = {0};
-    int occ[qp::kMaxS + 1][4] = {};    // resident CTAs per SM of the fused kernel per (S, k_fused3 mode)
+    int occ[qp::kMaxS + 1][5] = {};    // resident CTAs per SM of the fused kernel per (S, k_fused3 mode)
     int sms = 0;
     int64_t next_k = 1;
     bool inited = false;
@@ -501,7 +502,7 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
 // Persistent grid of one fused launch: fixed per (plan, launch set, device type), so the readout
 // order (block partials) is deterministic.
 static int launch_grid(qp_plan *P, int S, const qp::FusedArgs &a) {
-    const int mode = (a.lane_map & 1) + (a.use_tma ? 2 : 0);
+    const int mode = a.use_tma == 2 ? 4 : (a.lane_map & 1) + (a.use_tma ? 2 : 0);
     int &o = P->occ[S][mode];
     if (o == 0) o = std::max(1, qp::fused_occupancy(P->M, P->lattice, P->sym, P->kind, S, mode));
     return std::max(1, std::min<int>({a.n_tiles, P->sms * o, qp::kPartialsMax}));
@@ -618,6 +619,38 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     if (ls.tma_a >= 0) {
         const char *e = std::getenv("QUAPI_F3TMAP");
         a.lane_map = (e && e[0] == '1') ? 1 : 0;
+    }
+    // cp.async-staged rounds for the remaining slots of k_fused3 (an inner digit is ring slot 0, so no
+    // TMA box with slot 0 innermost gives conflict-free stage reads): the round's F fibres are
+    // uniformly strided (the lowest outer slots are consecutive); the copy walks the round in HBM
+    // order and the stage keeps that order, XOR-swizzled by fibre when fibres are >= 8 units apart.
+    ls.stg_ca = false;
+    a.use_tma = 0;
+    // Off by default: measured slower than plain 32-B loads on cfg3 (p0 = 0 / 12 / 13: 3.13 / 2.92 /
+    // 2.95 ms vs 2.93 / 2.43 / 2.62 ms); QUAPI_CA=1 enables it.
+    if (P.kind == 4 && M == 2 && S == 3 && removed.empty() && T >= 64 && ls.tma_a < 0 && std::getenv("QUAPI_CA")) {
+        const int F = qp::fused3_round_fibres(4);
+        const long long sfib = ipow(N, pos[outer[0]]);
+        bool uniform = true;  // fibres 0..F-1 of a round at stride sfib
+        for (int f = 0; f < F && uniform; ++f) uniform = ls.lofs[f].x == (long long)f * sfib;
+        if (uniform && T % F == 0) {
+            struct Fld { long long g; int lg, id; };
+            Fld fl[4] = {{a.pw_in[0], 2, 0}, {a.pw_in[1], 2, 1}, {a.pw_in[2], 2, 2}, {sfib, 0, 3}};
+            for (int lgF = 1; (1 << lgF) <= F; ++lgF) fl[3].lg = lgF;
+            std::sort(fl, fl + 4, [](const Fld &x, const Fld &y) { return x.g < y.g; });
+            int sst = 1, sf = 0, sd[3] = {0, 0, 0};
+            for (int i = 0; i < 4; ++i) {
+                a.stg_lg[i] = fl[i].lg;
+                a.stg_g[i] = fl[i].g;
+                a.stg_s[i] = sst;
+                if (fl[i].id == 3) a.stg_fi = i, sf = sst; else sd[fl[i].id] = sst;
+                sst <<= fl[i].lg;
+            }
+            a.tma_sf = sf, a.tma_s[0] = sd[0], a.tma_s[1] = sd[1], a.tma_s[2] = sd[2];
+            a.stg_swz = (sf % 8 == 0) ? 1 : 0;
+            ls.stg_ca = true;
+            a.lane_map = 0;
+        }
     }
     for (int st = 0; st < qp::kMaxS; ++st)
         for (int kap = 0; kap < 2; ++kap)
@@ -922,7 +955,7 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             qp::FusedArgs a = ls.args;
             a.A = A;
             a.small = small;
-            a.use_tma = 0;
+            a.use_tma = ls.stg_ca ? 2 : 0;
             if (ls.tma_a >= 0 && P->kind == 4 && S == 3 &&
                 encode_f3_tmap(*P, ls, A, qp::fused3_round_fibres((a.lane_map & 1) + 2))) {
                 a.use_tma = 1;

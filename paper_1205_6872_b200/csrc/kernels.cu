@@ -917,7 +917,7 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const void *tmap, unsigne
 template <bool SYM, int MAP, int BLOCK, int MINB, int PFM, bool RO>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ FusedArgs a) {
     constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2;
-    constexpr bool PF = PFM == 1, TM = PFM == 2;
+    constexpr bool PF = PFM == 1, TM = PFM == 2, CA = PFM == 3, STG = TM || CA;
     constexpr int F = 8 * (BLOCK / 32);  // outer fibres per round
     constexpr int NK = RO ? 2 : 1;
     constexpr int W = BLOCK / 32;
@@ -934,11 +934,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     // accumulators [S][N][BLOCK] (RO only)
     extern __shared__ __align__(1024) double2 dyn_smem_raw[];
     double2 *stage = dyn_smem_raw;
-    // TM: per-round outer factors E0 [2 buffers][S][2][D][F] and tile-local offsets [2][F] (bulk copies
-    // on the same mbarrier, double-buffered: read during the round while the next one lands)
-    double2 *sE0 = dyn_smem_raw + (TM ? F * 64 : 0);
-    int2 *sLo = reinterpret_cast<int2 *>(sE0 + (TM ? 2 * S * 2 * D * F : 0));
-    double2 *dyn_smem = sE0 + (TM ? 2 * S * 2 * D * F + F : 0);
+    // TM / CA: per-round outer factors E0 [2 buffers][S][2][D][F] and tile-local offsets [2][F] (copied
+    // with the round, double-buffered: read during the round while the next one lands)
+    double2 *sE0 = dyn_smem_raw + (STG ? F * 64 : 0);
+    int2 *sLo = reinterpret_cast<int2 *>(sE0 + (STG ? 2 * S * 2 * D * F : 0));
+    double2 *dyn_smem = sE0 + (STG ? 2 * S * 2 * D * F + F : 0);
     __shared__ __align__(8) unsigned long long sFull;
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem + W * 16 * 8);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
@@ -1072,7 +1072,37 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
         }
         bulk_g2s(sLo + buf * F, a.lofs + rd * F, F * 8, &sFull);
     };
+    // CA: every thread copies 16-B chunks of the round with cp.async: chunk q enumerates the round in
+    // HBM order (fields sorted by stride: a.stg_lg[i] = log2 radix, a.stg_g[i] global stride, a.stg_s[i]
+    // stage stride, field a.stg_fi = the fibre index), so consecutive lanes read consecutive 16 B; the
+    // stage position is XOR-swizzled with the fibre's low 3 bits when a.stg_swz (bank-conflict-free reads)
+    auto ca_issue = [&](int tau, int rd, int buf) {
+        const long long rb = tile_base(tau) + __ldg(&a.lofs[rd * F]).x;
+        for (int q = threadIdx.x; q < F * 64; q += BLOCK) {
+            int r = q, sp = 0, fv = 0;
+            long long go = rb;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int dg = r & ((1 << a.stg_lg[i]) - 1);
+                r >>= a.stg_lg[i];
+                go += (long long)dg * a.stg_g[i];
+                sp += dg * a.stg_s[i];
+                if (i == a.stg_fi) fv = dg;
+            }
+            if (a.stg_swz) sp ^= fv & 7;
+            cp_async16(stage + sp, a.A + go);
+        }
+        for (int q = threadIdx.x; q < S * 2 * D * F; q += BLOCK) {
+            const int qq = q / F, f = q % F, st = qq / (2 * D), kap = (qq / D) % 2, d = qq % D;
+            cp_async16(sE0 + ((size_t)buf * S * 2 * D + qq) * F + f,
+                       a.Etab + ((((size_t)st * 2 + kap) * a.G) * D + d) * a.X + rd * F + f);
+        }
+        for (int q = threadIdx.x; q < F / 2; q += BLOCK) cp_async16(sLo + buf * F + 2 * q, a.lofs + rd * F + 2 * q);
+        cp_async_commit();
+    };
     unsigned phase = 0, cur = 0;
+    if constexpr (CA)
+        if (t_begin < t_end) ca_issue(t_begin, 0, 0);
     if constexpr (TM) {
         if (threadIdx.x == 0) {
             mbar_init(&sFull, 1);
@@ -1131,6 +1161,21 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 __syncthreads();  // stage free: refill it with the next unit
                 const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
                 if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
+            } else if constexpr (CA) {  // the stage holds this unit (copied one unit ago)
+                cp_async_wait<0>();
+                __syncthreads();
+                cur = phase;
+                phase ^= 1;
+                lo = sLo[cur * F + fib];
+                const int sw = a.stg_swz ? (fib & 7) : 0;
+#pragma unroll
+                for (int d1 = 0; d1 < N; ++d1)
+#pragma unroll
+                    for (int d0 = 0; d0 < N; ++d0)
+                        X[d1][d0] = stage[(fib * a.tma_sf + d0 * a.tma_s[0] + d1 * a.tma_s[1] + j * a.tma_s[2]) ^ sw];
+                __syncthreads();  // stage free: refill it with the next unit
+                const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
+                if (taun < t_end) ca_issue(taun, rn, phase);
             } else if constexpr (PF) {  // this unit was loaded one unit ago; issue the next unit's loads now
 #pragma unroll
                 for (int d1 = 0; d1 < N; ++d1)
@@ -1166,7 +1211,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 double2 E0[NK][D];  // outer group-0 factor (kap = 1, readout: loaded at the end of the step)
 #pragma unroll
                 for (int d = 0; d < D; ++d) {
-                    E0[0][d] = TM ? sE0[((cur * S + s) * 2 * D + d) * F + fib]
+                    E0[0][d] = STG ? sE0[((cur * S + s) * 2 * D + d) * F + fib]
                                   : __ldg(&a.Etab[((size_t)s * 2 * a.G * D + d) * a.X + t]);
                     E0[NK - 1][d] = E0[0][d];
                 }
@@ -1198,7 +1243,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                         const int c = class_of(M, LAT, n / M, n % M);
                         if (c > 0)
                             acc[RO ? n : 0] =
-                                cmul(TM ? sE0[((cur * S + s) * 2 * D + D + (c > 0 ? c - 1 : 0)) * F + fib]
+                                cmul(STG ? sE0[((cur * S + s) * 2 * D + D + (c > 0 ? c - 1 : 0)) * F + fib]
                                         : __ldg(&a.Etab[(((size_t)s * 2 + 1) * a.G * D + (c > 0 ? c - 1 : 0)) * a.X + t]),
                                      acc[RO ? n : 0]);
                     }
@@ -1345,10 +1390,10 @@ static int eff_kind(int M, int S, int kind) { return kind == 4 ? ((M == 2 && S =
 #define QP_F3_CFGS(X)                                                                              \
     X(0, 0, 256, 2, 0) X(1, 0, 192, 2, 0) X(2, 0, 128, 3, 0) X(3, 1, 128, 3, 0) X(4, 1, 256, 1, 0) \
     X(5, 1, 384, 1, 0) X(6, 1, 128, 2, 1) X(7, 3, 128, 2, 2) X(8, 3, 256, 1, 2) X(9, 2, 128, 2, 2)              \
-    X(10, 2, 256, 1, 2)
-static int f3_mode(const FusedArgs &a) { return (a.lane_map & 1) + (a.use_tma ? 2 : 0); }
+    X(10, 2, 256, 1, 2) X(11, 4, 128, 2, 3)
+static int f3_mode(const FusedArgs &a) { return a.use_tma == 2 ? 4 : (a.lane_map & 1) + (a.use_tma ? 2 : 0); }
 static int f3_variant(int mode) {
-    const int def = mode == 0 ? 1 : (mode == 1 ? 3 : (mode == 2 ? 9 : 7));
+    const int def = mode == 0 ? 1 : (mode == 1 ? 3 : (mode == 2 ? 9 : (mode == 3 ? 7 : 11)));
     const char *e = std::getenv("QUAPI_F3");
     if (!e) return def;
     const int v = std::atoi(e);
@@ -1496,7 +1541,7 @@ static int fused_occ_t() {
 // M = 2: the lattice and general class maps give the same classes; the host uses LAT = false.
 static size_t fused3_dyn(int block, bool ro, int pfm) {
     const size_t F = block / 4;
-    return ((pfm == 2 ? F * 64 + 2 * 3 * 2 * 2 * F + F : 0) + (size_t)(block / 32) * 16 * 8 + (ro ? (size_t)3 * 4 * block : 0)) * 16;
+    return ((pfm >= 2 ? F * 64 + 2 * 3 * 2 * 2 * F + F : 0) + (size_t)(block / 32) * 16 * 8 + (ro ? (size_t)3 * 4 * block : 0)) * 16;
 }
 
 template <bool SYM, int MAP, int BLOCK, int MINB, int PF>

@@ -63,10 +63,12 @@ struct FusedArgs {
     int fixed_last;          // sub-step 0 'last' slot is a (fixed) shard slot: its value; else -1
     int rho_accumulate;      // 1: rho[n] += sum (several shard blocks contribute to one step)
     int lane_map;            // k_fused3 lane map (kernels.cu): 1 when tile fibres t, t+1 are adjacent in HBM
-    int use_tma;             // k_fused3 (lane map 1, unsharded): rounds staged by TMA through `tmap`
+    int use_tma;             // k_fused3 (unsharded): rounds staged by TMA through `tmap` (1) or cp.async (2)
     long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view (view B: 1)
     int tma_c0m;             // TMA coordinate 0 = tma_c0m x (G mod tma_nA) doubles
     int tma_sf, tma_s[3];    // stage strides (entries) of the round's fibre f and inner digits d0, d1, d2
+    int stg_lg[4], stg_s[4], stg_fi, stg_swz;  // cp.async staging (use_tma = 2): fields in HBM order, kernels.cu
+    long long stg_g[4];
     alignas(64) CUtensorMap tmap;
     int var[kMaxS];          // beta variant per sub-step: 1 for the first slide step k == L (initial-edge
                              // classes of the partner sigma_0), else 0 (SmallLayout::beta)
@@ -119,7 +121,7 @@ int fused_tile_digits_min(int M, int S, int kind);  // smallest v the kernel sup
 int fused_block(int M, int S, int kind);
 // Launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool readout, int grid, cudaStream_t s);
-// mode (k_fused3): lane map + 2 x TMA staging
+// mode (k_fused3): lane map + 2 x TMA staging; 4 = cp.async staging (lane map 0)
 int fused3_round_fibres(int mode);  // outer fibres per round (BLOCK / 4) of the mode's k_fused3 variant
 int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int mode = 0);  // resident CTAs per SM (needs a device)
 cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaStream_t s);
