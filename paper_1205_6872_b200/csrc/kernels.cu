@@ -1289,6 +1289,213 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
 }
 
 // --------------------------------------------------------------------------------------------
+// k_fused3s: shared-memory-resident rounds (TMA view A launch sets).  A round = F = 32 consecutive
+// outer fibres x the 64 inner entries, staged by TMA into one of two buffers (the next round lands
+// while this one is computed).  The three sub-steps run fibre by fibre on the staged round in place:
+// lane = outer fibre, warp = inner combination (warp-uniform KU rows and 'last' for sub-steps 1, 2;
+// stage reads/writes are 32 consecutive 16-B words), one CTA barrier between sub-steps; sub-step 2's
+// outputs go straight to HBM (32 lanes = 512 contiguous bytes).  No super-fibre in registers and the
+// readout accumulators stay in registers: 16 warps per SM instead of 8.
+// Stage layout [d2][d1][d0][f] (the view-A box).
+// --------------------------------------------------------------------------------------------
+template <bool SYM, int BLOCK, bool RO>
+__global__ void __launch_bounds__(BLOCK, 2) k_fused3s(const __grid_constant__ FusedArgs a) {
+    constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2, F = 32, W = BLOCK / 32, RPW = 16 / W;
+    constexpr int NK = RO ? 2 : 1;
+    constexpr bool LAT = false;
+    static_assert(16 % W == 0, "inner combinations per warp");
+    const SmallLayout lay{N, D, 0};
+    __shared__ double2 sK[2][N][N];
+    __shared__ double2 sIn[S][S][2][D][N];
+    __shared__ double2 KU[S][NK][Q][N][N];
+    __shared__ double2 sEhi[S][NK][D];
+    __shared__ double2 sBeta[S][2][D][N];
+    __shared__ long long sBase;
+    __shared__ int sLast;
+    __shared__ __align__(8) unsigned long long sFull[2];
+    extern __shared__ __align__(1024) double2 dyn_smem_raw[];
+    double2 *const stage0 = dyn_smem_raw;                               // [2][64 F]
+    double2 *const sE0 = dyn_smem_raw + 2 * 64 * F;                      // [2][S][2][D][F]
+    int2 *const sLo = reinterpret_cast<int2 *>(sE0 + 2 * S * 2 * D * F);  // [2][F]
+    for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
+    for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
+    for (int i = threadIdx.x; i < S * 2 * D * N; i += BLOCK) {
+        const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
+        (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = a.n_tiles / (int)gridDim.x, rem = a.n_tiles % (int)gridDim.x;
+    const int t_begin = (int)blockIdx.x * per + min((int)blockIdx.x, rem);
+    const int t_end = t_begin + per + ((int)blockIdx.x < rem ? 1 : 0);
+    const int rounds = a.T / F;
+    constexpr int NKU = S * NK * Q * N * N;
+    double2 accR[RO ? S : 1][RO ? N : 1];
+#pragma unroll
+    for (int s = 0; s < (RO ? S : 1); ++s)
+#pragma unroll
+        for (int n = 0; n < (RO ? N : 1); ++n) accR[s][n] = make_double2(0.0, 0.0);
+
+    auto issue = [&](int tau, int rd, int b) {  // thread 0: TMA box + E0 / offsets of unit (tau, rd)
+        const long long G = (long long)tau * a.T + (long long)rd * F;
+        fence_proxy_async();
+        mbar_expect_tx(&sFull[b], F * 64 * 16 + S * 2 * D * F * 16 + F * 8);
+        tma_load_5d(stage0 + b * 64 * F, &a.tmap, &sFull[b], (int)(a.tma_c0m * (G % a.tma_nA)), (int)(G / a.tma_nA));
+        for (int q = 0; q < S * 2 * D; ++q) {
+            const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
+            bulk_g2s(sE0 + ((size_t)b * S * 2 * D + q) * F, a.Etab + ((((size_t)st * 2 + kap) * a.G) * D + d) * a.X + rd * F,
+                     F * 16, &sFull[b]);
+        }
+        bulk_g2s(sLo + b * F, a.lofs + rd * F, F * 8, &sFull[b]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&sFull[0], 1);
+        mbar_init(&sFull[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && t_begin < t_end) {
+        issue(t_begin, 0, 0);
+        if (rounds > 1) issue(t_begin, 1, 1);
+        else if (t_begin + 1 < t_end) issue(t_begin + 1, 0, 1);
+    }
+    unsigned u = 0;  // unit counter of this CTA
+    for (int tau = t_begin; tau < t_end; ++tau) {
+        __syncthreads();  // previous tile's KU no longer in use
+        if ((int)threadIdx.x < S * NK * D) {
+            const int s = threadIdx.x / (NK * D), kap = (threadIdx.x / D) % NK, d = threadIdx.x % D;
+            double2 e = make_double2(1.0, 0.0);
+            for (int g = 1; g < a.G; ++g)
+                e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
+            sEhi[s][kap][d] = cmul(e, a.fixfac[s][kap][d]);
+        }
+        if ((int)threadIdx.x == BLOCK - 1) {
+            long long b = 0;
+            for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+            sBase = b;
+            sLast = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
+        }
+        __syncthreads();
+        for (int jj = threadIdx.x; jj < NKU; jj += BLOCK) {
+            const int last = jj % N, nw = (jj / N) % N, rr = (jj / (N * N)) % Q, kap = (jj / (N * N * Q)) % NK,
+                      s = jj / (N * N * Q * NK);
+            const int c = class_of(M, LAT, nw / M, nw % M);
+            double2 e = sK[kap][nw][last];
+            if (c > 0) {
+                e = cmul(e, sEhi[s][kap][c - 1]);
+                for (int i = 0; i < S; ++i)
+                    if (i != s) e = cmul(e, sIn[s][i][kap][c - 1][fib_digit<N, S>(s, rr, i)]);
+            }
+            KU[s][kap][rr][nw][last] = e;
+        }
+        __syncthreads();
+        const long long tbase = sBase;
+        const int last_t = sLast;
+        for (int rd = 0; rd < rounds; ++rd, ++u) {
+            const int b = u & 1;
+            mbar_wait(&sFull[b], (u >> 1) & 1);
+            double2 *const st = stage0 + b * 64 * F;
+            const int2 lo = sLo[b * F + lane];
+            const long long gbase = tbase + lo.x;
+            const int last0 = lo.y >= 0 ? lo.y : last_t;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const bool ro = RO && a.rho[s] != nullptr;
+                double2 E00[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) E00[d] = sE0[((b * S + s) * 2 * D + d) * F + lane];
+                double2 acc[RO ? N : 1];
+#pragma unroll
+                for (int n = 0; n < (RO ? N : 1); ++n) acc[n] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < RPW; ++i) {
+                    const int rr = warp + W * i, lo2 = rr & 3, hi2 = rr >> 2;
+                    // entry v of this fibre: stage word e0 + v * ev; KU row r; previous point 'last'
+                    int e0, ev, r, last;
+                    if (s == 0) e0 = (hi2 * 16 + lo2 * 4) * F, ev = F, r = lo2 + 4 * hi2, last = last0;
+                    else if (s == 1) e0 = (hi2 * 16 + lo2) * F, ev = 4 * F, r = lo2 + 4 * hi2, last = lo2;
+                    else e0 = (hi2 * 4 + lo2) * F, ev = 16 * F, r = lo2 + 4 * hi2, last = hi2;
+                    double2 xf[N];
+#pragma unroll
+                    for (int v = 0; v < N; ++v) xf[v] = st[e0 + v * ev + lane];
+                    double2 S0, m[NK][D];
+                    if constexpr (SYM) {
+                        const double2 uu = cadd(xf[0], xf[3]), w = make_double2(xf[0].x - xf[3].x, xf[0].y - xf[3].y);
+                        const double2 p = cadd(xf[1], xf[2]), q = make_double2(xf[1].x - xf[2].x, xf[1].y - xf[2].y);
+                        S0 = cadd(uu, p);
+#pragma unroll
+                        for (int kap = 0; kap < NK; ++kap) {
+                            if (kap == 1 && !ro) break;
+                            const double cr = a.sym[s][kap][0], ci = a.sym[s][kap][1], ch = a.sym[s][kap][2],
+                                         sh = a.sym[s][kap][3];
+                            const double2 A = make_double2(fma(cr, uu.x, ch * p.x), fma(cr, uu.y, ch * p.y));
+                            const double2 Bv = make_double2(fma(-ci, w.y, sh * q.x), fma(ci, w.x, sh * q.y));
+                            m[kap][0] = cadd(A, Bv);
+                            m[kap][1] = make_double2(A.x - Bv.x, A.y - Bv.y);
+                        }
+                    } else {
+                        S0 = cadd(cadd(xf[0], xf[1]), cadd(xf[2], xf[3]));
+#pragma unroll
+                        for (int kap = 0; kap < NK; ++kap) {
+                            if (kap == 1 && !ro) break;
+#pragma unroll
+                            for (int d = 0; d < D; ++d) {
+                                double2 mm = cmul(sBeta[s][kap][d][0], xf[0]);
+#pragma unroll
+                                for (int v = 1; v < N; ++v) mm = cfma(sBeta[s][kap][d][v], xf[v], mm);
+                                m[kap][d] = mm;
+                            }
+                        }
+                    }
+                    const double2 *ku0 = &KU[s][0][r][0][0], *ku1 = &KU[s][NK - 1][r][0][0];
+                    if (ro) {
+#pragma unroll
+                        for (int d = 0; d < D; ++d)
+#pragma unroll
+                            for (int nw = 0; nw < N; ++nw)
+                                if (class_of(M, LAT, nw / M, nw % M) == d + 1)
+                                    acc[RO ? nw : 0] = cfma(ku1[nw * N + last], m[NK - 1][d], acc[RO ? nw : 0]);
+                    }
+                    double2 P[D];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) P[d] = cmul(E00[d], m[0][d]);
+#pragma unroll
+                    for (int nw = 0; nw < N; ++nw) {
+                        const int c = class_of(M, LAT, nw / M, nw % M);
+                        const double2 o = cmul(ku0[nw * N + last], c == 0 ? S0 : P[c > 0 ? c - 1 : 0]);
+                        if (ro && c == 0) acc[RO ? nw : 0] = cadd(acc[RO ? nw : 0], o);
+                        if (s < 2) st[e0 + nw * ev + lane] = o;
+                        else __stcs(a.A + gbase + (long long)lo2 * a.pw_in[0] + (long long)hi2 * a.pw_in[1] +
+                                        (long long)nw * a.pw_in[2], o);
+                    }
+                }
+                if (ro) {
+#pragma unroll
+                    for (int n = 0; n < N; ++n) {
+                        const int c = class_of(M, LAT, n / M, n % M);
+                        if (c > 0)
+                            acc[RO ? n : 0] = cmul(sE0[((b * S + s) * 2 * D + D + (c > 0 ? c - 1 : 0)) * F + lane], acc[RO ? n : 0]);
+                        accR[RO ? s : 0][RO ? n : 0] = cadd(accR[RO ? s : 0][RO ? n : 0], acc[RO ? n : 0]);
+                    }
+                }
+                __syncthreads();  // sub-step s complete on the whole round (after s = 2: stage b free)
+            }
+            if (threadIdx.x == 0) {  // refill buffer b with unit u + 2
+                int tn = tau, rn = rd + 2;
+                while (rn >= rounds && tn < t_end) rn -= rounds, ++tn;
+                if (tn < t_end) issue(tn, rn, b);
+            }
+        }
+    }
+    if constexpr (RO) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (a.rho[s] != nullptr)
+                reduce_finalize<N, BLOCK>(accR[s], a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
+                                          a.rho_accumulate != 0);
+    }
+}
+
+// --------------------------------------------------------------------------------------------
 // Growth step 1 <= k < L: A_{k-1} (digits 0..k-1) -> A_k (digits 0..k), in place:
 //   A_k[x + v N^k] = K'(v, d_{k-1}(x)) exp(Ds(v) Psi_k(x)) A_{k-1}[x],
 //   Psi_k(x) = sum_{j=1..k} psi_{k,j}(d_{k-j}(x)),   classes eta_j (j<k), E_k (j=k, partner sigma_0).
@@ -1390,21 +1597,22 @@ static int eff_kind(int M, int S, int kind) { return kind == 4 ? ((M == 2 && S =
 #define QP_F3_CFGS(X)                                                                              \
     X(0, 0, 256, 2, 0) X(1, 0, 192, 2, 0) X(2, 0, 128, 3, 0) X(3, 1, 128, 3, 0) X(4, 1, 256, 1, 0) \
     X(5, 1, 384, 1, 0) X(6, 1, 128, 2, 1) X(7, 3, 128, 2, 2) X(8, 3, 256, 1, 2) X(9, 2, 128, 2, 2)              \
-    X(10, 2, 256, 1, 2) X(11, 4, 128, 2, 3)
+    X(10, 2, 256, 1, 2) X(11, 4, 128, 2, 3) X(12, 2, 256, 2, 4) X(13, 2, 128, 4, 4)
 static int f3_mode(const FusedArgs &a) { return a.use_tma == 2 ? 4 : (a.lane_map & 1) + (a.use_tma ? 2 : 0); }
-static int f3_variant(int mode) {
+static int f3_variant(int mode, bool view_a = true) {
     const int def = mode == 0 ? 1 : (mode == 1 ? 3 : (mode == 2 ? 9 : (mode == 3 ? 7 : 11)));
     const char *e = std::getenv("QUAPI_F3");
     if (!e) return def;
     const int v = std::atoi(e);
-#define X(I, MD, B, MB, PM) if (v == I) return MD == mode ? I : def;
+    // k_fused3s (PM 4) assumes the view-A stage layout
+#define X(I, MD, B, MB, PM) if (v == I) return (MD == mode && (PM != 4 || view_a)) ? I : def;
     QP_F3_CFGS(X)
 #undef X
     return def;
 }
 int fused3_round_fibres(int mode) {
     const int v = f3_variant(mode);
-#define X(I, MD, B, MB, PM) if (v == I) return B / 4;
+#define X(I, MD, B, MB, PM) if (v == I) return PM == 4 ? 32 : B / 4;
     QP_F3_CFGS(X)
 #undef X
     return 32;
@@ -1544,8 +1752,21 @@ static size_t fused3_dyn(int block, bool ro, int pfm) {
     return ((pfm >= 2 ? F * 64 + 2 * 3 * 2 * 2 * F + F : 0) + (size_t)(block / 32) * 16 * 8 + (ro ? (size_t)3 * 4 * block : 0)) * 16;
 }
 
+static constexpr size_t fused3s_dyn() { return (size_t)(2 * 64 * 32 + 2 * 3 * 2 * 2 * 32 + 32) * 16; }
+
 template <bool SYM, int MAP, int BLOCK, int MINB, int PF>
 static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    if constexpr (PF == 4) {
+        const size_t dyn = fused3s_dyn();
+        if (ro) {
+            cudaFuncSetAttribute(k_fused3s<SYM, BLOCK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            k_fused3s<SYM, BLOCK, true><<<grid, BLOCK, dyn, s>>>(a);
+        } else {
+            cudaFuncSetAttribute(k_fused3s<SYM, BLOCK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            k_fused3s<SYM, BLOCK, false><<<grid, BLOCK, dyn, s>>>(a);
+        }
+        return cudaGetLastError();
+    }
     const size_t dyn = fused3_dyn(BLOCK, ro, PF);
     if (ro) {
         cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -1560,6 +1781,14 @@ static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t 
 template <bool SYM, int MAP, int BLOCK, int MINB, int PF>
 static int fused3_occ_t() {
     int o1 = 0, o2 = 0;
+    if constexpr (PF == 4) {
+        const size_t dyn = fused3s_dyn();
+        cudaFuncSetAttribute(k_fused3s<SYM, BLOCK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_fused3s<SYM, BLOCK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_fused3s<SYM, BLOCK, true>, BLOCK, dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_fused3s<SYM, BLOCK, false>, BLOCK, dyn);
+        return o1 < o2 ? o1 : o2;
+    }
     const size_t d1 = fused3_dyn(BLOCK, true, PF), d2 = fused3_dyn(BLOCK, false, PF);
     cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d1);
     cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d2);
@@ -1572,7 +1801,7 @@ cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const F
     kind = eff_kind(M, S, kind);
     if (kind == 4) {
 #define X(I, MD, B, MB, PF)                                                                          \
-        if (f3_variant(f3_mode(a)) == I)                                                                 \
+        if (f3_variant(f3_mode(a), a.tma_sf == 1) == I)                                                                 \
             return sym ? fused3_t<true, (MD & 1), B, MB, PF>(a, ro, grid, s) : fused3_t<false, (MD & 1), B, MB, PF>(a, ro, grid, s);
         QP_F3_CFGS(X)
 #undef X
