@@ -54,6 +54,7 @@ class _Problem(ctypes.Structure):
         ("L", ctypes.c_int32),
         ("G_in", ctypes.POINTER(ctypes.c_double)),
         ("reading", ctypes.c_int32),
+        ("H_t", ctypes.POINTER(ctypes.c_double)),
     ]
 
 
@@ -107,6 +108,7 @@ class Problem:
     L: int = 3
     G_in: Optional[np.ndarray] = None
     reading: int = READING_STRANG
+    H_t: Optional[np.ndarray] = None  # [n_steps, M, M]: H on interval (t_{k-1}, t_k] of step k
     _keep: list = field(default_factory=list, repr=False)
 
     @property
@@ -123,11 +125,18 @@ class Problem:
             ga = np.ascontiguousarray(np.asarray(self.G_in, dtype=np.complex128)).view(np.float64)
             keep.append(ga)
             g = _dptr(ga)
+        ht = None
+        if self.H_t is not None:
+            ha = np.ascontiguousarray(np.asarray(self.H_t, dtype=np.complex128)).view(np.float64)
+            if ha.size != 2 * int(self.n_steps) * self.M * self.M:
+                raise ValueError("H_t must have shape [n_steps, M, M]")
+            keep.append(ha)
+            ht = _dptr(ha)
         self._keep = keep
         return _Problem(
             self.M, _dptr(s), _dptr(H), _dptr(r), int(self.kind), float(self.coupling),
             float(self.omega_c), float(self.kT), float(self.dt), int(self.n_steps), int(self.L),
-            g, int(self.reading),
+            g, int(self.reading), ht,
         )
 
 

@@ -382,6 +382,32 @@ typedef struct {
 
 static void ctx_free(ctx_t *c) { free(c->sp); free(c->sm); free(c->K); free(c->rho0); free(c->G); }
 
+/* K[sig' * N + sig] = U[a',a] conj(U[b',b]) with U = exp(-i H dt) for the Hamiltonian H (Eq. 8):
+   <s+_{k+1}|e^{-iH dt}|s+_k> <s-_k|e^{+iH dt}|s-_{k+1}>. */
+static void build_K(const or_problem *p, const double *H, cplx *K) {
+    const int M = p->M, N = M * M;
+    or_problem q = *p;
+    q.H = H;
+    double *U = malloc(sizeof(double) * 2 * M * M);
+    or_propagator(&q, U);
+    for (int a1 = 0; a1 < M; ++a1)
+        for (int b1 = 0; b1 < M; ++b1)
+            for (int a = 0; a < M; ++a)
+                for (int b = 0; b < M; ++b) {
+                    cplx ua = U[2 * (a1 * M + a)] + I * U[2 * (a1 * M + a) + 1];
+                    cplx ub = U[2 * (b1 * M + b)] + I * U[2 * (b1 * M + b) + 1];
+                    K[(a1 * M + b1) * N + (a * M + b)] = ua * conj(ub);
+                }
+    free(U);
+}
+
+/* propagator pair of step k (interval (t_{k-1}, t_k]): the time-dependent H_t[k-1] if given, else c->K */
+static const cplx *step_K(const or_problem *p, const ctx_t *c, int64_t k, cplx *buf) {
+    if (!p->H_t) return c->K;
+    build_K(p, p->H_t + 2 * (size_t)(k - 1) * c->M * c->M, buf);
+    return buf;
+}
+
 static int validate(const or_problem *p) {
     if (p->M < 1 || p->M > 8 || !p->s || !p->H || !p->rho0) return fail("config: need 1<=M<=8 and s/H/rho0");
     if (p->L < 1 || p->L > 60) return fail("config: L (Delta k_max) must be in [1,60]");
@@ -399,6 +425,15 @@ static int validate(const or_problem *p) {
             if (fabs(rr - qr) > 1e-12 || fabs(ri + qi) > 1e-12) return fail("config: rho0 not Hermitian");
         }
     for (int i = 0; i < M; ++i) { tr_re += p->rho0[2 * (i * M + i)]; tr_im += p->rho0[2 * (i * M + i) + 1]; }
+    if (p->H_t)
+        for (int64_t k = 0; k < p->n_steps; ++k)
+            for (int i = 0; i < M; ++i)
+                for (int j = 0; j < M; ++j) {
+                    const double *h = p->H_t + 2 * (k * M * M);
+                    if (fabs(h[2 * (i * M + j)] - h[2 * (j * M + i)]) > 1e-12 ||
+                        fabs(h[2 * (i * M + j) + 1] + h[2 * (j * M + i) + 1]) > 1e-12)
+                        return fail("config: H_t not Hermitian");
+                }
     if (fabs(tr_re - 1.0) > 1e-12 || fabs(tr_im) > 1e-12) return fail("config: trace(rho0) != 1");
     return 0;
 }
@@ -410,24 +445,13 @@ static int ctx_init(const or_problem *p, ctx_t *c) {
     c->M = M; c->N = N;
     c->sp = malloc(sizeof(double) * N); c->sm = malloc(sizeof(double) * N);
     c->K = malloc(sizeof(cplx) * N * N); c->rho0 = malloc(sizeof(cplx) * N);
-    double *U = malloc(sizeof(double) * 2 * M * M);
-    or_propagator(p, U);
     for (int a = 0; a < M; ++a)
         for (int b = 0; b < M; ++b) {
             int sg = a * M + b;
             c->sp[sg] = p->s[a]; c->sm[sg] = p->s[b];
             c->rho0[sg] = p->rho0[2 * sg] + I * p->rho0[2 * sg + 1];
         }
-    for (int a1 = 0; a1 < M; ++a1)
-        for (int b1 = 0; b1 < M; ++b1)
-            for (int a = 0; a < M; ++a)
-                for (int b = 0; b < M; ++b) {
-                    cplx ua = U[2 * (a1 * M + a)] + I * U[2 * (a1 * M + a) + 1];
-                    cplx ub = U[2 * (b1 * M + b)] + I * U[2 * (b1 * M + b) + 1];
-                    /* <s+_{k+1}|e^{-iH dt}|s+_k> <s-_k|e^{+iH dt}|s-_{k+1}> = U[a1,a] conj(U[b1,b]) */
-                    c->K[(a1 * M + b1) * N + (a * M + b)] = ua * conj(ub);
-                }
-    free(U);
+    build_K(p, p->H, c->K);
     if (build_G(p, &c->G, &c->nG)) { ctx_free(c); return 1; }
     return 0;
 }
@@ -466,11 +490,18 @@ int or_brute_force(const or_problem *p, double *rho_out) {
         for (int64_t tp = (t - p->L > 0 ? t - p->L : 0); tp <= t; ++tp) eta[t * W + tp] = eta_of(&ec, t, tp, Nt);
     cplx *acc = calloc((size_t)N, sizeof(cplx));
     int *path = malloc(sizeof(int) * (size_t)W);
+    /* Kt[t]: propagator pair of the interval (t_t, t_{t+1}] = step t+1 */
+    cplx *Kt = malloc(sizeof(cplx) * (size_t)Nt * N * N);
+    for (int64_t t = 0; t < Nt; ++t) {
+        cplx *buf = Kt + (size_t)t * N * N;
+        const cplx *k = step_K(p, &c, t + 1, buf);
+        if (k != buf) memcpy(buf, k, sizeof(cplx) * N * N);
+    }
     for (int64_t x = 0; x < npaths; ++x) {
         int64_t r = x;
         for (int64_t t = 0; t <= Nt; ++t) { path[t] = (int)(r % N); r /= N; }
         cplx w = c.rho0[path[0]];
-        for (int64_t t = 0; t < Nt; ++t) w *= c.K[path[t + 1] * N + path[t]];
+        for (int64_t t = 0; t < Nt; ++t) w *= Kt[(size_t)t * N * N + path[t + 1] * N + path[t]];
         if (w == 0) continue;
         cplx phase = 0;
         for (int64_t t = 0; t <= Nt; ++t)
@@ -484,7 +515,7 @@ int or_brute_force(const or_problem *p, double *rho_out) {
     }
     for (int sg = 0; sg < N; ++sg) { rho_out[2 * sg] = creal(acc[sg]); rho_out[2 * sg + 1] = cimag(acc[sg]); }
     (void)M;
-    free(eta); free(acc); free(path); ctx_free(&c);
+    free(eta); free(acc); free(path); free(Kt); ctx_free(&c);
     return 0;
 }
 
@@ -515,7 +546,8 @@ static cplx pairwise(const cplx *v, int64_t n) {
 }
 
 /* rho_k(sg_k) = sum_x K(sg_k, sg_{k-1}) prod_{j=0}^{min(k,L)} I_term(sg_k, sg_{k-j}) A_{k-1}[x]   (k >= 1) */
-static void readout(const ctx_t *c, const cplx *A, int w_old, const cplx *tab_term, int64_t k, int L, cplx *rho) {
+static void readout(const ctx_t *c, const cplx *K, const cplx *A, int w_old, const cplx *tab_term, int64_t k, int L,
+                    cplx *rho) {
     const int N = c->N;
     const int64_t n = ipow(N, w_old), BLK = 4096;
     const int64_t nblk = (n + BLK - 1) / BLK;
@@ -532,7 +564,7 @@ static void readout(const ctx_t *c, const cplx *A, int w_old, const cplx *tab_te
                 for (int64_t x = lo; x < hi; ++x) {
                     int64_t r = x;
                     for (int i = 0; i < w_old; ++i) { dig[i] = (int)(r % N); r /= N; } /* dig[i] = sigma_{k-1-i} */
-                    cplx f = c->K[sk * N + dig[0]] * tab_term[sk * N + sk];
+                    cplx f = K[sk * N + dig[0]] * tab_term[sk * N + sk];
                     for (int j = 1; j <= jmax; ++j) f *= tab_term[(size_t)j * N * N + sk * N + dig[j - 1]];
                     buf[x - lo] = f * A[x];
                 }
@@ -580,12 +612,14 @@ int or_run(const or_problem *p, const int64_t *out_steps, int64_t n_out, double 
     int64_t n_slide = 0;
     int w_old = 1;
     cplx rho[64];
+    cplx *Kbuf = malloc(sizeof(cplx) * (size_t)N * N);
     for (int64_t k = 1; k <= Nt; ++k) {
         double ts = now_s();
+        const cplx *Kk = step_K(p, &c, k, Kbuf); /* propagator pair of step k */
         /* readout of rho(t_k) from A_{k-1} (terminal classes) */
         if (o < n_out && out_steps[o] == k) {
             step_tables(&c, &ec, k, L, k, tabt);
-            readout(&c, A, w_old, tabt, k, L, rho);
+            readout(&c, Kk, A, w_old, tabt, k, L, rho);
             for (int sg = 0; sg < N; ++sg) {
                 rho_out[2 * (o * N + sg)] = creal(rho[sg]);
                 rho_out[2 * (o * N + sg) + 1] = cimag(rho[sg]);
@@ -613,12 +647,12 @@ int or_run(const or_problem *p, const int64_t *out_steps, int64_t n_out, double 
                 for (int j = 0; j <= jin; ++j) f *= tabp[(size_t)j * N * N + sk * N + dig[j]];
                 if (!contract) { /* growth: no sum, old index = y without its newest digit */
                     int64_t x = y / N;
-                    B[y] = f * c.K[sk * N + (int)(x % N)] * A[x];
+                    B[y] = f * Kk[sk * N + (int)(x % N)] * A[x];
                 } else {         /* slide: sum over sigma_{k-L} = most significant digit of the old index */
                     cplx s = 0;
                     for (int so = 0; so < N; ++so) {
                         int64_t x = y / N + (int64_t)so * top; /* sigma_{k-1} = x % N */
-                        s += tabp[(size_t)L * N * N + sk * N + so] * c.K[sk * N + (int)(x % N)] * A[x];
+                        s += tabp[(size_t)L * N * N + sk * N + so] * Kk[sk * N + (int)(x % N)] * A[x];
                     }
                     B[y] = f * s;
                 }
@@ -630,6 +664,6 @@ int or_run(const or_problem *p, const int64_t *out_steps, int64_t n_out, double 
         if (contract) { t_slide += dtk; ++n_slide; } else t_grow += dtk;
     }
     if (timings) { timings[0] = t_setup; timings[1] = t_grow; timings[2] = t_slide; timings[3] = (double)n_slide; }
-    free(A); free(B); free(tabp); free(tabt); ctx_free(&c);
+    free(A); free(B); free(tabp); free(tabt); free(Kbuf); ctx_free(&c);
     return 0;
 }

@@ -37,6 +37,9 @@ typedef struct {
     const double *G_in;    /* optional [(2L+3)*2]: G(m dt/2), m=0..2L+2, replaces the
                               quadrature (the paper's "alpha(t) given" input)            */
     int32_t reading;       /* OR_READING_STRANG (default) or OR_READING_AS_PRINTED              */
+    const double *H_t;     /* optional [n_steps][M*M*2]: time-dependent Hamiltonian, H_t[k-1] acts on
+                              the interval (t_{k-1}, t_k] of step k (the driven model of Sec. III,
+                              Omega(t) of P:288); NULL => H on every interval        */
 } or_problem;
 
 /* G(tau) = int_0^tau dt' int_0^t' dt'' alpha(t'-t'')  (Eq. 4 integrated twice). */
