@@ -172,6 +172,44 @@ void qp_plan_destroy(qp_plan *plan);
 /* Library build identification, e.g. "quapi 0.1 sm_100a". */
 const char *qp_version(void);
 
+/* ---------------------------------------------------------------- batched sweeps
+   B independent problems that share M, s, the bath, dt, L = dkmax, n_steps and out_steps, each with
+   its own initial state and its own drive: problem b propagates on the interval (t_{k-1}, t_k] of step
+   k with H_b(k) = H0 + f[b * n_steps + k - 1] * H1 -- the driven quantum dot of the paper's Sec. III
+   (Omega(t) of P:288), whose rho_11 is swept over pulse areas.  Step k uses the propagator
+   pair K_k = U_k (x) conj(U_k), U_k = exp(-i H_b(k) dt) (Eq. 8 with a step-dependent H); everything
+   else (eta classes, windows, readout from A_{k-1}) is the single-problem method.  One CTA owns one
+   problem for the whole run (one kernel launch, every step inside it). */
+typedef struct {
+    qp_problem base;         /* shared parameters; base.H = H0, base.rho0 = initial state of every problem
+                                unless rho0 below is given (base.rho0 is validated either way)          */
+    int32_t B;               /* number of problems >= 1                                                  */
+    const qp_c64 *H1;        /* [M*M] Hermitian drive operator, or NULL (no drive)                       */
+    const double *f;         /* [B][n_steps] finite drive amplitudes, or NULL (all 0)                    */
+    const qp_c64 *rho0;      /* [B][M*M] per-problem initial states (Hermitian, trace 1), or NULL      */
+} qp_batch;
+
+typedef struct qp_batch_plan qp_batch_plan;
+
+typedef struct {
+    int32_t B, M, N, L;
+    int64_t ardm_entries;    /* B * N^L                                                                  */
+    int64_t ardm_bytes;      /* 16 * B * N^L: the caller's ARDM buffer (problem b at offset 16 b N^L)    */
+    int64_t work_bytes;      /* device workspace (tables, drive, initial states, rho outputs)            */
+    int64_t n_out, n_steps;
+    int32_t block;           /* threads per problem (one CTA per problem)                                */
+    double setup_seconds;
+} qp_batch_sizes;
+
+/* Host only: validate (base as qp_plan_create; H1 Hermitian; f finite; each rho0 Hermitian with trace
+   1), eta and tables of the shared bath.  Errors as qp_plan_create. */
+qp_status qp_batch_create(const qp_batch *batch, qp_batch_plan **out);
+qp_status qp_batch_query(const qp_batch_plan *plan, qp_batch_sizes *out);
+/* Enqueue the whole batched run on `stream` (H2D of the tables, one kernel launch).  If rho_out is
+   not NULL, synchronises and writes rho_out[B][n_out][M][M] (host, caller-owned). */
+qp_status qp_batch_run(qp_batch_plan *plan, void *d_ardm, void *d_work, void *stream, qp_c64 *rho_out);
+void qp_batch_destroy(qp_batch_plan *plan);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1292,3 +1292,169 @@ qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_loc
 }
 
 }  // extern "C"
+
+// ===================================================================================== batched sweeps
+// B problems sharing the bath / grid, each with its own drive amplitude and initial state
+// (include/quapi.h).  The shared parts (validation, eta classes, Delta-s classes) come from an
+// internal qp_plan of the base problem; the device image holds the per-lag psi rows, the two
+// Hamiltonian parts, the drive amplitudes, the initial states and the output map.
+struct qp_batch_plan {
+    qp_plan *P = nullptr;
+    int B = 0;
+    std::vector<double2> tab, rho0;
+    std::vector<double> f;
+    std::vector<int> out_idx;
+    size_t off_tab = 0, off_f = 0, off_rho0 = 0, off_idx = 0, off_rho = 0, work_bytes = 0;
+    double setup_seconds = 0.0;
+};
+
+extern "C" {
+
+qp_status qp_batch_create(const qp_batch *bt, qp_batch_plan **out) {
+    if (!bt || !out) return err(QP_ERR_ARG, "arg: NULL batch or out");
+    *out = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (bt->B < 1) return err(QP_ERR_CONFIG, "config: batch size B must be >= 1 (got %d)", bt->B);
+    qp_problem base = bt->base;
+    const int64_t mb = base.max_bytes;
+    base.max_bytes = 0;  // capacity is checked for the whole batch below
+    qp_plan *P = nullptr;
+    qp_status st = qp_plan_create(&base, &P);
+    if (st) return st;
+    const int M = P->M, N = P->N, L = P->L;
+    auto fail = [&](qp_status code, const char *msg) {
+        qp_plan_destroy(P);
+        return err(code, "%s", msg);
+    };
+    if (bt->H1) {
+        for (int i = 0; i < M; ++i)
+            for (int j = 0; j < M; ++j) {
+                const cd h = {bt->H1[i * M + j].re, bt->H1[i * M + j].im}, hT = {bt->H1[j * M + i].re, bt->H1[j * M + i].im};
+                if (!(std::abs(h - std::conj(hT)) <= 1e-12) || !std::isfinite(h.real()) || !std::isfinite(h.imag()))
+                    return fail(QP_ERR_CONFIG, "config: H1 not Hermitian");
+            }
+    }
+    if (bt->f)
+        for (int64_t i = 0; i < (int64_t)bt->B * P->n_steps; ++i)
+            if (!std::isfinite(bt->f[i])) return fail(QP_ERR_CONFIG, "config: drive amplitude f not finite");
+    if (bt->rho0)
+        for (int b = 0; b < bt->B; ++b) {
+            const qp_c64 *r = bt->rho0 + (size_t)b * N;
+            cd tr = 0.0;
+            for (int i = 0; i < M; ++i) {
+                for (int j = 0; j < M; ++j) {
+                    const cd x = {r[i * M + j].re, r[i * M + j].im}, xT = {r[j * M + i].re, r[j * M + i].im};
+                    if (!(std::abs(x - std::conj(xT)) <= 1e-12)) return fail(QP_ERR_CONFIG, "config: a batch rho0 is not Hermitian");
+                }
+                tr += cd(r[i * M + i].re, r[i * M + i].im);
+            }
+            if (!(std::abs(tr - 1.0) <= 1e-12)) return fail(QP_ERR_CONFIG, "config: a batch rho0 does not have trace 1");
+        }
+    const double bytes = 16.0 * bt->B * std::pow((double)N, L);
+    if (mb > 0 && bytes > (double)mb) {
+        qp_plan_destroy(P);
+        return err(QP_ERR_CAPACITY, "capacity: need %.0f B for the batch ARDM, budget %lld B", bytes, (long long)mb);
+    }
+    auto *bp = new qp_batch_plan;
+    bp->P = P;
+    bp->B = bt->B;
+    // psi rows (lag j = 1..L), self classes, H0, H1
+    bp->tab.assign((size_t)(3 * (L + 1) + 2) * N + 2 * M * M, make_double2(0.0, 0.0));
+    for (int j = 1; j <= L; ++j)
+        for (int sg = 0; sg < N; ++sg) {
+            bp->tab[(size_t)j * N + sg] = d2(psi(*P, sg, P->eta[j]));
+            bp->tab[(size_t)(L + 1 + j) * N + sg] = d2(psi(*P, sg, P->E[j]));
+            bp->tab[(size_t)(2 * (L + 1) + j) * N + sg] = d2(psi(*P, sg, P->TI[j]));
+        }
+    for (int sg = 0; sg < N; ++sg) {
+        bp->tab[(size_t)3 * (L + 1) * N + sg] = d2(psi(*P, sg, P->self_int));
+        bp->tab[(size_t)(3 * (L + 1) + 1) * N + sg] = d2(psi(*P, sg, P->self_end));
+    }
+    const size_t oh = (size_t)(3 * (L + 1) + 2) * N;
+    for (int i = 0; i < M * M; ++i) {
+        bp->tab[oh + i] = d2(P->H[i]);
+        bp->tab[oh + M * M + i] = bt->H1 ? make_double2(bt->H1[i].re, bt->H1[i].im) : make_double2(0.0, 0.0);
+    }
+    if (bt->f && bt->H1) bp->f.assign(bt->f, bt->f + (size_t)bt->B * P->n_steps);
+    bp->rho0.resize((size_t)bt->B * N);
+    for (int b = 0; b < bt->B; ++b)
+        for (int n = 0; n < N; ++n)
+            bp->rho0[(size_t)b * N + n] = bt->rho0 ? make_double2(bt->rho0[(size_t)b * N + n].re, bt->rho0[(size_t)b * N + n].im)
+                                                   : d2(P->rho0[n]);
+    bp->out_idx.assign((size_t)P->n_steps + 1, -1);
+    for (size_t o = 0; o < P->out_steps.size(); ++o) bp->out_idx[(size_t)P->out_steps[o]] = (int)o;
+    size_t off = 0;
+    bp->off_tab = off;  off = align256(off + bp->tab.size() * sizeof(double2));
+    bp->off_f = off;    off = align256(off + bp->f.size() * sizeof(double));
+    bp->off_rho0 = off; off = align256(off + bp->rho0.size() * sizeof(double2));
+    bp->off_idx = off;  off = align256(off + bp->out_idx.size() * sizeof(int));
+    bp->off_rho = off;  off = align256(off + (size_t)bt->B * P->out_steps.size() * N * sizeof(double2));
+    bp->work_bytes = off;
+    bp->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = bp;
+    return QP_OK;
+}
+
+qp_status qp_batch_query(const qp_batch_plan *bp, qp_batch_sizes *o) {
+    if (!bp || !o) return err(QP_ERR_ARG, "arg: NULL batch plan or out");
+    const qp_plan *P = bp->P;
+    o->B = bp->B;
+    o->M = P->M, o->N = P->N, o->L = P->L;
+    o->ardm_entries = (int64_t)bp->B * ipow(P->N, P->L);
+    o->ardm_bytes = 16 * o->ardm_entries;
+    o->work_bytes = (int64_t)bp->work_bytes;
+    o->n_out = (int64_t)P->out_steps.size();
+    o->n_steps = P->n_steps;
+    o->block = qp::kBatchBlock;
+    o->setup_seconds = bp->setup_seconds;
+    return QP_OK;
+}
+
+qp_status qp_batch_run(qp_batch_plan *bp, void *d_ardm, void *d_work, void *stream, qp_c64 *rho_out) {
+    if (!bp || !d_ardm || !d_work) return err(QP_ERR_ARG, "arg: NULL batch plan or device buffer");
+    const qp_plan *P = bp->P;
+    const int N = P->N;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *w = (char *)d_work;
+    QP_CUDA(cudaMemcpyAsync(w + bp->off_tab, bp->tab.data(), bp->tab.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+    if (!bp->f.empty())
+        QP_CUDA(cudaMemcpyAsync(w + bp->off_f, bp->f.data(), bp->f.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    QP_CUDA(cudaMemcpyAsync(w + bp->off_rho0, bp->rho0.data(), bp->rho0.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+    QP_CUDA(cudaMemcpyAsync(w + bp->off_idx, bp->out_idx.data(), bp->out_idx.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    qp::BatchArgs a{};
+    a.A = (double2 *)d_ardm;
+    a.tab = (const double2 *)(w + bp->off_tab);
+    a.f = bp->f.empty() ? nullptr : (const double *)(w + bp->off_f);
+    a.rho0 = (const double2 *)(w + bp->off_rho0);
+    a.out_idx = (const int *)(w + bp->off_idx);
+    a.rho = (double2 *)(w + bp->off_rho);
+    a.NL = ipow(N, P->L);
+    a.n_steps = P->n_steps;
+    a.dt = P->dt;
+    a.L = P->L;
+    a.n_out = (int)P->out_steps.size();
+    a.D = P->D;
+    for (int n = 0; n < N; ++n) {
+        a.cls[n] = qp::class_of(P->M, P->lattice, n / P->M, n % P->M);
+        a.dsig[n] = dsig(*P, n);
+    }
+    for (int d = 0; d < P->D; ++d) a.delta[d] = P->delta[d];
+    const cudaError_t e = qp::launch_batch(P->M, a, bp->B, s);
+    if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: batch launch failed: %s", cudaGetErrorString(e));
+    if (rho_out) {
+        const size_t n = (size_t)bp->B * P->out_steps.size() * N;
+        std::vector<double2> h(n);
+        QP_CUDA(cudaMemcpyAsync(h.data(), w + bp->off_rho, n * sizeof(double2), cudaMemcpyDeviceToHost, s));
+        QP_CUDA(cudaStreamSynchronize(s));
+        for (size_t i = 0; i < n; ++i) rho_out[i] = qp_c64{h[i].x, h[i].y};
+    }
+    return QP_OK;
+}
+
+void qp_batch_destroy(qp_batch_plan *bp) {
+    if (!bp) return;
+    qp_plan_destroy(bp->P);
+    delete bp;
+}
+
+}  // extern "C"

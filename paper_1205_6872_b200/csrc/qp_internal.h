@@ -126,4 +126,27 @@ int fused3_round_fibres(int mode);  // outer fibres per round (BLOCK / 4) of the
 int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int mode = 0);  // resident CTAs per SM (needs a device)
 cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaStream_t s);
 
+// Batched sweeps (batch.cu): B independent problems, one CTA each, every step in one launch.
+// Table image (double2 entries) at `tab`: psi_eta[L+1][N], psi_E[L+1][N], psi_TI[L+1][N] (lag j = 1..L;
+// psi(sigma', e) = -(e s+(sigma') - conj(e) s-(sigma'))), psi_self[2][N] (self interior G(1), self end
+// G(1/2)), H0[M*M], H1[M*M].
+struct BatchArgs {
+    double2 *A;              // [B][N^L] in place
+    const double2 *tab;
+    const double *f;         // [B][n_steps] drive amplitudes (nullptr: none)
+    const double2 *rho0;     // [B][N]
+    const int *out_idx;      // [n_steps + 1]: output slot of step k, or -1
+    double2 *rho;            // [B][n_out][N]
+    long long NL;            // N^L
+    long long n_steps;
+    double dt;
+    int L, n_out, D;
+    int cls[kMaxN];          // Delta-s class of pair state n (0: Delta s = 0, else d + 1)
+    double dsig[kMaxN];      // Delta s(n)
+    double delta[kMaxD];     // Delta s of class d + 1
+};
+size_t batch_dyn_smem(int M, int L);
+cudaError_t launch_batch(int M, const BatchArgs &a, int B, cudaStream_t s);
+constexpr int kBatchBlock = 256;
+
 }  // namespace qp

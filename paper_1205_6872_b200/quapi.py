@@ -72,11 +72,28 @@ class qp_shard_sizes(ctypes.Structure):
     ]
 
 
+class qp_batch(ctypes.Structure):
+    _fields_ = [
+        ("base", qp_problem), ("B", ctypes.c_int32), ("H1", ctypes.POINTER(qp_c64)),
+        ("f", ctypes.POINTER(ctypes.c_double)), ("rho0", ctypes.POINTER(qp_c64)),
+    ]
+
+
+class qp_batch_sizes(ctypes.Structure):
+    _fields_ = [
+        ("B", ctypes.c_int32), ("M", ctypes.c_int32), ("N", ctypes.c_int32), ("L", ctypes.c_int32),
+        ("ardm_entries", ctypes.c_int64), ("ardm_bytes", ctypes.c_int64), ("work_bytes", ctypes.c_int64),
+        ("n_out", ctypes.c_int64), ("n_steps", ctypes.c_int64), ("block", ctypes.c_int32),
+        ("setup_seconds", ctypes.c_double),
+    ]
+
+
 # Every symbol include/quapi.h declares (tests check the library exports all of them).
 EXPORTS = ("qp_plan_create", "qp_plan_query", "qp_plan_eta", "qp_plan_propagator", "qp_init", "qp_steps",
            "qp_read_rho", "qp_run", "qp_last_error", "qp_plan_destroy", "qp_version",
            "qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_extract", "qp_shard_steps",
-           "qp_shard_pack", "qp_shard_unpack")
+           "qp_shard_pack", "qp_shard_unpack", "qp_batch_create", "qp_batch_query", "qp_batch_run",
+           "qp_batch_destroy")
 
 _lib = None
 
@@ -115,6 +132,13 @@ def lib() -> ctypes.CDLL:
         L.qp_shard_unpack.argtypes = [vp, vp, vp, vp]
         for f in ("qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_extract", "qp_shard_steps",
                   "qp_shard_pack", "qp_shard_unpack"):
+            getattr(L, f).restype = ctypes.c_int
+        L.qp_batch_create.argtypes = [ctypes.POINTER(qp_batch), PP]
+        L.qp_batch_query.argtypes = [vp, ctypes.POINTER(qp_batch_sizes)]
+        L.qp_batch_run.argtypes = [vp, vp, vp, vp, ctypes.POINTER(qp_c64)]
+        L.qp_batch_destroy.argtypes = [vp]
+        L.qp_batch_destroy.restype = None
+        for f in ("qp_batch_create", "qp_batch_query", "qp_batch_run"):
             getattr(L, f).restype = ctypes.c_int
         L.qp_last_error.restype = ctypes.c_char_p
         L.qp_version.restype = ctypes.c_char_p
@@ -167,6 +191,36 @@ class Sizes:
     fuse_steps: int
 
 
+def _problem(w: W.Workload, keep: list, out_steps=None, J=None, J_cutoff: float = 0.0, G_in=None,
+             max_bytes: int = 0) -> qp_problem:
+    """Marshal a Workload into a ``qp_problem`` (host arrays kept alive in ``keep``)."""
+    s = np.ascontiguousarray(w.s, dtype=np.float64)
+    H, rho0 = _c64_array(w.H), _c64_array(w.rho0)
+    keep += [s, H, rho0]
+    pr = qp_problem()
+    pr.M = w.M
+    pr.s = s.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    pr.H, pr.rho0 = H, rho0
+    pr.kind = int(w.kind)
+    pr.coupling, pr.omega_c, pr.kT = float(w.coupling), float(w.omega_c), float(w.kT)
+    if J is not None:
+        cb = _JFUNC(lambda x, _u: float(J(x)))
+        keep.append(cb)
+        pr.kind, pr.J, pr.J_cutoff = QP_J_CALLBACK, cb, float(J_cutoff)
+    if G_in is not None:
+        g = _c64_array(G_in)
+        keep.append(g)
+        pr.kind, pr.G_in = QP_J_G_TABLE, g
+    pr.dt, pr.n_steps, pr.dkmax = float(w.dt), int(w.n_steps), int(w.L)
+    if out_steps is not None:
+        o = np.ascontiguousarray(np.asarray(out_steps, dtype=np.int64))
+        keep.append(o)
+        pr.out_steps = o.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        pr.n_out = len(o)
+    pr.max_bytes = int(max_bytes)
+    return pr
+
+
 class Plan:
     """An opaque ``qp_plan`` (host setup done at construction: validation, U, eta, tables)."""
 
@@ -176,30 +230,7 @@ class Plan:
         L = lib()
         self.w = w
         self._keep = []
-        s = np.ascontiguousarray(w.s, dtype=np.float64)
-        H, rho0 = _c64_array(w.H), _c64_array(w.rho0)
-        self._keep += [s, H, rho0]
-        pr = qp_problem()
-        pr.M = w.M
-        pr.s = s.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        pr.H, pr.rho0 = H, rho0
-        pr.kind = int(w.kind)
-        pr.coupling, pr.omega_c, pr.kT = float(w.coupling), float(w.omega_c), float(w.kT)
-        if J is not None:
-            cb = _JFUNC(lambda x, _u: float(J(x)))
-            self._keep.append(cb)
-            pr.kind, pr.J, pr.J_cutoff = QP_J_CALLBACK, cb, float(J_cutoff)
-        if G_in is not None:
-            g = _c64_array(G_in)
-            self._keep.append(g)
-            pr.kind, pr.G_in = QP_J_G_TABLE, g
-        pr.dt, pr.n_steps, pr.dkmax = float(w.dt), int(w.n_steps), int(w.L)
-        if out_steps is not None:
-            o = np.ascontiguousarray(np.asarray(out_steps, dtype=np.int64))
-            self._keep.append(o)
-            pr.out_steps = o.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
-            pr.n_out = len(o)
-        pr.max_bytes = int(max_bytes)
+        pr = _problem(w, self._keep, out_steps, J, J_cutoff, G_in, max_bytes)
         h = ctypes.c_void_p()
         _check(L.qp_plan_create(ctypes.byref(pr), ctypes.byref(h)))
         self._h = h
@@ -309,6 +340,69 @@ class Plan:
     def shard_unpack(self, recv, local, stream=None):
         _check(lib().qp_shard_unpack(self._h, ctypes.c_void_p(recv.data_ptr()), ctypes.c_void_p(local.data_ptr()),
                                      ctypes.c_void_p(self._stream_ptr(stream))))
+
+
+class BatchPlan:
+    """An opaque ``qp_batch_plan``: B problems sharing ``w``'s bath, grid and memory length, problem b
+    driven by H0 + f[b, k-1] H1 on step k (H0 = w.H) and started from rho0s[b] (default w.rho0)."""
+
+    def __init__(self, w: W.Workload, B: int, H1: Optional[np.ndarray] = None, f: Optional[np.ndarray] = None,
+                 rho0s: Optional[np.ndarray] = None, out_steps: Optional[Sequence[int]] = None, max_bytes: int = 0,
+                 G_in: Optional[np.ndarray] = None):
+        L = lib()
+        self.w, self.B = w, int(B)
+        self._keep = []
+        bt = qp_batch()
+        bt.base = _problem(w, self._keep, out_steps, G_in=G_in, max_bytes=max_bytes)
+        bt.B = self.B
+        if H1 is not None:
+            h1 = _c64_array(H1)
+            self._keep.append(h1)
+            bt.H1 = h1
+        if f is not None:
+            fa = np.ascontiguousarray(np.asarray(f, dtype=np.float64))
+            if fa.shape != (self.B, w.n_steps):
+                raise ValueError(f"f must have shape (B, n_steps) = {(self.B, w.n_steps)}")
+            self._keep.append(fa)
+            bt.f = fa.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        if rho0s is not None:
+            r = np.asarray(rho0s, dtype=np.complex128)
+            if r.shape != (self.B, w.M, w.M):
+                raise ValueError(f"rho0s must have shape (B, M, M) = {(self.B, w.M, w.M)}")
+            ra = _c64_array(r)
+            self._keep.append(ra)
+            bt.rho0 = ra
+        h = ctypes.c_void_p()
+        _check(L.qp_batch_create(ctypes.byref(bt), ctypes.byref(h)))
+        self._h = h
+        self.out_steps = (np.arange(w.n_steps + 1) if out_steps is None else np.asarray(out_steps, dtype=np.int64))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.qp_batch_destroy(h)
+            self._h = None
+
+    @property
+    def sizes(self) -> "qp_batch_sizes":
+        o = qp_batch_sizes()
+        _check(lib().qp_batch_query(self._h, ctypes.byref(o)))
+        return o
+
+    def alloc(self, device="cuda"):
+        import torch
+        sz = self.sizes
+        ardm = torch.empty(sz.ardm_entries * 2, dtype=torch.float64, device=device)
+        work = torch.empty((sz.work_bytes + 7) // 8, dtype=torch.float64, device=device)
+        return ardm, work
+
+    def run(self, ardm, work, stream=None, read: bool = True):
+        """Enqueue the batched run; with ``read`` synchronise and return rho [B, n_out, M, M]."""
+        n = len(self.out_steps)
+        buf = (qp_c64 * max(1, self.B * n * self.w.N))() if read else None
+        _check(lib().qp_batch_run(self._h, ctypes.c_void_p(ardm.data_ptr()), ctypes.c_void_p(work.data_ptr()),
+                                  ctypes.c_void_p(Plan._stream_ptr(stream)), buf))
+        return _to_numpy(buf, (self.B, n, self.w.M, self.w.M)) if read else None
 
 
 def solve(w: W.Workload, out_steps: Optional[Sequence[int]] = None, device: str = "cuda", **kw) -> np.ndarray:
