@@ -484,16 +484,33 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
                                   16ull * ipow(P.N, p0 + 2)};
         const cuuint32_t bx[5] = {(cuuint32_t)(2 * boxA), (cuuint32_t)(F / boxA), 4, 4, 4};
         std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
-    } else {  // view B: (slots 0..L-3 = d2 + 4 f as doubles, d0, d1, unit dims); stage [d1][d0][f][d2]
-        if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F || 8 * F > 256) return false;
-        const cuuint64_t gd[5] = {2ull * ipow(P.N, L - 2), 4, 4, 1, 1};
-        const cuuint64_t gs[4] = {16ull * ipow(P.N, L - 2), 16ull * ipow(P.N, L - 1), 16ull * ipow(P.N, L), 16ull * ipow(P.N, L)};
-        const cuuint32_t bx[5] = {(cuuint32_t)(8 * F), 4, 4, 1, 1};
+    } else if (ls.tma_a == -3) {  // view D (p0 = 0): (d0 = slot 0 as doubles, f, d1, d2): 64-B rows, 64-B
+              // swizzle.  stage [d2][d1][f] rows of the 4 d0 entries, chunk XOR ((row >> 1) & 3)
+        if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F) return false;
+        const cuuint64_t gd[5] = {8, (cuuint64_t)ipow(P.N, L - 3), 4, 4, 1};
+        const cuuint64_t gs[4] = {16ull * 64, 16ull * 4, 16ull * 16, 16ull * ipow(P.N, L)};
+        const cuuint32_t bx[5] = {8, (cuuint32_t)F, 4, 4, 1};
+        std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
+    } else if (ls.tma_a == -2) {  // view C (p0 = L-1): slots 0..L-2 (= d1 + 4 d2 + 16 f) as 128-B rows
+              // (d1, d2 & 1), two rows per fibre, then d0 = slot L-1; 128-B swizzle.  stage [d0][2 f + d2/2][8]
+        if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F || 2 * F > 256) return false;
+        const cuuint64_t gd[5] = {16, (cuuint64_t)ipow(P.N, L - 1) / 8, 4, 1, 1};
+        const cuuint64_t gs[4] = {128, 16ull * ipow(P.N, L - 1), 16ull * ipow(P.N, L), 16ull * ipow(P.N, L)};
+        const cuuint32_t bx[5] = {16, (cuuint32_t)(2 * F), 4, 1, 1};
+        std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
+    } else {  // view B: slots 0..L-3 (= d2 + 4 f) as 128-B rows of two fibres, d0, d1; 128-B swizzle.
+              // stage [d1][d0][f/2] rows of 8 entries (f & 1, d2), 16-B chunk XOR (row & 7)
+        if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F || F % 2) return false;
+        const cuuint64_t gd[5] = {16, (cuuint64_t)ipow(P.N, L - 2) / 8, 4, 4, 1};
+        const cuuint64_t gs[4] = {128, 16ull * ipow(P.N, L - 2), 16ull * ipow(P.N, L - 1), 16ull * ipow(P.N, L)};
+        const cuuint32_t bx[5] = {16, (cuuint32_t)(F / 2), 4, 4, 1};
         std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
     }
     const cuuint32_t es[5] = {1, 1, 1, 1, 1};
     if (enc(&ls.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)A, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            ls.tma_a > 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : (ls.tma_a == -3 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     ls.tma_A = A;
     return true;
@@ -607,16 +624,17 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     if (const char *e = std::getenv("QUAPI_F3MAP")) a.lane_map = (e[0] == '1' && T >= 64) ? 1 : 0;
     // TMA staging (k_fused3, unsharded, lane map 1 with slot 0 the lowest outer slot): the outer
     // slots are two runs of consecutive slots, A = 0 .. p0-1 and B = p0+3 .. L-1
-    ls.tma_a = -1;
+    ls.tma_a = -1;  // (-1: no TMA view; 0: view B; -2: view C; -3: view D)
     if (P.kind == 4 && M == 2 && S == 3 && removed.empty() && T >= 64 && !std::getenv("QUAPI_NO_TMA")) {
         if (a.lane_map == 1 && p0 >= 1 && p0 + S <= L) ls.tma_a = p0, ls.tma_b = L - p0 - S;
-        // view B (p0 = L-2) is implemented but off: measured 2.49 ms vs 2.43 ms with plain 32-B loads
-        else if (p0 == L - 2 && L >= 6 && std::getenv("QUAPI_TMA_VIEWB")) ls.tma_a = 0, ls.tma_b = 0;
+        else if (p0 == L - 2 && L >= 6 && !std::getenv("QUAPI_NO_VIEWB")) ls.tma_a = 0, ls.tma_b = 0;
+        else if (p0 == L - 1 && L >= 6 && !std::getenv("QUAPI_NO_VIEWC")) ls.tma_a = -2, ls.tma_b = 0;
+        else if (p0 == 0 && L >= 6 && !std::getenv("QUAPI_NO_VIEWD")) ls.tma_a = -3, ls.tma_b = 0;
     }
     // TMA-staged sets read the stage with lane map 0 by default (quarters of a super-fibre in one warp:
     // the digit transpose needs no CTA barrier); QUAPI_F3TMAP=1 selects map 1.  If the tensor map
     // cannot be encoded the launch falls back to plain loads with this lane map.
-    if (ls.tma_a >= 0) {
+    if (ls.tma_a != -1) {
         const char *e = std::getenv("QUAPI_F3TMAP");
         a.lane_map = (e && e[0] == '1') ? 1 : 0;
     }
@@ -628,7 +646,7 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     a.use_tma = 0;
     // Off by default: measured slower than plain 32-B loads on cfg3 (p0 = 0 / 12 / 13: 3.13 / 2.92 /
     // 2.95 ms vs 2.93 / 2.43 / 2.62 ms); QUAPI_CA=1 enables it.
-    if (P.kind == 4 && M == 2 && S == 3 && removed.empty() && T >= 64 && ls.tma_a < 0 && std::getenv("QUAPI_CA")) {
+    if (P.kind == 4 && M == 2 && S == 3 && removed.empty() && T >= 64 && ls.tma_a == -1 && std::getenv("QUAPI_CA")) {
         const int F = qp::fused3_round_fibres(4);
         const long long sfib = ipow(N, pos[outer[0]]);
         bool uniform = true;  // fibres 0..F-1 of a round at stride sfib
@@ -956,14 +974,17 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             a.A = A;
             a.small = small;
             a.use_tma = ls.stg_ca ? 2 : 0;
-            if (ls.tma_a >= 0 && P->kind == 4 && S == 3 &&
+            if (ls.tma_a != -1 && P->kind == 4 && S == 3 &&
                 encode_f3_tmap(*P, ls, A, qp::fused3_round_fibres((a.lane_map & 1) + 2))) {
                 a.use_tma = 1;
                 a.tmap = ls.tmap;
                 const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2);
                 // TMA box coordinates of round G: c0 = tma_c0m (G mod tma_nA), c1 = G / tma_nA
-                a.tma_nA = ls.tma_a > 0 ? ipow(P->N, ls.tma_a) : (1LL << 62);
-                a.tma_c0m = ls.tma_a > 0 ? 2 : 8;
+                // view B: c0 = 0, c1 = G / 2 (rows of two fibres); view C: c1 = 2 G (two rows per fibre)
+                a.tma_nA = ls.tma_a > 0 ? ipow(P->N, ls.tma_a) : (ls.tma_a == 0 ? 2 : 1);
+                a.tma_c0m = ls.tma_a > 0 ? 2 : 0;
+                a.tma_c1m = ls.tma_a == -2 ? 2 : 1;
+                a.tma_swz = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? 2 : 3));
                 if (ls.tma_a > 0) a.tma_sf = 1, a.tma_s[0] = F, a.tma_s[1] = 4 * F, a.tma_s[2] = 16 * F;
                 else a.tma_sf = 4, a.tma_s[0] = 4 * F, a.tma_s[1] = 16 * F, a.tma_s[2] = 1;
             }

@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
         const long long G = (long long)tau * a.T + (long long)rd * F;
         fence_proxy_async();
         mbar_expect_tx(&sFull, F * 64 * 16 + S * 2 * D * F * 16 + F * 8);
-        tma_load_5d(stage, &a.tmap, &sFull, (int)(a.tma_c0m * (G % a.tma_nA)), (int)(G / a.tma_nA));
+        tma_load_5d(stage, &a.tmap, &sFull, (int)(a.tma_c0m * (G % a.tma_nA)), (int)(a.tma_c1m * (G / a.tma_nA)));
         for (int q = 0; q < S * 2 * D; ++q) {  // q = (s, kap, d): Etab[s][kap][g = 0][d][t0 ..]
             const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
             bulk_g2s(sE0 + ((size_t)buf * S * 2 * D + q) * F,
@@ -1156,8 +1156,20 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
 #pragma unroll
                 for (int d1 = 0; d1 < N; ++d1)
 #pragma unroll
-                    for (int d0 = 0; d0 < N; ++d0)
-                        X[d1][d0] = stage[fib * a.tma_sf + d0 * a.tma_s[0] + d1 * a.tma_s[1] + j * a.tma_s[2]];
+                    for (int d0 = 0; d0 < N; ++d0) {
+                        if (a.tma_swz == 1) {  // view B: row r of 8 entries (fibre parity, d2); chunk XOR (r & 7)
+                            const int r = (d1 * N + d0) * (F / 2) + (fib >> 1);
+                            X[d1][d0] = stage[r * 8 + ((((fib & 1) << 2) | j) ^ (r & 7))];
+                        } else if (a.tma_swz == 3) {  // view D: 64-B row r = (d2, d1, f) of the d0 entries
+                            const int r = (j * N + d1) * F + fib;
+                            X[d1][d0] = stage[r * 4 + (d0 ^ ((r >> 1) & 3))];
+                        } else if (a.tma_swz == 2) {  // view C: row r of 8 entries (d2 parity, d1)
+                            const int r = d0 * 2 * F + 2 * fib + (j >> 1);
+                            X[d1][d0] = stage[r * 8 + ((((j & 1) << 2) | d1) ^ (r & 7))];
+                        } else {
+                            X[d1][d0] = stage[fib * a.tma_sf + d0 * a.tma_s[0] + d1 * a.tma_s[1] + j * a.tma_s[2]];
+                        }
+                    }
                 __syncthreads();  // stage free: refill it with the next unit
                 const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
                 if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
@@ -1339,7 +1351,8 @@ __global__ void __launch_bounds__(BLOCK, 2) k_fused3s(const __grid_constant__ Fu
         const long long G = (long long)tau * a.T + (long long)rd * F;
         fence_proxy_async();
         mbar_expect_tx(&sFull[b], F * 64 * 16 + S * 2 * D * F * 16 + F * 8);
-        tma_load_5d(stage0 + b * 64 * F, &a.tmap, &sFull[b], (int)(a.tma_c0m * (G % a.tma_nA)), (int)(G / a.tma_nA));
+        tma_load_5d(stage0 + b * 64 * F, &a.tmap, &sFull[b], (int)(a.tma_c0m * (G % a.tma_nA)),
+                    (int)(a.tma_c1m * (G / a.tma_nA)));
         for (int q = 0; q < S * 2 * D; ++q) {
             const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
             bulk_g2s(sE0 + ((size_t)b * S * 2 * D + q) * F, a.Etab + ((((size_t)st * 2 + kap) * a.G) * D + d) * a.X + rd * F,

@@ -18,7 +18,7 @@ for kind in ("reg", "warp", "async", "split"):
         r = pl.run(a, wk)
         assert np.isfinite(r).all()
 os.environ["QUAPI_FUSED_KIND"] = "3"
-for env in ({}, {"QUAPI_NO_TMA": "1"}, {"QUAPI_F3TMAP": "1"}, {"QUAPI_TMA_VIEWB": "1"}, {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "1"}, {"QUAPI_CA": "1"}):
+for env in ({}, {"QUAPI_NO_TMA": "1"}, {"QUAPI_F3TMAP": "1"}, {"QUAPI_NO_VIEWB": "1", "QUAPI_NO_VIEWC": "1", "QUAPI_NO_VIEWD": "1"}, {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "1"}, {"QUAPI_CA": "1"}):
     os.environ.update(env)
     w = W.random_problem(7, 2, 8, 20)  # L = 8: TMA-staged, plain-load and 32-B-load ring slots all occur
     pl = Q.Plan(w)
