@@ -58,9 +58,11 @@ typedef enum {
     QP_J_DEBYE = 2,            /* J = (pi/2) xi w wc^2/(w^2+wc^2)            (reading C.3-9)   */
     QP_J_SUPEROHMIC_GAUSS = 3, /* J = A w^3 exp(-(w/wc)^2)   Eq. 21, P:291   (reading C.3-5)   */
     QP_J_CALLBACK = 4,         /* J(w) from a caller function, integrated on (0, J_cutoff]     */
-    QP_J_G_TABLE = 5           /* bath given directly as G(m dt/2), m = 0..2L+2, where
+    QP_J_G_TABLE = 5,          /* bath given directly as G(m dt/2), m = 0..2L+2, where
                                   G(tau) = int_0^tau int_0^t' alpha(t'-t'') dt'' dt'  -- the
                                   paper's "or the bath response function alpha(t)"     */
+    QP_J_ETA_TABLE = 6         /* bath given as its 3L+2 eta classes (qp_plan_eta order) in eta_in,
+                                  e.g. computed on the device by qp_eta_device                  */
 } qp_bath_kind;
 
 typedef struct {
@@ -82,6 +84,7 @@ typedef struct {
     const int64_t *out_steps;/* sorted unique step indices in [0, n_steps]; NULL => all         */
     int64_t n_out;           /* length of out_steps (ignored when out_steps == NULL)            */
     int64_t max_bytes;       /* capacity budget for ARDM + workspace; 0 => no budget check      */
+    const qp_c64 *eta_in;    /* QP_J_ETA_TABLE only: [3*dkmax+2] eta classes, qp_plan_eta order   */
 } qp_problem;
 
 typedef struct qp_plan qp_plan;
@@ -166,6 +169,28 @@ qp_status qp_shard_steps(qp_plan *plan, int64_t k_begin, int64_t k_end, void *d_
 /* Re-shard from segment j to j+1: pack local -> send (rank-major), unpack recv -> local (advances j). */
 qp_status qp_shard_pack(qp_plan *plan, const void *d_local, void *d_send, void *stream);
 qp_status qp_shard_unpack(qp_plan *plan, const void *d_recv, void *d_local, void *stream);
+
+/* ---------------------------------------------------------------- device eta setup
+   Host-setup step a3 on the GPU: every eta class of Eqs. 10-16 (Strang windows, DESIGN.md
+   reading C.3-1) for B baths at once -- the setup the paper names as the bottleneck once propagation
+   runs on the GPU, and the per-problem tables of temperature / coupling sweeps.
+   Each class is the omega-integral of its window kernel on a fixed composite Gauss-Kronrod 21 rule
+   (panels short against the integrand's nearest complex singularity; Debye: closed-form tail), one
+   8-CTA cluster per (bath, class), deterministic (fixed-order reductions, no atomics). */
+typedef struct {
+    int32_t kind;            /* QP_J_ZERO, QP_J_OHMIC_EXP, QP_J_DEBYE or QP_J_SUPEROHMIC_GAUSS          */
+    double coupling;         /* xi (Ohmic, Debye) or A (super-Ohmic Gaussian), as in qp_problem         */
+    double omega_c;          /* > 0                                                                      */
+    double kT;               /* >= 0                                                                     */
+} qp_bath;
+/* Enqueue on `stream`: d_eta[b][c] (device, caller-owned, B*(3*dkmax+2) qp_c64) = eta class c of bath b
+   in the qp_plan_eta order [self_interior, self_end, eta_1..L, E_1..L, TI_1..L] for time step dt and
+   L = dkmax; d_err (device, B*(3*dkmax+2) doubles, may be NULL) = the summed |K21 - G10| panel
+   estimate (a loose upper bound on the quadrature error).  baths: host [B], read before return.
+   Errors: QP_ERR_ARG (NULL, B < 1, dt <= 0, L out of range), QP_ERR_CONFIG (kind not one of the four
+   analytic families, omega_c <= 0, kT < 0, non-finite coupling), QP_ERR_CUDA (launch). */
+qp_status qp_eta_device(const qp_bath *baths, int32_t B, double dt, int32_t dkmax, qp_c64 *d_eta, double *d_err,
+                        void *stream);
 
 const char *qp_last_error(void);
 void qp_plan_destroy(qp_plan *plan);

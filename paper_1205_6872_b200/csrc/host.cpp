@@ -408,6 +408,17 @@ qp_status compute_eta(qp_plan &P, const qp_problem &pr) {
     P.eta.assign(L + 1, 0.0);
     P.E.assign(L + 1, 0.0);
     P.TI.assign(L + 1, 0.0);
+    if (pr.kind == QP_J_ETA_TABLE) {  // eta classes given (e.g. by qp_eta_device), qp_plan_eta order
+        auto e = [&](int i) { return cd(pr.eta_in[i].re, pr.eta_in[i].im); };
+        P.self_int = e(0);
+        P.self_end = e(1);
+        for (int j = 1; j <= L; ++j) {
+            P.eta[j] = e(1 + j);
+            P.E[j] = e(1 + L + j);
+            P.TI[j] = e(1 + 2 * L + j);
+        }
+        return QP_OK;
+    }
     if (pr.kind == QP_J_G_TABLE) {  // alpha given as G(m dt/2): four-corner rule, G'' = alpha
         auto G = [&](int m) { return cd(pr.G_in[m].re, pr.G_in[m].im); };  // m = 2 x
         P.self_int = G(2);
@@ -783,6 +794,12 @@ qp_status validate(const qp_problem *pr) {
     case QP_J_G_TABLE:
         if (!pr->G_in) return err(QP_ERR_CONFIG, "config: G_TABLE bath needs G_in[2*dkmax+3]");
         break;
+    case QP_J_ETA_TABLE:
+        if (!pr->eta_in) return err(QP_ERR_CONFIG, "config: ETA_TABLE bath needs eta_in[3*dkmax+2]");
+        for (int i = 0; i < 3 * pr->dkmax + 2; ++i)
+            if (!std::isfinite(pr->eta_in[i].re) || !std::isfinite(pr->eta_in[i].im))
+                return err(QP_ERR_CONFIG, "config: eta_in[%d] not finite", i);
+        break;
     default: return err(QP_ERR_CONFIG, "config: unknown bath kind %d", pr->kind);
     }
     if (pr->out_steps) {
@@ -879,6 +896,38 @@ qp_status qp_plan_eta(const qp_plan *P, qp_c64 *out, int64_t cap) {
         put(1 + j, P->eta[j]);
         put(1 + P->L + j, P->E[j]);
         put(1 + 2 * P->L + j, P->TI[j]);
+    }
+    return QP_OK;
+}
+
+qp_status qp_eta_device(const qp_bath *baths, int32_t B, double dt, int32_t L, qp_c64 *d_eta, double *d_err,
+                        void *stream) {
+    if (!baths || !d_eta) return err(QP_ERR_ARG, "arg: NULL baths or d_eta");
+    if (B < 1) return err(QP_ERR_ARG, "arg: B must be >= 1 (got %d)", B);
+    if (!(dt > 0.0) || !std::isfinite(dt)) return err(QP_ERR_ARG, "arg: dt must be finite and > 0");
+    if (L < 1 || L > qp::kMaxL) return err(QP_ERR_ARG, "arg: dkmax must be in [1, %d] (got %d)", qp::kMaxL, L);
+    for (int b = 0; b < B; ++b) {
+        const qp_bath &q = baths[b];
+        if (q.kind < QP_J_ZERO || q.kind > QP_J_SUPEROHMIC_GAUSS)
+            return err(QP_ERR_CONFIG, "config: bath %d: kind %d has no device quadrature (analytic families 0..3 only)", b, q.kind);
+        if (q.kind != QP_J_ZERO) {
+            if (!(q.omega_c > 0.0) || !std::isfinite(q.omega_c)) return err(QP_ERR_CONFIG, "config: bath %d: omega_c must be > 0", b);
+            if (!(q.kT >= 0.0) || !std::isfinite(q.kT)) return err(QP_ERR_CONFIG, "config: bath %d: kT must be >= 0", b);
+            if (!std::isfinite(q.coupling)) return err(QP_ERR_CONFIG, "config: bath %d: coupling not finite", b);
+        }
+    }
+    const cudaStream_t s = (cudaStream_t)stream;
+    const size_t nc = 3 * (size_t)L + 2;
+    static thread_local qp::EtaBatch batch;  // 16 KB kernel parameter block
+    for (int b0 = 0; b0 < B; b0 += qp::kEtaBatchMax) {
+        const int nb = std::min(B - b0, qp::kEtaBatchMax);
+        for (int i = 0; i < nb; ++i) {
+            const qp_bath &q = baths[b0 + i];
+            batch.b[i] = qp::EtaBath{q.kind, q.coupling, q.omega_c, q.kT};
+        }
+        const cudaError_t e = qp::launch_eta(batch, nb, L, dt, reinterpret_cast<double2 *>(d_eta) + (size_t)b0 * nc,
+                                             d_err ? d_err + (size_t)b0 * nc : nullptr, s);
+        if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: eta launch: %s", cudaGetErrorString(e));
     }
     return QP_OK;
 }

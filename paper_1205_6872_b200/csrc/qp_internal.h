@@ -148,6 +148,16 @@ struct BatchArgs {
     double delta[kMaxD];     // Delta s of class d + 1
 };
 size_t batch_dyn_smem(int M, int L);
+// Device eta setup (eta.cu): kind as qp_bath_kind (0..3), xi = coupling.
+struct EtaBath {
+    int kind;
+    double xi, wc, kT;
+};
+constexpr int kEtaBatchMax = 512;  // baths per launch (passed by value as a __grid_constant__ parameter)
+struct EtaBatch {
+    EtaBath b[kEtaBatchMax];
+};
+cudaError_t launch_eta(const EtaBatch &baths, int B, int L, double dt, double2 *d_eta, double *d_err, cudaStream_t s);
 cudaError_t launch_batch(int M, const BatchArgs &a, int B, cudaStream_t s);
 constexpr int kBatchBlock = 256;
 

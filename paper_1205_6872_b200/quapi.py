@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "lib", "libquapi.so")
 
 QP_OK, QP_ERR_ARG, QP_ERR_CONFIG, QP_ERR_CAPACITY, QP_ERR_QUADRATURE, QP_ERR_CUDA, QP_ERR_COMM = 0, 1, 2, 3, 4, 6, 7
-QP_J_CALLBACK, QP_J_G_TABLE = 4, 5
+QP_J_CALLBACK, QP_J_G_TABLE, QP_J_ETA_TABLE = 4, 5, 6
 
 _JFUNC = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
 
@@ -50,7 +50,13 @@ class qp_problem(ctypes.Structure):
         ("out_steps", ctypes.POINTER(ctypes.c_int64)),
         ("n_out", ctypes.c_int64),
         ("max_bytes", ctypes.c_int64),
+        ("eta_in", ctypes.POINTER(qp_c64)),
     ]
+
+
+class qp_bath(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("coupling", ctypes.c_double), ("omega_c", ctypes.c_double),
+                ("kT", ctypes.c_double)]
 
 
 class qp_sizes(ctypes.Structure):
@@ -93,7 +99,7 @@ EXPORTS = ("qp_plan_create", "qp_plan_query", "qp_plan_eta", "qp_plan_propagator
            "qp_read_rho", "qp_run", "qp_last_error", "qp_plan_destroy", "qp_version",
            "qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_extract", "qp_shard_steps",
            "qp_shard_pack", "qp_shard_unpack", "qp_batch_create", "qp_batch_query", "qp_batch_run",
-           "qp_batch_destroy")
+           "qp_batch_destroy", "qp_eta_device")
 
 _lib = None
 
@@ -140,6 +146,9 @@ def lib() -> ctypes.CDLL:
         L.qp_batch_destroy.restype = None
         for f in ("qp_batch_create", "qp_batch_query", "qp_batch_run"):
             getattr(L, f).restype = ctypes.c_int
+        L.qp_eta_device.argtypes = [ctypes.POINTER(qp_bath), ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
+                                    vp, vp, vp]
+        L.qp_eta_device.restype = ctypes.c_int
         L.qp_last_error.restype = ctypes.c_char_p
         L.qp_version.restype = ctypes.c_char_p
         L.qp_plan_destroy.argtypes = [ctypes.c_void_p]
@@ -192,7 +201,7 @@ class Sizes:
 
 
 def _problem(w: W.Workload, keep: list, out_steps=None, J=None, J_cutoff: float = 0.0, G_in=None,
-             max_bytes: int = 0) -> qp_problem:
+             max_bytes: int = 0, eta_in=None) -> qp_problem:
     """Marshal a Workload into a ``qp_problem`` (host arrays kept alive in ``keep``)."""
     s = np.ascontiguousarray(w.s, dtype=np.float64)
     H, rho0 = _c64_array(w.H), _c64_array(w.rho0)
@@ -211,6 +220,12 @@ def _problem(w: W.Workload, keep: list, out_steps=None, J=None, J_cutoff: float 
         g = _c64_array(G_in)
         keep.append(g)
         pr.kind, pr.G_in = QP_J_G_TABLE, g
+    if eta_in is not None:
+        e = _c64_array(eta_in)
+        if len(e) != 3 * w.L + 2:
+            raise ValueError(f"eta_in needs 3L+2 = {3 * w.L + 2} classes")
+        keep.append(e)
+        pr.kind, pr.eta_in = QP_J_ETA_TABLE, e
     pr.dt, pr.n_steps, pr.dkmax = float(w.dt), int(w.n_steps), int(w.L)
     if out_steps is not None:
         o = np.ascontiguousarray(np.asarray(out_steps, dtype=np.int64))
@@ -226,11 +241,18 @@ class Plan:
 
     def __init__(self, w: W.Workload, out_steps: Optional[Sequence[int]] = None,
                  J: Optional[Callable[[float], float]] = None, J_cutoff: float = 0.0,
-                 G_in: Optional[np.ndarray] = None, max_bytes: int = 0):
+                 G_in: Optional[np.ndarray] = None, max_bytes: int = 0, eta_in: Optional[np.ndarray] = None,
+                 eta_setup: str = "host"):
+        """``eta_setup="device"``: the eta classes (host-setup step a3) come from ``eta_device`` on the
+        current CUDA device instead of the host quadrature (analytic bath families only)."""
         L = lib()
         self.w = w
         self._keep = []
-        pr = _problem(w, self._keep, out_steps, J, J_cutoff, G_in, max_bytes)
+        if eta_setup == "device" and eta_in is None and J is None and G_in is None:
+            eta_in = eta_device([bath_of(w)], w.dt, w.L)[0]
+        elif eta_setup not in ("host", "device"):
+            raise ValueError(f"eta_setup must be 'host' or 'device', got {eta_setup!r}")
+        pr = _problem(w, self._keep, out_steps, J, J_cutoff, G_in, max_bytes, eta_in)
         h = ctypes.c_void_p()
         _check(L.qp_plan_create(ctypes.byref(pr), ctypes.byref(h)))
         self._h = h
@@ -403,6 +425,38 @@ class BatchPlan:
         _check(lib().qp_batch_run(self._h, ctypes.c_void_p(ardm.data_ptr()), ctypes.c_void_p(work.data_ptr()),
                                   ctypes.c_void_p(Plan._stream_ptr(stream)), buf))
         return _to_numpy(buf, (self.B, n, self.w.M, self.w.M)) if read else None
+
+
+def bath_of(w: W.Workload) -> tuple:
+    """(kind, coupling, omega_c, kT) of a workload's analytic bath."""
+    return (int(w.kind), float(w.coupling), float(w.omega_c), float(w.kT))
+
+
+def eta_device(baths: Sequence[tuple], dt: float, L: int, stream=None, out=None, err: bool = False):
+    """Every eta class of each bath (kind, coupling, omega_c, kT) on the current CUDA device
+    (``qp_eta_device``).  Returns complex [B, 3L+2] on the host in the ``Plan.eta()``
+    order [self_interior, self_end, eta_1..L, E_1..L, TI_1..L] (and the [B, 3L+2] panel error
+    estimates when ``err``).  ``out``: a preallocated device float64 tensor of 2*B*(3L+2) entries
+    (then nothing is synchronised or copied back and ``out`` is returned)."""
+    import torch
+    B = len(baths)
+    arr = (qp_bath * B)()
+    for i, b in enumerate(baths):
+        arr[i].kind, arr[i].coupling, arr[i].omega_c, arr[i].kT = int(b[0]), float(b[1]), float(b[2]), float(b[3])
+    nc = 3 * int(L) + 2
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d = out if out is not None else torch.empty(2 * B * nc, dtype=torch.float64, device=dev)
+    de = torch.empty(B * nc, dtype=torch.float64, device=d.device) if err else None
+    _check(lib().qp_eta_device(arr, B, float(dt), int(L), ctypes.c_void_p(d.data_ptr()),
+                               ctypes.c_void_p(de.data_ptr() if de is not None else 0),
+                               ctypes.c_void_p(Plan._stream_ptr(stream))))
+    if out is not None:
+        return out
+    if stream is not None:
+        stream.synchronize()
+    v = d.view(B, nc, 2).cpu().numpy()
+    eta = v[..., 0] + 1j * v[..., 1]
+    return (eta, de.view(B, nc).cpu().numpy()) if err else eta
 
 
 def solve(w: W.Workload, out_steps: Optional[Sequence[int]] = None, device: str = "cuda", **kw) -> np.ndarray:

@@ -120,3 +120,49 @@ def test_gpu_entry_points_fail_loudly_without_device():
     buf = (ctypes.c_double * 4096)()
     st = Q.lib().qp_init(pl._h, ctypes.cast(buf, ctypes.c_void_p), ctypes.cast(buf, ctypes.c_void_p), None)
     assert st != Q.QP_OK
+
+
+def _eta_dev(baths, B=None, dt=0.25, L=4, ptr=1 << 20):
+    arr = (Q.qp_bath * max(1, len(baths)))()
+    for i, b in enumerate(baths):
+        arr[i].kind, arr[i].coupling, arr[i].omega_c, arr[i].kT = b
+    return Q.lib().qp_eta_device(arr, len(baths) if B is None else B, dt, L, ctypes.c_void_p(ptr), None, None)
+
+
+def test_eta_device_validation():
+    """qp_eta_device validates on the host before any launch and names the bath."""
+    ok = (1, 0.1, 7.5, 0.2)
+    assert _eta_dev([ok], B=0) == Q.QP_ERR_ARG
+    assert _eta_dev([ok], dt=0.0) == Q.QP_ERR_ARG
+    assert _eta_dev([ok], L=0) == Q.QP_ERR_ARG
+    assert Q.lib().qp_eta_device(None, 1, 0.25, 4, ctypes.c_void_p(1), None, None) == Q.QP_ERR_ARG
+    assert _eta_dev([ok], ptr=0) == Q.QP_ERR_ARG
+    assert _eta_dev([ok, (4, 0.1, 7.5, 0.2)]) == Q.QP_ERR_CONFIG
+    assert "bath 1" in Q.lib().qp_last_error().decode()
+    assert _eta_dev([(2, 0.1, 0.0, 0.2)]) == Q.QP_ERR_CONFIG
+    assert _eta_dev([(1, 0.1, 7.5, -1.0)]) == Q.QP_ERR_CONFIG
+    assert _eta_dev([(1, float("nan"), 7.5, 0.2)]) == Q.QP_ERR_CONFIG
+
+
+def test_eta_device_fails_loudly_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    assert _eta_dev([(1, 0.1, 7.5, 0.2)]) == Q.QP_ERR_CUDA
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_eta_table_input_reproduces_plan(cfg):
+    """kind = ETA_TABLE: a plan built from another plan's eta classes carries exactly those classes."""
+    w = W.CONFIGS[cfg].with_(L=min(W.CONFIGS[cfg].L, 6))
+    e = Q.Plan(w, out_steps=[0]).eta()
+    flat = np.concatenate([[e["self_interior"], e["self_end"]], e["eta"], e["E"], e["TI"]])
+    e2 = Q.Plan(w, out_steps=[0], eta_in=flat).eta()
+    for k in e:
+        assert np.array_equal(np.asarray(e[k]), np.asarray(e2[k])), k
+    with pytest.raises(ValueError):
+        Q.Plan(w, eta_in=flat[:-1])
+    bad = flat.copy()
+    bad[3] = np.nan
+    with pytest.raises(Q.QuapiError, match="eta_in"):
+        Q.Plan(w, eta_in=bad)
