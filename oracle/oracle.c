@@ -208,7 +208,9 @@ int or_G(const or_problem *p, double tau, double *re, double *im) {
     switch (p->kind) {
     case OR_J_OHMIC_EXP: Om = 60.0 * wc; break;      /* e^-60 ~ 1e-26 tail */
     case OR_J_SUPEROHMIC_GAUSS: Om = 12.0 * wc; break; /* e^-144 tail */
-    default: Om = fmax(200.0 * wc, 80.0 * p->kT); break; /* Debye: analytic tail added below */
+    default: /* Debye: analytic tail added below.  Its asymptotic series in 1/(Omega tau) needs
+                Omega tau >= 400 to reach rounding level (at Omega tau ~ 13 it stalls near 1e-8) */
+        Om = fmax(fmax(200.0 * wc, 80.0 * p->kT), 400.0 / tau); break;
     }
     /* panels no wider than a quarter oscillation period and wc/4 */
     double hpan = fmin(0.25 * wc, 0.5 * M_PI / tau);

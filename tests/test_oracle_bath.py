@@ -38,9 +38,11 @@ def test_G_ohmic_closed_form(tau, kT):
     assert close(g, ex, 3e-15), (g, ex, abs(g - ex))
 
 
-@pytest.mark.parametrize("tau", TAUS)
-@pytest.mark.parametrize("kT,wc", [(0.2, 7.5), (1.0, 3.0)])
+@pytest.mark.parametrize("tau", TAUS + [0.05])
+@pytest.mark.parametrize("kT,wc", [(0.2, 7.5), (1.0, 3.0), (2.0, 1.0)])
 def test_G_debye_matsubara(tau, kT, wc):
+    """(2.0, 1.0) at tau = 0.05: small wc tau, where the closed-form Debye tail beyond the quadrature
+    cutoff needs Omega tau large (the oracle picks Omega >= 400 / tau)."""
     g = O.G(prob(kind=O.J_DEBYE, kT=kT, omega_c=wc), tau)
     ex = CF.G_debye(0.1, wc, kT, tau)
     assert close(g, ex, 3e-15), (g, ex, abs(g - ex))
