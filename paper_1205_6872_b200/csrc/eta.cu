@@ -149,11 +149,25 @@ __device__ double2 debye_tail(const EtaBath &b, double tau, double Om) {
     return make_double2(0.5 * b.xi * (non.x - osc.x), 0.5 * b.xi * (non.y - osc.y));
 }
 
-__device__ double upper_limit(const EtaBath &b) {
+// the window pair's positive corner separations: the closed-form Debye tail is evaluated at each
+__device__ void corners(const Win &w, double (&t)[4]) {
+    t[0] = w.dc + 0.5 * (w.wa + w.wb), t[1] = w.dc - 0.5 * (w.wa + w.wb);
+    t[2] = w.dc - 0.5 * w.wa + 0.5 * w.wb, t[3] = w.dc + 0.5 * w.wa - 0.5 * w.wb;
+}
+
+__device__ double upper_limit(const EtaBath &b, const Win &w) {
     switch (b.kind) {
     case 1: return 64.0 * b.wc;                       // e^{-64}: below rounding
     case 3: return 13.0 * b.wc;                       // e^{-169}
-    case 2: return fmax(256.0 * b.wc, 80.0 * b.kT);   // + closed-form tail (coth = 1 beyond)
+    case 2: {  // + closed-form tail (coth = 1 beyond); its asymptotic series needs Om * tau >= 512
+        double tmin = w.self ? w.w0 : 1e300, t[4];
+        if (!w.self) {
+            corners(w, t);
+            for (int i = 0; i < 4; ++i)
+                if (t[i] > 0.0) tmin = fmin(tmin, t[i]);
+        }
+        return fmax(fmax(256.0 * b.wc, 80.0 * b.kT), 512.0 / tmin);
+    }
     default: return 0.0;
     }
 }
@@ -173,17 +187,24 @@ __global__ void __cluster_dims__(kEtaCluster, 1, 1) __launch_bounds__(kEtaBlock)
 
     double sr = 0.0, si = 0.0, se = 0.0;
     if (b.kind != 0) {
-        const double Om = upper_limit(b);
-        const double h0 = fmin(0.25 * b.wc, 0.5 * M_PI / win.span);
+        // three uniform-panel regions: [0, W1] near the coth poles (width h1), [W1, W2] (h0), and the
+        // far tail [W2, Om] beyond 64 wc where only the oscillation limits the width (h2)
+        const double Om = upper_limit(b, win);
+        const double hosc = 0.5 * M_PI / win.span;
+        const double h0 = fmin(0.25 * b.wc, hosc);
         const double W1 = b.kT > 0.0 ? fmin(Om, 16.0 * M_PI * b.kT) : 0.0;
         const double h1 = b.kT > 0.0 ? fmin(h0, M_PI * b.kT) : h0;
+        const double W2 = fmax(W1, fmin(Om, 64.0 * b.wc));
+        const double h2 = fmin(hosc, 8.0 * b.wc);
         const long n1 = W1 > 0.0 ? (long)ceil(W1 / h1) : 0;
-        const long n2 = (long)ceil((Om - W1) / h0);
-        const long np = n1 + n2;
+        const long n2 = W2 > W1 ? (long)ceil((W2 - W1) / h0) : 0;
+        const long n3 = Om > W2 ? (long)ceil((Om - W2) / h2) : 0;
+        const long np = n1 + n2 + n3;
         for (long i = (long)rank * kEtaBlock + threadIdx.x; i < np; i += (long)kEtaCluster * kEtaBlock) {
             double lo, hi;
             if (i < n1) { lo = W1 * double(i) / double(n1); hi = W1 * double(i + 1) / double(n1); }
-            else { const long q = i - n1; lo = W1 + (Om - W1) * double(q) / double(n2); hi = W1 + (Om - W1) * double(q + 1) / double(n2); }
+            else if (i < n1 + n2) { const long q = i - n1; lo = W1 + (W2 - W1) * double(q) / double(n2); hi = W1 + (W2 - W1) * double(q + 1) / double(n2); }
+            else { const long q = i - n1 - n2; lo = W2 + (Om - W2) * double(q) / double(n3); hi = W2 + (Om - W2) * double(q + 1) / double(n3); }
             const double m = 0.5 * (lo + hi), hw = 0.5 * (hi - lo);
             const double2 f0 = integrand(b, win, m);
             double kr = cWgk[10] * f0.x, ki = cWgk[10] * f0.y, gr = 0.0, gi = 0.0;
@@ -230,15 +251,15 @@ __global__ void __cluster_dims__(kEtaCluster, 1, 1) __launch_bounds__(kEtaBlock)
             tr += p[0], ti += p[1], te += p[2];
         }
         if (b.kind == 2) {  // Debye: closed-form tail beyond Om
-            const double Om = upper_limit(b);
+            const double Om = upper_limit(b, win);
             double2 t;
             if (win.self) {
                 t = debye_tail(b, win.w0, Om);
             } else {  // four corners of the window pair (later [a1,a2], earlier [b1,b2])
-                const double t1 = win.dc + 0.5 * (win.wa + win.wb), t2 = win.dc - 0.5 * (win.wa + win.wb);
-                const double t3 = win.dc - 0.5 * win.wa + 0.5 * win.wb, t4 = win.dc + 0.5 * win.wa - 0.5 * win.wb;
-                const double2 a1 = debye_tail(b, t1, Om), a2 = debye_tail(b, t2, Om);
-                const double2 a3 = debye_tail(b, t3, Om), a4 = debye_tail(b, t4, Om);
+                double c4[4];
+                corners(win, c4);
+                const double2 a1 = debye_tail(b, c4[0], Om), a2 = debye_tail(b, c4[1], Om);
+                const double2 a3 = debye_tail(b, c4[2], Om), a4 = debye_tail(b, c4[3], Om);
                 t = make_double2(a1.x + a2.x - a3.x - a4.x, a1.y + a2.y - a3.y - a4.y);
             }
             tr += t.x, ti += t.y;

@@ -272,7 +272,15 @@ qp_status eta_class(const Bath &b, const WinClass &c, cd *out, const char *name,
     switch (b.kind) {
     case QP_J_OHMIC_EXP: Om = 64.0 * b.wc; break;
     case QP_J_SUPEROHMIC_GAUSS: Om = 13.0 * b.wc; break;
-    case QP_J_DEBYE: Om = std::max(256.0 * b.wc, 80.0 * b.kT); break;
+    case QP_J_DEBYE: {  // the closed-form tail's asymptotic series needs Om * tau >= 512 at every corner tau
+        double tmin = c.self ? c.w0 : 1e300;
+        if (!c.self)
+            for (double t : {c.dc + 0.5 * (c.wa + c.wb), c.dc - 0.5 * (c.wa + c.wb), c.dc - 0.5 * c.wa + 0.5 * c.wb,
+                             c.dc + 0.5 * c.wa - 0.5 * c.wb})
+                if (t > 0.0) tmin = std::min(tmin, t);
+        Om = std::max({256.0 * b.wc, 80.0 * b.kT, 512.0 / tmin});
+        break;
+    }
     default: Om = b.cutoff; break;
     }
     const double span = c.self ? c.w0 : c.dc + 0.5 * (c.wa + c.wb);
