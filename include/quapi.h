@@ -212,6 +212,10 @@ typedef struct {
     const qp_c64 *H1;        /* [M*M] Hermitian drive operator, or NULL (no drive)                       */
     const double *f;         /* [B][n_steps] finite drive amplitudes, or NULL (all 0)                    */
     const qp_c64 *rho0;      /* [B][M*M] per-problem initial states (Hermitian, trace 1), or NULL      */
+    const qp_bath *baths;    /* [B] per-problem baths (temperature / coupling sweeps),
+                                or NULL (every problem uses base's bath).  Their eta classes are
+                                computed on the device at qp_batch_run (as qp_eta_device); base's bath
+                                is then unused and may be QP_J_ZERO.  Analytic families 0..3 only.   */
 } qp_batch;
 
 typedef struct qp_batch_plan qp_batch_plan;

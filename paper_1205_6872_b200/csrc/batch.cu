@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(BLOCK) k_batch(const __grid_constant__ BatchAr
     __shared__ double2 sKp[2][N][N];     // K'(new, last) for propagate (0) / terminal (1) self classes
     __shared__ double2 sBeta[2][DM][N];  // exp(delta_d psi_L(old)): propagate / terminal
     __shared__ double2 red[W][N];
-    for (int i = threadIdx.x; i < ntab; i += BLOCK) tabs[i] = a.tab[i];
+    const double2 *src = a.ptab ? a.ptab + (size_t)b * ntab : a.tab;  // per-problem bath or the shared one
+    for (int i = threadIdx.x; i < ntab; i += BLOCK) tabs[i] = src[i];
     if (threadIdx.x < M * M) {
         (&sH0[0][0])[threadIdx.x] = a.tab[ntab + threadIdx.x];
         (&sH1[0][0])[threadIdx.x] = a.tab[ntab + M * M + threadIdx.x];
@@ -253,6 +254,34 @@ __global__ void __launch_bounds__(BLOCK) k_batch(const __grid_constant__ BatchAr
     }
 }
 
+// psi(sigma', e) = -(e s+(sigma') - conj(e) s-(sigma')) (Eq. 9 summand without the later point's Delta s)
+// for every eta class of problem b: rows j = 1..L of psi_eta / psi_E / psi_TI, then psi_self [2][N].
+struct PsiArgs {
+    double s[kMaxM];
+    int M, L;
+};
+__global__ void k_psi(const PsiArgs p, const double2 *__restrict__ eta, double2 *__restrict__ ptab, int B) {
+    const int N = p.M * p.M, L = p.L, nc = 3 * L + 2, ntab = (3 * (L + 1) + 2) * N;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * ntab;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(i / ntab), r = (int)(i % ntab), row = r / N, sg = r % N;
+        int c = -1;  // eta class of this row (qp_plan_eta order), -1: unused row 0 of a lag table
+        if (row < 3 * (L + 1)) {
+            const int g = row / (L + 1), j = row % (L + 1);
+            if (j > 0) c = 2 + g * L + (j - 1);
+        } else {
+            c = row - 3 * (L + 1);  // 0: self interior, 1: self end
+        }
+        double2 v = make_double2(0.0, 0.0);
+        if (c >= 0) {
+            const double2 e = eta[(size_t)b * nc + c];
+            const double sp = p.s[sg / p.M], sm = p.s[sg % p.M];
+            v = make_double2(-(e.x * sp - e.x * sm), -(e.y * sp + e.y * sm));
+        }
+        ptab[i] = v;
+    }
+}
+
 template <int M>
 cudaError_t batch_t(const BatchArgs &a, int B, cudaStream_t s) {
     const size_t dyn = batch_dyn_smem(M, a.L);
@@ -264,6 +293,16 @@ cudaError_t batch_t(const BatchArgs &a, int B, cudaStream_t s) {
 }  // namespace
 
 size_t batch_dyn_smem(int M, int L) { return (size_t)(3 * (L + 1) + 2) * M * M * sizeof(double2); }
+
+cudaError_t launch_psi_tables(int M, const double (&s)[kMaxM], const double2 *eta, double2 *ptab, int B, int L, cudaStream_t st) {
+    PsiArgs p{};
+    for (int i = 0; i < kMaxM; ++i) p.s[i] = s[i];
+    p.M = M, p.L = L;
+    const long long n = (long long)B * (3 * (L + 1) + 2) * M * M;
+    const int grid = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+    k_psi<<<grid, 256, 0, st>>>(p, eta, ptab, B);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_batch(int M, const BatchArgs &a, int B, cudaStream_t s) {
     switch (M) {

@@ -908,23 +908,19 @@ qp_status qp_plan_eta(const qp_plan *P, qp_c64 *out, int64_t cap) {
     return QP_OK;
 }
 
-qp_status qp_eta_device(const qp_bath *baths, int32_t B, double dt, int32_t L, qp_c64 *d_eta, double *d_err,
-                        void *stream) {
-    if (!baths || !d_eta) return err(QP_ERR_ARG, "arg: NULL baths or d_eta");
-    if (B < 1) return err(QP_ERR_ARG, "arg: B must be >= 1 (got %d)", B);
-    if (!(dt > 0.0) || !std::isfinite(dt)) return err(QP_ERR_ARG, "arg: dt must be finite and > 0");
-    if (L < 1 || L > qp::kMaxL) return err(QP_ERR_ARG, "arg: dkmax must be in [1, %d] (got %d)", qp::kMaxL, L);
-    for (int b = 0; b < B; ++b) {
-        const qp_bath &q = baths[b];
-        if (q.kind < QP_J_ZERO || q.kind > QP_J_SUPEROHMIC_GAUSS)
-            return err(QP_ERR_CONFIG, "config: bath %d: kind %d has no device quadrature (analytic families 0..3 only)", b, q.kind);
-        if (q.kind != QP_J_ZERO) {
-            if (!(q.omega_c > 0.0) || !std::isfinite(q.omega_c)) return err(QP_ERR_CONFIG, "config: bath %d: omega_c must be > 0", b);
-            if (!(q.kT >= 0.0) || !std::isfinite(q.kT)) return err(QP_ERR_CONFIG, "config: bath %d: kT must be >= 0", b);
-            if (!std::isfinite(q.coupling)) return err(QP_ERR_CONFIG, "config: bath %d: coupling not finite", b);
-        }
+static qp_status validate_bath(const qp_bath &q, int b) {
+    if (q.kind < QP_J_ZERO || q.kind > QP_J_SUPEROHMIC_GAUSS)
+        return err(QP_ERR_CONFIG, "config: bath %d: kind %d has no device quadrature (analytic families 0..3 only)", b, q.kind);
+    if (q.kind != QP_J_ZERO) {
+        if (!(q.omega_c > 0.0) || !std::isfinite(q.omega_c)) return err(QP_ERR_CONFIG, "config: bath %d: omega_c must be > 0", b);
+        if (!(q.kT >= 0.0) || !std::isfinite(q.kT)) return err(QP_ERR_CONFIG, "config: bath %d: kT must be >= 0", b);
+        if (!std::isfinite(q.coupling)) return err(QP_ERR_CONFIG, "config: bath %d: coupling not finite", b);
     }
-    const cudaStream_t s = (cudaStream_t)stream;
+    return QP_OK;
+}
+
+// enqueue k_eta over B baths (chunks of kEtaBatchMax): d_eta [B][3L+2]
+static qp_status enqueue_eta(const qp_bath *baths, int B, double dt, int L, double2 *d_eta, double *d_err, cudaStream_t s) {
     const size_t nc = 3 * (size_t)L + 2;
     static thread_local qp::EtaBatch batch;  // 16 KB kernel parameter block
     for (int b0 = 0; b0 < B; b0 += qp::kEtaBatchMax) {
@@ -933,11 +929,21 @@ qp_status qp_eta_device(const qp_bath *baths, int32_t B, double dt, int32_t L, q
             const qp_bath &q = baths[b0 + i];
             batch.b[i] = qp::EtaBath{q.kind, q.coupling, q.omega_c, q.kT};
         }
-        const cudaError_t e = qp::launch_eta(batch, nb, L, dt, reinterpret_cast<double2 *>(d_eta) + (size_t)b0 * nc,
-                                             d_err ? d_err + (size_t)b0 * nc : nullptr, s);
+        const cudaError_t e = qp::launch_eta(batch, nb, L, dt, d_eta + (size_t)b0 * nc, d_err ? d_err + (size_t)b0 * nc : nullptr, s);
         if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: eta launch: %s", cudaGetErrorString(e));
     }
     return QP_OK;
+}
+
+qp_status qp_eta_device(const qp_bath *baths, int32_t B, double dt, int32_t L, qp_c64 *d_eta, double *d_err,
+                        void *stream) {
+    if (!baths || !d_eta) return err(QP_ERR_ARG, "arg: NULL baths or d_eta");
+    if (B < 1) return err(QP_ERR_ARG, "arg: B must be >= 1 (got %d)", B);
+    if (!(dt > 0.0) || !std::isfinite(dt)) return err(QP_ERR_ARG, "arg: dt must be finite and > 0");
+    if (L < 1 || L > qp::kMaxL) return err(QP_ERR_ARG, "arg: dkmax must be in [1, %d] (got %d)", qp::kMaxL, L);
+    for (int b = 0; b < B; ++b)
+        if (qp_status st = validate_bath(baths[b], b)) return st;
+    return enqueue_eta(baths, B, dt, L, reinterpret_cast<double2 *>(d_eta), d_err, (cudaStream_t)stream);
 }
 
 qp_status qp_plan_propagator(const qp_plan *P, qp_c64 *U) {
@@ -1382,7 +1388,8 @@ struct qp_batch_plan {
     std::vector<double2> tab, rho0;
     std::vector<double> f;
     std::vector<int> out_idx;
-    size_t off_tab = 0, off_f = 0, off_rho0 = 0, off_idx = 0, off_rho = 0, work_bytes = 0;
+    std::vector<qp_bath> baths;        // per-problem baths (empty: base's bath for all)
+    size_t off_tab = 0, off_f = 0, off_rho0 = 0, off_idx = 0, off_rho = 0, off_eta = 0, off_ptab = 0, work_bytes = 0;
     double setup_seconds = 0.0;
 };
 
@@ -1412,6 +1419,12 @@ qp_status qp_batch_create(const qp_batch *bt, qp_batch_plan **out) {
                     return fail(QP_ERR_CONFIG, "config: H1 not Hermitian");
             }
     }
+    if (bt->baths)
+        for (int b = 0; b < bt->B; ++b)
+            if (validate_bath(bt->baths[b], b)) {
+                const std::string m = g_err;
+                return fail(QP_ERR_CONFIG, m.c_str());
+            }
     if (bt->f)
         for (int64_t i = 0; i < (int64_t)bt->B * P->n_steps; ++i)
             if (!std::isfinite(bt->f[i])) return fail(QP_ERR_CONFIG, "config: drive amplitude f not finite");
@@ -1467,6 +1480,11 @@ qp_status qp_batch_create(const qp_batch *bt, qp_batch_plan **out) {
     bp->off_rho0 = off; off = align256(off + bp->rho0.size() * sizeof(double2));
     bp->off_idx = off;  off = align256(off + bp->out_idx.size() * sizeof(int));
     bp->off_rho = off;  off = align256(off + (size_t)bt->B * P->out_steps.size() * N * sizeof(double2));
+    if (bt->baths) {  // device eta [B][3L+2] and per-problem psi tables [B][(3(L+1)+2) N]
+        bp->baths.assign(bt->baths, bt->baths + bt->B);
+        bp->off_eta = off;  off = align256(off + (size_t)bt->B * (3 * L + 2) * sizeof(double2));
+        bp->off_ptab = off; off = align256(off + (size_t)bt->B * (3 * (L + 1) + 2) * N * sizeof(double2));
+    }
     bp->work_bytes = off;
     bp->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = bp;
@@ -1517,6 +1535,15 @@ qp_status qp_batch_run(qp_batch_plan *bp, void *d_ardm, void *d_work, void *stre
         a.dsig[n] = dsig(*P, n);
     }
     for (int d = 0; d < P->D; ++d) a.delta[d] = P->delta[d];
+    if (!bp->baths.empty()) {  // per-problem eta on the device, then psi rows (Eq. 9 exponents) per problem
+        double2 *eta = (double2 *)(w + bp->off_eta);
+        if (qp_status st = enqueue_eta(bp->baths.data(), bp->B, P->dt, P->L, eta, nullptr, s)) return st;
+        double sv[qp::kMaxM] = {0};
+        for (int i = 0; i < P->M; ++i) sv[i] = P->s[i];
+        a.ptab = (double2 *)(w + bp->off_ptab);
+        const cudaError_t ep = qp::launch_psi_tables(P->M, sv, eta, (double2 *)a.ptab, bp->B, P->L, s);
+        if (ep != cudaSuccess) return err(QP_ERR_CUDA, "cuda: psi table launch failed: %s", cudaGetErrorString(ep));
+    }
     const cudaError_t e = qp::launch_batch(P->M, a, bp->B, s);
     if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: batch launch failed: %s", cudaGetErrorString(e));
     if (rho_out) {

@@ -135,6 +135,7 @@ cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaSt
 struct BatchArgs {
     double2 *A;              // [B][N^L] in place
     const double2 *tab;
+    const double2 *ptab;     // per-problem psi tables [B][(3(L+1)+2) N] (layout of tab's psi part), or nullptr
     const double *f;         // [B][n_steps] drive amplitudes (nullptr: none)
     const double2 *rho0;     // [B][N]
     const int *out_idx;      // [n_steps + 1]: output slot of step k, or -1
@@ -159,6 +160,8 @@ struct EtaBatch {
 };
 cudaError_t launch_eta(const EtaBatch &baths, int B, int L, double dt, double2 *d_eta, double *d_err, cudaStream_t s);
 cudaError_t launch_batch(int M, const BatchArgs &a, int B, cudaStream_t s);
+// psi rows of B problems from their eta classes [B][3L+2] (qp_plan_eta order): ptab[b] in tab's layout
+cudaError_t launch_psi_tables(int M, const double (&s)[kMaxM], const double2 *eta, double2 *ptab, int B, int L, cudaStream_t st);
 constexpr int kBatchBlock = 256;
 
 }  // namespace qp

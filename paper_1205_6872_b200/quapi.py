@@ -82,6 +82,7 @@ class qp_batch(ctypes.Structure):
     _fields_ = [
         ("base", qp_problem), ("B", ctypes.c_int32), ("H1", ctypes.POINTER(qp_c64)),
         ("f", ctypes.POINTER(ctypes.c_double)), ("rho0", ctypes.POINTER(qp_c64)),
+        ("baths", ctypes.POINTER(qp_bath)),
     ]
 
 
@@ -370,7 +371,9 @@ class BatchPlan:
 
     def __init__(self, w: W.Workload, B: int, H1: Optional[np.ndarray] = None, f: Optional[np.ndarray] = None,
                  rho0s: Optional[np.ndarray] = None, out_steps: Optional[Sequence[int]] = None, max_bytes: int = 0,
-                 G_in: Optional[np.ndarray] = None):
+                 G_in: Optional[np.ndarray] = None, baths: Optional[Sequence[tuple]] = None):
+        """``baths``: per-problem (kind, coupling, omega_c, kT) (temperature / coupling sweeps); their eta
+        classes are computed on the device at run time (qp_eta_device) and w's own bath is unused."""
         L = lib()
         self.w, self.B = w, int(B)
         self._keep = []
@@ -394,6 +397,14 @@ class BatchPlan:
             ra = _c64_array(r)
             self._keep.append(ra)
             bt.rho0 = ra
+        if baths is not None:
+            if len(baths) != self.B:
+                raise ValueError(f"baths must hold B = {self.B} entries")
+            ba = (qp_bath * self.B)()
+            for i, q in enumerate(baths):
+                ba[i].kind, ba[i].coupling, ba[i].omega_c, ba[i].kT = int(q[0]), float(q[1]), float(q[2]), float(q[3])
+            self._keep.append(ba)
+            bt.baths = ba
         h = ctypes.c_void_p()
         _check(L.qp_batch_create(ctypes.byref(bt), ctypes.byref(h)))
         self._h = h

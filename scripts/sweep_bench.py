@@ -37,10 +37,17 @@ def main():
     ap.add_argument("--L", type=int, default=7)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--temperature-sweep", action="store_true",
+                    help="problem b also gets its own phonon temperature (5..50 K): per-problem baths, "
+                         "eta classes on the device inside the timed qp_batch_run (SURVEY 8(f2))")
     a = ap.parse_args()
     w, f, areas = sweep_inputs(a.B, a.steps, a.L)
     H1 = 0.5 * np.array([[0, 1], [1, 0]], dtype=complex)
-    bp = Q.BatchPlan(w, a.B, H1=H1, f=f)
+    baths = None
+    if a.temperature_sweep:
+        temps = np.linspace(5.0, 50.0, a.B)
+        baths = [(w.kind, w.coupling, w.omega_c, float(T) * W.KB_OVER_HBAR_PS_K) for T in temps]
+    bp = Q.BatchPlan(w, a.B, H1=H1, f=f, baths=baths)
     ardm, work = bp.alloc()
     st = torch.cuda.current_stream()
     rho = bp.run(ardm, work, st)  # warm-up + result
@@ -56,7 +63,8 @@ def main():
     t = float(np.median(times))
     N, L = 4, a.L
     ps = a.B * a.steps / t
-    line = {"metric": "batched pulse-area sweep: problem-steps/s (Sec. III dot, allPoints readout)",
+    line = {"metric": "batched pulse-area sweep: problem-steps/s (Sec. III dot, allPoints readout)"
+                      + (", per-problem temperature 5..50 K" if baths else ""),
             "value": ps, "unit": "problem-steps/s", "n_gpus": 1, "B": a.B, "steps": a.steps, "L": L,
             "seconds": t, "element_updates_per_s": ps * N ** L, "ardm_bytes_total": 16 * a.B * N ** L,
             "launches_per_run": 1, "dtype": "f64", "data": "synthetic (pulse areas 0..6 pi)",
@@ -70,7 +78,8 @@ def main():
         nsample = 0
         while nsample < a.B and time.perf_counter() - t0 < 10.0:
             Ht = np.stack([w.H + f[nsample, k] * H1 for k in range(a.steps)])
-            ro = O.run(P(w, H_t=Ht), nthreads=ncpu)
+            kT = baths[nsample][3] if baths else w.kT
+            ro = O.run(P(w, H_t=Ht, kT=kT), nthreads=ncpu)
             assert np.abs(ro - rho[nsample]).max() <= 1e-10
             nsample += 1
         el = time.perf_counter() - t0

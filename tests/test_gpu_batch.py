@@ -110,3 +110,34 @@ def test_batch_determinism_and_edges():
     assert np.abs(r2[1] - O.run(P(w2), out_steps=[0, 2, 4])).max() <= TOL
     r3, _ = batch_run(w2.with_(n_steps=0), 2)
     assert np.array_equal(r3[0, 0], w2.rho0)
+
+
+@pytest.mark.parametrize("M,L,n", [(2, 4, 24), (2, 6, 18), (3, 3, 12)])
+def test_per_problem_baths_match_oracle(M, L, n):
+    """Temperature / coupling / spectral-family sweep: problem b has its own bath; its eta
+    classes come from the device quadrature (qp_eta_device) and its psi rows from k_psi.  Each problem
+    vs the oracle run with that bath (its own adaptive G)."""
+    rng = np.random.default_rng(70 + 10 * M + L)
+    baths = [(W.J_OHMIC_EXP, 0.1, 7.5, 0.2), (W.J_OHMIC_EXP, 0.3, 2.0, 0.0), (W.J_DEBYE, 0.1, 7.5, 1.0),
+             (W.J_DEBYE, 0.2, 3.0, 0.05), (W.J_SUPEROHMIC_GAUSS, 0.05, 2.2, 0.3), (W.J_ZERO, 0.0, 1.0, 0.0)]
+    B = len(baths)
+    w = W.random_problem(700 + M + L, M, L, n, kind=W.J_ZERO)  # base bath unused
+    H1 = W.random_hermitian(rng, M)
+    f = 0.5 * rng.standard_normal((B, n))
+    rg, _ = batch_run(w, B, H1=H1, f=f, baths=baths)
+    for b, (kind, xi, wc, kT) in enumerate(baths):
+        wb = w.with_(kind=kind, coupling=xi, omega_c=wc, kT=kT)
+        ro = oracle_problem(wb, b, H1, f)
+        assert np.abs(rg[b] - ro).max() <= TOL, (b, np.abs(rg[b] - ro).max())
+        assert np.abs(np.einsum("kii->k", rg[b]) - 1).max() <= 1e-12
+
+
+def test_per_problem_baths_equal_shared_bath():
+    """baths = B copies of the shared bath reproduces the shared-bath batch (device vs host eta: within
+    rounding, so within 1e-13 rather than bit for bit)."""
+    w = W.CONFIGS[3].with_(L=5, n_steps=30)
+    rng = np.random.default_rng(5)
+    rho0s = np.stack([W.random_density_matrix(rng, 2) for _ in range(3)])
+    a, _ = batch_run(w, 3, rho0s=rho0s)
+    b, _ = batch_run(w, 3, rho0s=rho0s, baths=[Q.bath_of(w)] * 3)
+    assert np.abs(a - b).max() < 1e-13

@@ -166,3 +166,13 @@ def test_eta_table_input_reproduces_plan(cfg):
     bad[3] = np.nan
     with pytest.raises(Q.QuapiError, match="eta_in"):
         Q.Plan(w, eta_in=bad)
+
+
+def test_batch_per_problem_bath_validation():
+    w = W.random_problem(3, 2, 3, 6, kind=W.J_ZERO)
+    with pytest.raises(Q.QuapiError, match="bath 1"):
+        Q.BatchPlan(w, 2, baths=[(1, 0.1, 7.5, 0.2), (W.J_DEBYE, 0.1, -1.0, 0.2)])
+    with pytest.raises(ValueError):
+        Q.BatchPlan(w, 2, baths=[(1, 0.1, 7.5, 0.2)])
+    bp = Q.BatchPlan(w, 2, baths=[(1, 0.1, 7.5, 0.2), (2, 0.1, 7.5, 0.2)])
+    assert bp.sizes.work_bytes > Q.BatchPlan(w, 2).sizes.work_bytes
