@@ -11,6 +11,8 @@
 //   out[new] = K'(new, last) exp(Ds(new) Psi(mid)) sum_old exp(Ds(new) psi_L(old)) a[old]
 // with the Eq. 9 exponents evaluated directly from the per-lag psi tables (Psi = sum over the kept
 // partners, one complex exp per Delta-s class), so no per-launch-set factor tables are needed.
+#include <cstdlib>
+
 #include "qp_internal.h"
 
 namespace qp {
@@ -96,18 +98,28 @@ __device__ void expm_herm(const double2 (&H)[M][M], double dt, double2 (&U)[M][M
     }
 }
 
-template <int M, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_batch(const __grid_constant__ BatchArgs a) {
+// SMEM: the problem's whole ARDM lives in shared memory for the run (small L), written back at the end.
+template <int M, int BLOCK, bool SMEM, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) k_batch(const __grid_constant__ BatchArgs a) {
     constexpr int N = M * M, W = BLOCK / 32, DM = kMaxD;
-    const int b = blockIdx.x, L = a.L;
-    double2 *const A = a.A + (size_t)b * a.NL;
-    extern __shared__ double2 tabs[];  // psi_eta, psi_E, psi_TI [L+1][N]; psi_self [2][N]
+    constexpr int DMX = M * (M - 1);  // largest class count for this M (general s)
+    const int b = blockIdx.x, L = a.L, D = a.D;
+    // dynamic shared memory: psi_eta, psi_E, psi_TI [L+1][N]; psi_self [2][N]; then the slide factor
+    // tables sT[kap][d][j][sigma] = exp(delta_d psi^kap_j(sigma)) (kap 0: eta_j rows, propagate; 1: E_j
+    // rows, terminal; j = 0..L-1, row 0 = 1); then (SMEM) the ARDM
+    extern __shared__ double2 tabs[];
     const int ntab = (3 * (L + 1) + 2) * N;
     double2 *const pEta = tabs, *const pE = tabs + (L + 1) * N, *const pTI = tabs + 2 * (L + 1) * N,
                    *const pSelf = tabs + 3 * (L + 1) * N;
+    double2 *const sT = tabs + ntab;
+    const int nT = 2 * D * L * N;
+    double2 *const A = SMEM ? sT + nT : a.A + (size_t)b * a.NL;
     __shared__ double2 sH0[M][M], sH1[M][M], sU[M][M];
     __shared__ double2 sKp[2][N][N];     // K'(new, last) for propagate (0) / terminal (1) self classes
-    __shared__ double2 sBeta[2][DM][N];  // exp(delta_d psi_L(old)): propagate / terminal
+    // exp(delta_d psi_L(old)) of the lag-L partner [variant][kap][d][old]: variant 0 (k > L) propagate
+    // eta_L / terminal E_L; variant 1 (k == L, partner sigma_0) propagate E_L / terminal TI_L
+    __shared__ double2 sBetaV[2][2][DMX][N];
+    __shared__ double2 sSelf[2][N];      // exp(Ds(n) psi_self(n)): interior G(1) / end G(1/2) self factor
     __shared__ double2 red[W][N];
     const double2 *src = a.ptab ? a.ptab + (size_t)b * ntab : a.tab;  // per-problem bath or the shared one
     for (int i = threadIdx.x; i < ntab; i += BLOCK) tabs[i] = src[i];
@@ -116,6 +128,17 @@ __global__ void __launch_bounds__(BLOCK) k_batch(const __grid_constant__ BatchAr
         (&sH1[0][0])[threadIdx.x] = a.tab[ntab + M * M + threadIdx.x];
     }
     __syncthreads();
+    for (int i = threadIdx.x; i < nT; i += BLOCK) {  // read after the step loop's first barrier
+        const int kap = i / (D * L * N), d = (i / (L * N)) % D, j = (i / N) % L, sg = i % N;
+        sT[i] = j == 0 ? make_double2(1.0, 0.0) : bexp(bscale((kap == 0 ? pEta : pE)[j * N + sg], a.delta[d]));
+    }
+    for (int i = threadIdx.x; i < 2 * 2 * D * N; i += BLOCK) {  // step-independent factors, built once
+        const int var = i / (2 * D * N), kap = (i / (D * N)) % 2, d = (i / N) % D, old = i % N;
+        const double2 ps = kap == 0 ? (var ? pE[L * N + old] : pEta[L * N + old])
+                                    : (var ? pTI[L * N + old] : pE[L * N + old]);
+        sBetaV[var][kap][d][old] = bexp(bscale(ps, a.delta[d]));
+    }
+    for (int i = threadIdx.x; i < 2 * N; i += BLOCK) sSelf[i / N][i % N] = bexp(bscale(pSelf[i], a.dsig[i % N]));
     const double2 *r0 = a.rho0 + (size_t)b * N;
     if (threadIdx.x < N) {  // A_0(sigma_0) = rho0(sigma_0) I(sigma_0, sigma_0; eta_00 = G(1/2))
         const int n = threadIdx.x;
@@ -135,22 +158,16 @@ __global__ void __launch_bounds__(BLOCK) k_batch(const __grid_constant__ BatchAr
                 for (int j = 0; j < M; ++j) sU[i][j] = U[i][j];
         }
         __syncthreads();  // sU ready; previous step's writes visible
-        for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) {
-            const int kap = i / (N * N), nw = (i / N) % N, last = i % N;
-            // K(new, last) = U[a, a'] conj(U[b, b']) (Eq. 8), times the self factor of the new point
-            const double2 ua = sU[nw / M][last / M], ub = sU[nw % M][last % M];
-            const double2 kk = bmul(ua, make_double2(ub.x, -ub.y));
-            sKp[kap][nw][last] = bmul(kk, bexp(bscale(pSelf[kap * N + nw], a.dsig[nw])));
-        }
-        if (k >= L)
-            for (int i = threadIdx.x; i < 2 * a.D * N; i += BLOCK) {
-                const int kap = i / (a.D * N), d = (i / N) % a.D, old = i % N;
-                // lag-L partner sigma_{k-L}: propagate eta_L (E_L at k = L), terminal E_L (TI_L at k = L)
-                const double2 ps = kap == 0 ? (k == L ? pE[L * N + old] : pEta[L * N + old])
-                                            : (k == L ? pTI[L * N + old] : pE[L * N + old]);
-                sBeta[kap][d][old] = bexp(bscale(ps, a.delta[d]));
+        if (k == 1 || a.f != nullptr) {
+            for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) {
+                const int kap = i / (N * N), nw = (i / N) % N, last = i % N;
+                // K(new, last) = U[a, a'] conj(U[b, b']) (Eq. 8), times the self factor of the new point
+                const double2 ua = sU[nw / M][last / M], ub = sU[nw % M][last % M];
+                sKp[kap][nw][last] = bmul(bmul(ua, make_double2(ub.x, -ub.y)), sSelf[kap][nw]);
             }
-        __syncthreads();
+            __syncthreads();
+        }
+        const double2(*sBeta)[DMX][N] = sBetaV[k == L ? 1 : 0];
         double2 acc[N];
 #pragma unroll
         for (int n = 0; n < N; ++n) acc[n] = make_double2(0.0, 0.0);
@@ -158,51 +175,59 @@ __global__ void __launch_bounds__(BLOCK) k_batch(const __grid_constant__ BatchAr
             long long nin = 1;
             for (int t = 0; t < k; ++t) nin *= N;
             for (long long x = threadIdx.x; x < nin; x += BLOCK) {
-                int dig[kMaxL];
-                long long r = x;
-                for (int t = 0; t < k; ++t) dig[t] = (int)(r % N), r /= N;
-                const int last = dig[k - 1];
+                int last = 0;
                 double2 Pp = make_double2(0.0, 0.0), Pt = make_double2(0.0, 0.0);
-                for (int j = 1; j <= k; ++j) {  // partner point k - j in digit k - j
-                    const int sg = dig[k - j];
+                long long r = x;
+                for (int t = 0; t < k; ++t) {  // digit t holds point t, the partner at lag j = k - t
+                    const int sg = (int)(r % N), j = k - t;
+                    r /= N;
+                    if (t == k - 1) last = sg;
                     Pp = badd(Pp, j < k ? pEta[j * N + sg] : pE[k * N + sg]);
                     Pt = badd(Pt, j < k ? pE[j * N + sg] : pTI[k * N + sg]);
                 }
                 const double2 ax = A[x];
-                double2 Ep[DM], Et[DM];
-                for (int d = 0; d < a.D; ++d) {
+                double2 Ep[DMX] = {}, Et[DMX] = {};
+#pragma unroll
+                for (int d = 0; d < DMX; ++d) {
+                    if (d >= D) break;
                     Ep[d] = bexp(bscale(Pp, a.delta[d]));
                     if (ro) Et[d] = bexp(bscale(Pt, a.delta[d]));
                 }
-                if (ro)
-#pragma unroll
-                    for (int n = 0; n < N; ++n) {
-                        const int c = a.cls[n];
-                        acc[n] = bfma(c ? bmul(sKp[1][n][last], Et[c - 1]) : sKp[1][n][last], ax, acc[n]);
-                    }
 #pragma unroll
                 for (int v = N - 1; v >= 0; --v) {  // v = 0 overwrites x itself: last
                     const int c = a.cls[v];
-                    A[x + v * nin] = bmul(c ? bmul(sKp[0][v][last], Ep[c - 1]) : sKp[0][v][last], ax);
+                    double2 fp = make_double2(1.0, 0.0), ft = make_double2(1.0, 0.0);
+#pragma unroll
+                    for (int d = 0; d < DMX; ++d)  // register-resident select
+                        if (c == d + 1) fp = Ep[d], ft = Et[d];
+                    if (ro) acc[v] = bfma(bmul(sKp[1][v][last], ft), ax, acc[v]);
+                    A[x + v * nin] = bmul(bmul(sKp[0][v][last], fp), ax);
                 }
             }
-        } else {  // slide on slot p = k mod L
-            const int p = (int)(k % L);
-            long long Pp_ = 1;
+        } else {  // slide on slot p = k mod L: exp(delta_d Psi) as products of the sT digit factors
+            const int p = (int)(k % L), qlast = (p - 1 + L) % L;
+            unsigned Pp_ = 1;
             for (int t = 0; t < p; ++t) Pp_ *= N;
-            const long long nf = a.NL / N;
-            for (long long fi = threadIdx.x; fi < nf; fi += BLOCK) {
-                const long long xb = (fi % Pp_) + (fi / Pp_) * Pp_ * N;
-                int dig[kMaxL];
-                long long r = xb;
-                for (int t = 0; t < L; ++t) dig[t] = (int)(r % N), r /= N;
-                const int last = dig[(p - 1 + L) % L];
-                double2 Pp = make_double2(0.0, 0.0), Pt = make_double2(0.0, 0.0);
+            const unsigned nf = (unsigned)(a.NL / N);  // N^(L-1) < 2^32 for batch problems
+            for (unsigned fi = threadIdx.x; fi < nf; fi += BLOCK) {
+                const unsigned xb = (fi % Pp_) + (fi / Pp_) * Pp_ * N;
+                double2 Ep[DMX], Et[DMX];
+#pragma unroll
+                for (int d = 0; d < DMX; ++d) Ep[d] = Et[d] = make_double2(1.0, 0.0);
+                int last = 0;
+                unsigned r = xb;
                 for (int q = 0; q < L; ++q) {
+                    const int dq = (int)(r % N);
+                    r /= N;
+                    if (q == qlast) last = dq;
                     if (q == p) continue;
-                    const int lag = (p - q + L) % L;  // 1..L-1
-                    Pp = badd(Pp, pEta[lag * N + dig[q]]);
-                    Pt = badd(Pt, pE[lag * N + dig[q]]);
+                    const double2 *t0 = sT + ((p - q + L) % L) * N + dq;  // lag 1..L-1
+#pragma unroll
+                    for (int d = 0; d < DMX; ++d)
+                        if (d < D) {
+                            Ep[d] = bmul(Ep[d], t0[d * L * N]);
+                            if (ro) Et[d] = bmul(Et[d], t0[(D + d) * L * N]);
+                        }
                 }
                 double2 xo[N];
 #pragma unroll
@@ -210,26 +235,30 @@ __global__ void __launch_bounds__(BLOCK) k_batch(const __grid_constant__ BatchAr
                 double2 S0 = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int o = 0; o < N; ++o) S0 = badd(S0, xo[o]);
-                double2 mP[DM], mT[DM];
-                for (int d = 0; d < a.D; ++d) {
-                    const double2 Ed = bexp(bscale(Pp, a.delta[d]));
+                double2 mP[DMX] = {}, mT[DMX] = {};
+#pragma unroll
+                for (int d = 0; d < DMX; ++d) {
+                    if (d >= D) break;
                     double2 m = make_double2(0.0, 0.0);
 #pragma unroll
                     for (int o = 0; o < N; ++o) m = bfma(sBeta[0][d][o], xo[o], m);
-                    mP[d] = bmul(Ed, m);
+                    mP[d] = bmul(Ep[d], m);
                     if (ro) {
-                        const double2 Td = bexp(bscale(Pt, a.delta[d]));
                         double2 mt = make_double2(0.0, 0.0);
 #pragma unroll
                         for (int o = 0; o < N; ++o) mt = bfma(sBeta[1][d][o], xo[o], mt);
-                        mT[d] = bmul(Td, mt);
+                        mT[d] = bmul(Et[d], mt);
                     }
                 }
 #pragma unroll
                 for (int n = 0; n < N; ++n) {
                     const int c = a.cls[n];
-                    A[xb + n * Pp_] = bmul(sKp[0][n][last], c ? mP[c - 1] : S0);
-                    if (ro) acc[n] = bfma(sKp[1][n][last], c ? mT[c - 1] : S0, acc[n]);
+                    double2 mp = S0, mt = S0;
+#pragma unroll
+                    for (int d = 0; d < DMX; ++d)  // register-resident select (no local-memory indexing)
+                        if (c == d + 1) mp = mP[d], mt = mT[d];
+                    A[xb + n * Pp_] = bmul(sKp[0][n][last], mp);
+                    if (ro) acc[n] = bfma(sKp[1][n][last], mt, acc[n]);
                 }
             }
         }
@@ -252,6 +281,8 @@ __global__ void __launch_bounds__(BLOCK) k_batch(const __grid_constant__ BatchAr
         }
         __syncthreads();  // step complete before the next step reads A
     }
+    if constexpr (SMEM)  // the caller's ARDM buffer holds the final A, as on the global-memory path
+        for (long long i = threadIdx.x; i < a.NL; i += BLOCK) a.A[(size_t)b * a.NL + i] = A[i];
 }
 
 // psi(sigma', e) = -(e s+(sigma') - conj(e) s-(sigma')) (Eq. 9 summand without the later point's Delta s)
@@ -282,17 +313,35 @@ __global__ void k_psi(const PsiArgs p, const double2 *__restrict__ eta, double2 
     }
 }
 
+constexpr size_t kBatchSmemArdmMax = 100 * 1024;  // ARDM + tables in shared memory up to this size
+
+template <int M, bool SMEM, int MINB>
+cudaError_t batch_launch(const BatchArgs &a, int B, size_t dyn, cudaStream_t s) {
+    cudaFuncSetAttribute(k_batch<M, kBatchBlock, SMEM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    k_batch<M, kBatchBlock, SMEM, MINB><<<B, kBatchBlock, dyn, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int M>
 cudaError_t batch_t(const BatchArgs &a, int B, cudaStream_t s) {
-    const size_t dyn = batch_dyn_smem(M, a.L);
-    cudaFuncSetAttribute(k_batch<M, kBatchBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    k_batch<M, kBatchBlock><<<B, kBatchBlock, dyn, s>>>(a);
-    return cudaGetLastError();
+    const size_t tab = batch_dyn_smem(M, a.L, a.D);
+    const size_t full = tab + (size_t)a.NL * sizeof(double2);
+    const bool smem = full <= kBatchSmemArdmMax && !std::getenv("QUAPI_BATCH_GLOBAL");
+    // M = 2: 3 CTAs (24 warps, 80 registers) per SM for the shared-memory-resident ARDM, 2 CTAs (128
+    // registers, no spills) when the ARDM stays in global memory (measured: L = 5 13.8 vs 15.0 ms, L = 7
+    // 0.198 vs 0.177 s for 1024 problems x 1000 steps); QUAPI_BATCH_MINB=2|3 overrides
+    const char *mb = std::getenv("QUAPI_BATCH_MINB");
+    const bool three = mb ? mb[0] == '3' : smem;
+    if (M == 2 && three)
+        return smem ? batch_launch<M, true, 3>(a, B, full, s) : batch_launch<M, false, 3>(a, B, tab, s);
+    return smem ? batch_launch<M, true, M == 2 ? 2 : 1>(a, B, full, s) : batch_launch<M, false, M == 2 ? 2 : 1>(a, B, tab, s);
 }
 
 }  // namespace
 
-size_t batch_dyn_smem(int M, int L) { return (size_t)(3 * (L + 1) + 2) * M * M * sizeof(double2); }
+size_t batch_dyn_smem(int M, int L, int D) {
+    return ((size_t)(3 * (L + 1) + 2) * M * M + (size_t)2 * D * L * M * M) * sizeof(double2);
+}
 
 cudaError_t launch_psi_tables(int M, const double (&s)[kMaxM], const double2 *eta, double2 *ptab, int B, int L, cudaStream_t st) {
     PsiArgs p{};

@@ -148,7 +148,7 @@ struct BatchArgs {
     double dsig[kMaxN];      // Delta s(n)
     double delta[kMaxD];     // Delta s of class d + 1
 };
-size_t batch_dyn_smem(int M, int L);
+size_t batch_dyn_smem(int M, int L, int D);  // tables only (the ARDM may add N^L entries)
 // Device eta setup (eta.cu): kind as qp_bath_kind (0..3), xi = coupling.
 struct EtaBath {
     int kind;
