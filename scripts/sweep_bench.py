@@ -70,6 +70,25 @@ def main():
             "launches_per_run": 1, "dtype": "f64", "data": "synthetic (pulse areas 0..6 pi)",
             "rho11_final_min_max": [float(rho[:, -1, 1, 1].real.min()), float(rho[:, -1, 1, 1].real.max())],
             "max_abs_trace_err": float(np.abs(np.einsum("bkii->bk", rho) - 1).max())}
+    # roofline of k_batch (one step per pass over each problem's ARDM): FP64 flops per element update
+    # counted from the slide step with readout (M = 2, D = 2; per fibre of N = 4 entries: digit-factor
+    # products 24 (L-1), S0 6, beta moments 128, class factors 24, outputs 24, readout 32), bytes 32 per
+    # element update when the ARDM streams through HBM (B N^L 16 B > L2), else none (L2 / smem resident)
+    flops = (24 * (L - 1) + 214) / N
+    tflops = ps * N ** L * flops / 1e12
+    fp64_peak = 35.1  # measured DFMA rate, scripts/membench.cu (profiles/README.md); no FP64 in MEASURED_PEAKS
+    ardm = 16 * a.B * N ** L
+    hbm = None
+    if ardm > 2 * 126e6:
+        pk = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
+        gbs = ps * N ** L * 32 / 1e9
+        hbm = {"achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"]}
+    alu = {"achieved": tflops, "peak": fp64_peak, "unit": "TFLOP/s", "frac": tflops / fp64_peak,
+           "flops_per_element_update": flops}
+    if hbm and hbm["frac"] > alu["frac"]:
+        line["roofline"] = {"bound": "hbm", **hbm, "alu": alu}
+    else:
+        line["roofline"] = {"bound": "alu", **alu, "hbm": hbm}
     if not a.no_cpu_baseline:
         import oracle as O
         from tests.test_oracle_engine import P
