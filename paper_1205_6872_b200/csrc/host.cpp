@@ -641,6 +641,8 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     // k_fused3 lane map 1 (32 consecutive fibres per warp load) when fibres t, t+1 are adjacent
     a.lane_map = (T >= 64 && ls.lofs[1].x == 1) ? 1 : 0;
     if (const char *e = std::getenv("QUAPI_F3MAP")) a.lane_map = (e[0] == '1' && T >= 64) ? 1 : 0;
+    // measured on cfg3: CTA barrier per round 1.99 ms per launch vs 2.06 ms with last-reader refill
+    a.tma_last_reader = std::getenv("QUAPI_F3_LASTREADER") ? 1 : 0;
     // TMA staging (k_fused3, unsharded, lane map 1 with slot 0 the lowest outer slot): the outer
     // slots are two runs of consecutive slots, A = 0 .. p0-1 and B = p0+3 .. L-1
     ls.tma_a = -1;  // (-1: no TMA view; 0: view B; -2: view C; -3: view D)

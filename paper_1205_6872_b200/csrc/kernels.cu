@@ -940,6 +940,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     int2 *sLo = reinterpret_cast<int2 *>(sE0 + (STG ? 2 * S * 2 * D * F : 0));
     double2 *dyn_smem = sE0 + (STG ? 2 * S * 2 * D * F + F : 0);
     __shared__ __align__(8) unsigned long long sFull;
+    __shared__ unsigned sRead;  // warps that have read the current stage (tma_last_reader)
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem + W * 16 * 8);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
@@ -1106,6 +1107,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     if constexpr (TM) {
         if (threadIdx.x == 0) {
             mbar_init(&sFull, 1);
+            sRead = 0;
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
@@ -1170,9 +1172,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                             X[d1][d0] = stage[fib * a.tma_sf + d0 * a.tma_s[0] + d1 * a.tma_s[1] + j * a.tma_s[2]];
                         }
                     }
-                __syncthreads();  // stage free: refill it with the next unit
                 const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
-                if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
+                if (a.tma_last_reader) {
+                    // the last warp to finish reading the stage refills it: no CTA-wide barrier per round.
+                    // (A warp reads round r+1's stage only after finishing round r, so when round r+1 has
+                    // been read by every warp the double-buffered E0 / offsets of round r are free too.)
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        if (atomicAdd(&sRead, 1u) == (unsigned)W - 1) {
+                            atomicExch(&sRead, 0u);
+                            if (taun < t_end) tma_issue(taun, rn, phase);
+                        }
+                    }
+                } else {
+                    __syncthreads();  // stage free: refill it with the next unit
+                    if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
+                }
             } else if constexpr (CA) {  // the stage holds this unit (copied one unit ago)
                 cp_async_wait<0>();
                 __syncthreads();

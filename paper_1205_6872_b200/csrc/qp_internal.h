@@ -64,6 +64,8 @@ struct FusedArgs {
     int rho_accumulate;      // 1: rho[n] += sum (several shard blocks contribute to one step)
     int lane_map;            // k_fused3 lane map (kernels.cu): 1 when tile fibres t, t+1 are adjacent in HBM
     int use_tma;             // k_fused3 (unsharded): rounds staged by TMA through `tmap` (1) or cp.async (2)
+    int tma_last_reader;     // k_fused3 TMA rounds: 1 = the last warp to read the stage issues the next
+                             // round (no CTA barrier per round; slower, kept selectable); 0 = CTA barrier
     long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view (view B: 1)
     int tma_c0m;             // TMA coordinate 0 = tma_c0m x (G mod tma_nA) doubles
     int tma_swz;             // 1 / 2: view-B / view-C stage (128-B rows, 128-B swizzle; kernels.cu k_fused3)
