@@ -101,7 +101,7 @@ __device__ void expm_herm(const double2 (&H)[M][M], double dt, double2 (&U)[M][M
 // SMEM: the problem's whole ARDM lives in shared memory for the run (small L), written back at the end.
 template <int M, int BLOCK, bool SMEM, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB) k_batch(const __grid_constant__ BatchArgs a) {
-    constexpr int N = M * M, W = BLOCK / 32, DM = kMaxD;
+    constexpr int N = M * M, W = BLOCK / 32;
     constexpr int DMX = M * (M - 1);  // largest class count for this M (general s)
     const int b = blockIdx.x, L = a.L, D = a.D;
     // dynamic shared memory: psi_eta, psi_E, psi_TI [L+1][N]; psi_self [2][N]; then the slide factor
