@@ -487,11 +487,15 @@ static EncodeTiledFn encode_tiled() {
 // k_fused3's TMA view of the ARDM for launch set ls: 5-D tensor of FP64 (run A as 2 x N^a doubles,
 // run B, inner d0, d1, d2), box = one round of F outer fibres x N^3 inner entries.  Returns false
 // (the kernel then loads with plain LDG) if the driver cannot encode it.
+// view D (p0 = 0) with the original 64-B rows + 64-B swizzle instead of 128-B rows (QUAPI_VIEWD64=1)
+static bool f3_view_d64() { return std::getenv("QUAPI_VIEWD64") != nullptr; }
+
 static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, double2 *A, int F) {
     if (ls.tma_A == A) return true;
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return false;
     const int p0 = ls.p0, L = P.L;
+    const bool d64 = f3_view_d64();
     cuuint64_t gdim[5], gstr[4];
     cuuint32_t box[5];
     if (ls.tma_a > 0) {  // view A: (run A as doubles, run B, d0, d1, d2); stage [d2][d1][d0][f]
@@ -503,12 +507,19 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
                                   16ull * ipow(P.N, p0 + 2)};
         const cuuint32_t bx[5] = {(cuuint32_t)(2 * boxA), (cuuint32_t)(F / boxA), 4, 4, 4};
         std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
-    } else if (ls.tma_a == -3) {  // view D (p0 = 0): (d0 = slot 0 as doubles, f, d1, d2): 64-B rows, 64-B
-              // swizzle.  stage [d2][d1][f] rows of the 4 d0 entries, chunk XOR ((row >> 1) & 3)
+    } else if (ls.tma_a == -3 && d64) {  // view D, 64-B rows (p0 = 0): (d0 = slot 0 as doubles, f, d1, d2),
+              // 64-B swizzle.  stage [d2][d1][f] rows of the 4 d0 entries, chunk XOR ((row >> 1) & 3)
         if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F) return false;
         const cuuint64_t gd[5] = {8, (cuuint64_t)ipow(P.N, L - 3), 4, 4, 1};
         const cuuint64_t gs[4] = {16ull * 64, 16ull * 4, 16ull * 16, 16ull * ipow(P.N, L)};
         const cuuint32_t bx[5] = {8, (cuuint32_t)F, 4, 4, 1};
+        std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
+    } else if (ls.tma_a == -3) {  // view D (p0 = 0): 128-B rows of the 8 entries (d1 & 1, d0), then f,
+              // d1 / 2, d2; 128-B swizzle.  stage [d2][d1 / 2][f] rows, 16-B chunk XOR (row & 7)
+        if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F) return false;
+        const cuuint64_t gd[5] = {16, (cuuint64_t)ipow(P.N, L - 3), 2, 4, 1};
+        const cuuint64_t gs[4] = {16ull * 64, 16ull * 8, 16ull * 16, 16ull * ipow(P.N, L)};
+        const cuuint32_t bx[5] = {16, (cuuint32_t)F, 2, 4, 1};
         std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
     } else if (ls.tma_a == -2) {  // view C (p0 = L-1): slots 0..L-2 (= d1 + 4 d2 + 16 f) as 128-B rows
               // (d1, d2 & 1), two rows per fibre, then d0 = slot L-1; 128-B swizzle.  stage [d0][2 f + d2/2][8]
@@ -527,7 +538,7 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
     }
     const cuuint32_t es[5] = {1, 1, 1, 1, 1};
     if (enc(&ls.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)A, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            ls.tma_a > 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : (ls.tma_a == -3 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
+            ls.tma_a > 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : (ls.tma_a == -3 && d64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
@@ -641,8 +652,6 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     // k_fused3 lane map 1 (32 consecutive fibres per warp load) when fibres t, t+1 are adjacent
     a.lane_map = (T >= 64 && ls.lofs[1].x == 1) ? 1 : 0;
     if (const char *e = std::getenv("QUAPI_F3MAP")) a.lane_map = (e[0] == '1' && T >= 64) ? 1 : 0;
-    // measured on cfg3: CTA barrier per round 1.99 ms per launch vs 2.06 ms with last-reader refill
-    a.tma_last_reader = std::getenv("QUAPI_F3_LASTREADER") ? 1 : 0;
     // TMA staging (k_fused3, unsharded, lane map 1 with slot 0 the lowest outer slot): the outer
     // slots are two runs of consecutive slots, A = 0 .. p0-1 and B = p0+3 .. L-1
     ls.tma_a = -1;  // (-1: no TMA view; 0: view B; -2: view C; -3: view D)
@@ -1049,7 +1058,7 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
                 a.tma_nA = ls.tma_a > 0 ? ipow(P->N, ls.tma_a) : (ls.tma_a == 0 ? 2 : 1);
                 a.tma_c0m = ls.tma_a > 0 ? 2 : 0;
                 a.tma_c1m = ls.tma_a == -2 ? 2 : 1;
-                a.tma_swz = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? 2 : 3));
+                a.tma_swz = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? 2 : (f3_view_d64() ? 3 : 4)));
                 if (ls.tma_a > 0) a.tma_sf = 1, a.tma_s[0] = F, a.tma_s[1] = 4 * F, a.tma_s[2] = 16 * F;
                 else a.tma_sf = 4, a.tma_s[0] = 4 * F, a.tma_s[1] = 16 * F, a.tma_s[2] = 1;
             }

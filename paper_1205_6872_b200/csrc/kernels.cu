@@ -914,7 +914,9 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const void *tmap, unsigne
 
 // PFM (next-round prefetch): 0 none, 1 registers, 2 TMA box into a shared-memory stage (lane map 1,
 // unsharded layouts: FusedArgs::tmap, dims (run A, run B, d0, d1, d2), see host.cpp)
-template <bool SYM, int MAP, int BLOCK, int MINB, int PFM, bool RO>
+// VW: the TMA stage view (FusedArgs::tma_swz) fixed at compile time (-1: read a.tma_swz at run time);
+// one view per instantiation keeps the other views' stage-read code out of the register allocation.
+template <bool SYM, int MAP, int BLOCK, int MINB, int PFM, bool RO, int VW = -1>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ FusedArgs a) {
     constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2;
     constexpr bool PF = PFM == 1, TM = PFM == 2, CA = PFM == 3, STG = TM || CA;
@@ -940,7 +942,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     int2 *sLo = reinterpret_cast<int2 *>(sE0 + (STG ? 2 * S * 2 * D * F : 0));
     double2 *dyn_smem = sE0 + (STG ? 2 * S * 2 * D * F + F : 0);
     __shared__ __align__(8) unsigned long long sFull;
-    __shared__ unsigned sRead;  // warps that have read the current stage (tma_last_reader)
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem + W * 16 * 8);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
@@ -1107,7 +1108,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     if constexpr (TM) {
         if (threadIdx.x == 0) {
             mbar_init(&sFull, 1);
-            sRead = 0;
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
@@ -1155,40 +1155,30 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 cur = phase;
                 phase ^= 1;
                 lo = sLo[cur * F + fib];
+                const int swz = VW >= 0 ? VW : a.tma_swz;
 #pragma unroll
                 for (int d1 = 0; d1 < N; ++d1)
 #pragma unroll
                     for (int d0 = 0; d0 < N; ++d0) {
-                        if (a.tma_swz == 1) {  // view B: row r of 8 entries (fibre parity, d2); chunk XOR (r & 7)
+                        if (swz == 1) {  // view B: row r of 8 entries (fibre parity, d2); chunk XOR (r & 7)
                             const int r = (d1 * N + d0) * (F / 2) + (fib >> 1);
                             X[d1][d0] = stage[r * 8 + ((((fib & 1) << 2) | j) ^ (r & 7))];
-                        } else if (a.tma_swz == 3) {  // view D: 64-B row r = (d2, d1, f) of the d0 entries
+                        } else if (swz == 4) {  // view D: 128-B row r = (d2, d1 / 2, f) of entries (d1 & 1, d0)
+                            const int r = (j * 2 + (d1 >> 1)) * F + fib;
+                            X[d1][d0] = stage[r * 8 + ((((d1 & 1) << 2) | d0) ^ (r & 7))];
+                        } else if (swz == 3) {  // view D, 64-B rows: row r = (d2, d1, f) of the d0 entries
                             const int r = (j * N + d1) * F + fib;
                             X[d1][d0] = stage[r * 4 + (d0 ^ ((r >> 1) & 3))];
-                        } else if (a.tma_swz == 2) {  // view C: row r of 8 entries (d2 parity, d1)
+                        } else if (swz == 2) {  // view C: row r of 8 entries (d2 parity, d1)
                             const int r = d0 * 2 * F + 2 * fib + (j >> 1);
                             X[d1][d0] = stage[r * 8 + ((((j & 1) << 2) | d1) ^ (r & 7))];
                         } else {
                             X[d1][d0] = stage[fib * a.tma_sf + d0 * a.tma_s[0] + d1 * a.tma_s[1] + j * a.tma_s[2]];
                         }
                     }
+                __syncthreads();  // stage free: refill it with the next unit
                 const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
-                if (a.tma_last_reader) {
-                    // the last warp to finish reading the stage refills it: no CTA-wide barrier per round.
-                    // (A warp reads round r+1's stage only after finishing round r, so when round r+1 has
-                    // been read by every warp the double-buffered E0 / offsets of round r are free too.)
-                    __syncwarp();
-                    if (lane == 0) {
-                        __threadfence_block();
-                        if (atomicAdd(&sRead, 1u) == (unsigned)W - 1) {
-                            atomicExch(&sRead, 0u);
-                            if (taun < t_end) tma_issue(taun, rn, phase);
-                        }
-                    }
-                } else {
-                    __syncthreads();  // stage free: refill it with the next unit
-                    if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
-                }
+                if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
             } else if constexpr (CA) {  // the stage holds this unit (copied one unit ago)
                 cp_async_wait<0>();
                 __syncthreads();
@@ -1283,12 +1273,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
             }
             if (valid) {  // X[d1][d2] with digit 0 = j
                 const long long b0 = base + (long long)j * a.pw_in[0];
-                if (a.pw_in[2] == 1) {  // d2 is ring slot 0: 32-B stores of adjacent pairs
+                // store path: which inner digit is ring slot 0 follows from the view when VW is fixed
+                // (view B: d2 = slot 0; view C: d1 = slot 0; views A and D: neither)
+                const bool st_d2 = VW >= 0 ? VW == 1 : a.pw_in[2] == 1;
+                const bool st_d1 = VW >= 0 ? VW == 2 : a.pw_in[1] == 1;
+                if (st_d2) {  // d2 is ring slot 0: 32-B stores of adjacent pairs
 #pragma unroll
                     for (int d1 = 0; d1 < N; ++d1)
 #pragma unroll
                         for (int d2 = 0; d2 < N; d2 += 2) st2_cs(a.A + b0 + (long long)d1 * a.pw_in[1] + d2, X[d1][d2], X[d1][d2 + 1]);
-                } else if (a.pw_in[1] == 1) {
+                } else if (st_d1) {
 #pragma unroll
                     for (int d1 = 0; d1 < N; d1 += 2)
 #pragma unroll
@@ -1797,13 +1791,24 @@ static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t 
         return cudaGetLastError();
     }
     const size_t dyn = fused3_dyn(BLOCK, ro, PF);
-    if (ro) {
-        cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        k_fused3<SYM, MAP, BLOCK, MINB, PF, true><<<grid, BLOCK, dyn, s>>>(a);
-    } else {
-        cudaFuncSetAttribute(k_fused3<SYM, MAP, BLOCK, MINB, PF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        k_fused3<SYM, MAP, BLOCK, MINB, PF, false><<<grid, BLOCK, dyn, s>>>(a);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        kern<<<grid, BLOCK, dyn, s>>>(a);
+    };
+    // the default TMA variant (lane map 0, 128 threads) gets one instantiation per stage view
+    constexpr bool spec = PF == 2 && MAP == 0 && BLOCK == 128 && MINB == 2;
+    if (spec && a.use_tma == 1) {
+        switch (a.tma_swz) {
+        case 0: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 0 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 0 : -1>); break;
+        case 1: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 1 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 1 : -1>); break;
+        case 2: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 2 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 2 : -1>); break;
+        case 3: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 3 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 3 : -1>); break;
+        default: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 4 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 4 : -1>); break;
+        }
+        return cudaGetLastError();
     }
+    if (ro) go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true>);
+    else go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false>);
     return cudaGetLastError();
 }
 

@@ -64,11 +64,10 @@ struct FusedArgs {
     int rho_accumulate;      // 1: rho[n] += sum (several shard blocks contribute to one step)
     int lane_map;            // k_fused3 lane map (kernels.cu): 1 when tile fibres t, t+1 are adjacent in HBM
     int use_tma;             // k_fused3 (unsharded): rounds staged by TMA through `tmap` (1) or cp.async (2)
-    int tma_last_reader;     // k_fused3 TMA rounds: 1 = the last warp to read the stage issues the next
-                             // round (no CTA barrier per round; slower, kept selectable); 0 = CTA barrier
     long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view (view B: 1)
     int tma_c0m;             // TMA coordinate 0 = tma_c0m x (G mod tma_nA) doubles
-    int tma_swz;             // 1 / 2: view-B / view-C stage (128-B rows, 128-B swizzle; kernels.cu k_fused3)
+    int tma_swz;             // 1 / 2 / 4: view-B / view-C / view-D stage (128-B rows, 128-B swizzle), 3: view D
+                             // with 64-B rows (kernels.cu k_fused3)
     int tma_c1m;             // TMA coordinate 1 = tma_c1m x (G / tma_nA)
     int tma_sf, tma_s[3];    // stage strides (entries) of the round's fibre f and inner digits d0, d1, d2
     int stg_lg[4], stg_s[4], stg_fi, stg_swz;  // cp.async staging (use_tma = 2): fields in HBM order, kernels.cu

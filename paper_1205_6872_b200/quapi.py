@@ -18,7 +18,7 @@ import numpy as np
 from . import workloads as W
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "lib", "libquapi.so")
+SO_PATH = os.environ.get("QUAPI_SO") or os.path.join(_HERE, "lib", "libquapi.so")  # QUAPI_SO: A/B builds
 
 QP_OK, QP_ERR_ARG, QP_ERR_CONFIG, QP_ERR_CAPACITY, QP_ERR_QUADRATURE, QP_ERR_CUDA, QP_ERR_COMM = 0, 1, 2, 3, 4, 6, 7
 QP_J_CALLBACK, QP_J_G_TABLE, QP_J_ETA_TABLE = 4, 5, 6
