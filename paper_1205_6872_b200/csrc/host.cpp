@@ -489,6 +489,8 @@ static EncodeTiledFn encode_tiled() {
 // (the kernel then loads with plain LDG) if the driver cannot encode it.
 // view D (p0 = 0) with the original 64-B rows + 64-B swizzle instead of 128-B rows (QUAPI_VIEWD64=1)
 static bool f3_view_d64() { return std::getenv("QUAPI_VIEWD64") != nullptr; }
+// view C (p0 = L-1) with the original fibre-major row order (2-way bank conflicts; QUAPI_VIEWC_OLD=1)
+static bool f3_view_c_old() { return std::getenv("QUAPI_VIEWC_OLD") != nullptr; }
 
 static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, double2 *A, int F) {
     if (ls.tma_A == A) return true;
@@ -521,7 +523,15 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
         const cuuint64_t gs[4] = {16ull * 64, 16ull * 8, 16ull * 16, 16ull * ipow(P.N, L)};
         const cuuint32_t bx[5] = {16, (cuuint32_t)F, 2, 4, 1};
         std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
-    } else if (ls.tma_a == -2) {  // view C (p0 = L-1): slots 0..L-2 (= d1 + 4 d2 + 16 f) as 128-B rows
+    } else if (ls.tma_a == -2 && !f3_view_c_old()) {  // view C (p0 = L-1): 128-B rows of the 8 entries
+              // (d1, d2 & 1), then f, d2 / 2, d0 = slot L-1; 128-B swizzle.  stage [d0][d2 / 2][f] rows,
+              // 16-B chunk XOR (row & 7): the 8 fibres of a quarter-warp hit 8 distinct chunks
+        if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F) return false;
+        const cuuint64_t gd[5] = {16, (cuuint64_t)ipow(P.N, L - 3), 2, 4, 1};
+        const cuuint64_t gs[4] = {256, 128, 16ull * ipow(P.N, L - 1), 16ull * ipow(P.N, L)};
+        const cuuint32_t bx[5] = {16, (cuuint32_t)F, 2, 4, 1};
+        std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
+    } else if (ls.tma_a == -2) {  // view C, fibre-major rows (p0 = L-1): slots 0..L-2 (= d1 + 4 d2 + 16 f) as 128-B rows
               // (d1, d2 & 1), two rows per fibre, then d0 = slot L-1; 128-B swizzle.  stage [d0][2 f + d2/2][8]
         if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F || 2 * F > 256) return false;
         const cuuint64_t gd[5] = {16, (cuuint64_t)ipow(P.N, L - 1) / 8, 4, 1, 1};
@@ -1057,8 +1067,8 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
                 // view B: c0 = 0, c1 = G / 2 (rows of two fibres); view C: c1 = 2 G (two rows per fibre)
                 a.tma_nA = ls.tma_a > 0 ? ipow(P->N, ls.tma_a) : (ls.tma_a == 0 ? 2 : 1);
                 a.tma_c0m = ls.tma_a > 0 ? 2 : 0;
-                a.tma_c1m = ls.tma_a == -2 ? 2 : 1;
-                a.tma_swz = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? 2 : (f3_view_d64() ? 3 : 4)));
+                a.tma_c1m = (ls.tma_a == -2 && f3_view_c_old()) ? 2 : 1;
+                a.tma_swz = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? (f3_view_c_old() ? 2 : 5) : (f3_view_d64() ? 3 : 4)));
                 if (ls.tma_a > 0) a.tma_sf = 1, a.tma_s[0] = F, a.tma_s[1] = 4 * F, a.tma_s[2] = 16 * F;
                 else a.tma_sf = 4, a.tma_s[0] = 4 * F, a.tma_s[1] = 16 * F, a.tma_s[2] = 1;
             }

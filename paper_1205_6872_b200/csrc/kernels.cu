@@ -1169,7 +1169,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                         } else if (swz == 3) {  // view D, 64-B rows: row r = (d2, d1, f) of the d0 entries
                             const int r = (j * N + d1) * F + fib;
                             X[d1][d0] = stage[r * 4 + (d0 ^ ((r >> 1) & 3))];
-                        } else if (swz == 2) {  // view C: row r of 8 entries (d2 parity, d1)
+                        } else if (swz == 5) {  // view C: 128-B row r = (d0, d2 / 2, f) of entries (d2 & 1, d1)
+                            const int r = (d0 * 2 + (j >> 1)) * F + fib;
+                            X[d1][d0] = stage[r * 8 + ((((j & 1) << 2) | d1) ^ (r & 7))];
+                        } else if (swz == 2) {  // view C, fibre-major rows: row r of 8 entries (d2 parity, d1)
                             const int r = d0 * 2 * F + 2 * fib + (j >> 1);
                             X[d1][d0] = stage[r * 8 + ((((j & 1) << 2) | d1) ^ (r & 7))];
                         } else {
@@ -1276,7 +1279,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 // store path: which inner digit is ring slot 0 follows from the view when VW is fixed
                 // (view B: d2 = slot 0; view C: d1 = slot 0; views A and D: neither)
                 const bool st_d2 = VW >= 0 ? VW == 1 : a.pw_in[2] == 1;
-                const bool st_d1 = VW >= 0 ? VW == 2 : a.pw_in[1] == 1;
+                const bool st_d1 = VW >= 0 ? (VW == 2 || VW == 5) : a.pw_in[1] == 1;
                 if (st_d2) {  // d2 is ring slot 0: 32-B stores of adjacent pairs
 #pragma unroll
                     for (int d1 = 0; d1 < N; ++d1)
@@ -1803,6 +1806,7 @@ static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t 
         case 1: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 1 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 1 : -1>); break;
         case 2: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 2 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 2 : -1>); break;
         case 3: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 3 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 3 : -1>); break;
+        case 5: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 5 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 5 : -1>); break;
         default: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 4 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 4 : -1>); break;
         }
         return cudaGetLastError();

@@ -66,8 +66,8 @@ struct FusedArgs {
     int use_tma;             // k_fused3 (unsharded): rounds staged by TMA through `tmap` (1) or cp.async (2)
     long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view (view B: 1)
     int tma_c0m;             // TMA coordinate 0 = tma_c0m x (G mod tma_nA) doubles
-    int tma_swz;             // 1 / 2 / 4: view-B / view-C / view-D stage (128-B rows, 128-B swizzle), 3: view D
-                             // with 64-B rows (kernels.cu k_fused3)
+    int tma_swz;             // 1 / 5 / 4: view-B / view-C / view-D stage (128-B rows, 128-B swizzle); 2, 3:
+                             // view C fibre-major rows, view D 64-B rows (kernels.cu k_fused3)
     int tma_c1m;             // TMA coordinate 1 = tma_c1m x (G / tma_nA)
     int tma_sf, tma_s[3];    // stage strides (entries) of the round's fibre f and inner digits d0, d1, d2
     int stg_lg[4], stg_s[4], stg_fi, stg_swz;  // cp.async staging (use_tma = 2): fields in HBM order, kernels.cu
