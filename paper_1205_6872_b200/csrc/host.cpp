@@ -335,6 +335,9 @@ struct qp_plan {
         std::vector<double2> Etab;     // [S][2][G][D][X]
         std::vector<long long> goff;   // [G][X]
         std::vector<int2> lofs;        // [T]
+        std::vector<double2> E0r;      // TMA sets: per round of e0r_F fibres [S][2][D][F] factors + F offsets
+        int e0r_F = 0;
+        size_t off_E0r = 0;
         size_t off_inner = 0, off_E = 0, off_goff = 0, off_lofs = 0;
         qp::FusedArgs args{};          // table pointers filled in qp_steps
         // k_fused3 TMA view (-1: none).  View A (1 <= p0 <= L-3): run A = slots 0..tma_a-1 (tma_a = p0),
@@ -677,6 +680,24 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     if (ls.tma_a != -1) {
         const char *e = std::getenv("QUAPI_F3TMAP");
         a.lane_map = (e && e[0] == '1') ? 1 : 0;
+        // per-round contiguous copy of the group-0 factors and offsets (one bulk copy per round)
+        const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2);
+        ls.E0r.clear();
+        ls.e0r_F = 0;
+        if (T % F == 0 && F % 2 == 0 && !std::getenv("QUAPI_E0_SLICES")) {
+            const int R = T / F, Q = S * 2 * D;
+            const size_t blk = (size_t)Q * F + F / 2;
+            ls.E0r.assign((size_t)R * blk, make_double2(0.0, 0.0));
+            for (int rd = 0; rd < R; ++rd) {
+                double2 *b = ls.E0r.data() + rd * blk;
+                for (int q = 0; q < Q; ++q) {  // q = (st, kap, d): Etab[st][kap][g = 0][d][rd F + f]
+                    const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
+                    for (int f = 0; f < F; ++f) b[(size_t)q * F + f] = ls.Etab[((((size_t)st * 2 + kap) * G) * D + d) * X + rd * F + f];
+                }
+                std::memcpy(b + (size_t)Q * F, ls.lofs.data() + (size_t)rd * F, F * sizeof(int2));
+            }
+            ls.e0r_F = F;
+        }
     }
     // cp.async-staged rounds for the remaining slots of k_fused3 (an inner digit is ring slot 0, so no
     // TMA box with slot 0 innermost gives conflict-free stage reads): the round's F fibres are
@@ -725,6 +746,7 @@ void compute_layout(qp_plan &P) {
         ls.off_E = off;     off = align256(off + ls.Etab.size() * sizeof(double2));
         ls.off_goff = off;  off = align256(off + ls.goff.size() * sizeof(long long));
         ls.off_lofs = off;  off = align256(off + ls.lofs.size() * sizeof(int2));
+        ls.off_E0r = off;   off = align256(off + ls.E0r.size() * sizeof(double2));
     };
     for (auto &ls : P.sets) place(ls);
     for (auto &ls : P.sh.sets) place(ls);
@@ -991,6 +1013,8 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
         QP_CUDA(cudaMemcpyAsync(w + ls.off_E, ls.Etab.data(), ls.Etab.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
         QP_CUDA(cudaMemcpyAsync(w + ls.off_goff, ls.goff.data(), ls.goff.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
         QP_CUDA(cudaMemcpyAsync(w + ls.off_lofs, ls.lofs.data(), ls.lofs.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        if (!ls.E0r.empty())
+            QP_CUDA(cudaMemcpyAsync(w + ls.off_E0r, ls.E0r.data(), ls.E0r.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
     }
     QP_CUDA(cudaMemsetAsync(w + P->off_cnt, 0, 256, s));
     std::vector<double2> a0(P->N);
@@ -1071,6 +1095,7 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
                 a.tma_swz = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? (f3_view_c_old() ? 2 : 5) : (f3_view_d64() ? 3 : 4)));
                 if (ls.tma_a > 0) a.tma_sf = 1, a.tma_s[0] = F, a.tma_s[1] = 4 * F, a.tma_s[2] = 16 * F;
                 else a.tma_sf = 4, a.tma_s[0] = 4 * F, a.tma_s[1] = 16 * F, a.tma_s[2] = 1;
+                a.E0r = (ls.e0r_F == F) ? (const double2 *)(w + ls.off_E0r) : nullptr;
             }
             a.inner = (const double2 *)(w + ls.off_inner);
             a.Etab = (const double2 *)(w + ls.off_E);

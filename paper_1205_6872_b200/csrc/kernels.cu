@@ -1062,11 +1062,25 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     if constexpr (PF)
         if (t_begin < t_end) load_unit(t_begin, 0, Xn, lon);
     // TM: one stage; thread 0 issues the TMA box of unit (tau, rd): outer fibres G = tau T + rd F
+    // E0r (TM): the round's factors and offsets are one contiguous block of E0B entries (one bulk copy);
+    // the two buffers then are [2][E0B] over the same shared-memory region
+    constexpr int E0B = S * 2 * D * F + F / 2;
+    const bool e0r = STG && a.E0r != nullptr;
+    auto e0_at = [&](int buf, int q) -> double2 {  // q = (s, kap, d)
+        return e0r ? sE0[buf * E0B + q * F + fib] : sE0[(buf * S * 2 * D + q) * F + fib];
+    };
+    auto lo_at = [&](int buf) -> int2 {
+        return e0r ? reinterpret_cast<const int2 *>(sE0 + buf * E0B + S * 2 * D * F)[fib] : sLo[buf * F + fib];
+    };
     auto tma_issue = [&](int tau, int rd, int buf) {
         const long long G = (long long)tau * a.T + (long long)rd * F;
         fence_proxy_async();
         mbar_expect_tx(&sFull, F * 64 * 16 + S * 2 * D * F * 16 + F * 8);
         tma_load_5d(stage, &a.tmap, &sFull, (int)(a.tma_c0m * (G % a.tma_nA)), (int)(a.tma_c1m * (G / a.tma_nA)));
+        if (e0r) {
+            bulk_g2s(sE0 + buf * E0B, a.E0r + (size_t)rd * E0B, E0B * 16, &sFull);
+            return;
+        }
         for (int q = 0; q < S * 2 * D; ++q) {  // q = (s, kap, d): Etab[s][kap][g = 0][d][t0 ..]
             const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
             bulk_g2s(sE0 + ((size_t)buf * S * 2 * D + q) * F,
@@ -1154,7 +1168,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 mbar_wait(&sFull, phase);
                 cur = phase;
                 phase ^= 1;
-                lo = sLo[cur * F + fib];
+                lo = lo_at(cur);
                 const int swz = VW >= 0 ? VW : a.tma_swz;
 #pragma unroll
                 for (int d1 = 0; d1 < N; ++d1)
@@ -1232,8 +1246,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                 double2 E0[NK][D];  // outer group-0 factor (kap = 1, readout: loaded at the end of the step)
 #pragma unroll
                 for (int d = 0; d < D; ++d) {
-                    E0[0][d] = STG ? sE0[((cur * S + s) * 2 * D + d) * F + fib]
-                                  : __ldg(&a.Etab[((size_t)s * 2 * a.G * D + d) * a.X + t]);
+                    E0[0][d] = STG ? e0_at(cur, s * 2 * D + d) : __ldg(&a.Etab[((size_t)s * 2 * a.G * D + d) * a.X + t]);
                     E0[NK - 1][d] = E0[0][d];
                 }
                 double2 acc[RO ? N : 1];
@@ -1264,7 +1277,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
                         const int c = class_of(M, LAT, n / M, n % M);
                         if (c > 0)
                             acc[RO ? n : 0] =
-                                cmul(STG ? sE0[((cur * S + s) * 2 * D + D + (c > 0 ? c - 1 : 0)) * F + fib]
+                                cmul(STG ? e0_at(cur, s * 2 * D + D + (c > 0 ? c - 1 : 0))
                                         : __ldg(&a.Etab[(((size_t)s * 2 + 1) * a.G * D + (c > 0 ? c - 1 : 0)) * a.X + t]),
                                      acc[RO ? n : 0]);
                     }

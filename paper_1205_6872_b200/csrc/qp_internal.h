@@ -47,6 +47,8 @@ struct FusedArgs {
     const double2 *small;    // SmallLayout block (K', beta)
     const double2 *inner;    // [S][S][2][D][N]: inner-slot factors per sub-step
     const double2 *Etab;     // [S][2][G][D][X]: outer digit-group factor tables per sub-step
+    const double2 *E0r;      // k_fused3 TMA rounds: per round the group-0 factors [S][2][D][F] then the F
+                             // tile-local offsets (int2), contiguous: one bulk copy per round; or nullptr
     const long long *goff;   // [G][X]: address offset of outer digit group g >= 1
     const int2 *lofs;        // [T]: x = address offset of tile-local fibre t, y = 'last' digit of sub-step 0 or -1
     double2 *partials;       // [kMaxS][kPartialsMax][N] readout block partials
