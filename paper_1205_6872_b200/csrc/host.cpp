@@ -801,8 +801,18 @@ void build_tables(qp_plan &P) {
     if (P.kind == 4 && M == 2) P.Smax = std::max(1, std::min(3, L - 1));
     if (const char *ev = std::getenv("QUAPI_FUSE_S")) P.Smax = std::max(1, std::min(P.Smax, std::atoi(ev)));
     P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
-    for (int p0 = 0; p0 < L; ++p0)
-        for (int S = 1; S <= P.Smax; ++S) build_launch_set(P, p0, S, {}, P.sets[(size_t)p0 * P.Smax + (S - 1)]);
+    {  // the L * Smax launch sets are independent (read-only plan, own tables): build them on host threads
+        const int nset = L * P.Smax;
+        const int nth = (int)std::max(1u, std::min<unsigned>((unsigned)nset, std::min(16u, std::thread::hardware_concurrency())));
+        std::atomic<int> next{0};
+        auto worker = [&] {
+            for (int i = next++; i < nset; i = next++) build_launch_set(P, i / P.Smax, i % P.Smax + 1, {}, P.sets[(size_t)i]);
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nth; ++t) pool.emplace_back(worker);
+        worker();
+        for (auto &th : pool) th.join();
+    }
     // ---- A_0(sigma_0) = rho0(sigma_0) I(sigma_0, sigma_0; eta_00 = G(1/2))   (Eq. 13, reading C.3-2)
     P.A0.assign(N, 0.0);
     for (int sg = 0; sg < N; ++sg) P.A0[sg] = P.rho0[sg] * std::exp(dsig(P, sg) * psi(P, sg, P.self_end));
@@ -900,8 +910,16 @@ qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
     for (int i = 0; i < P->M * P->M; ++i) X[i] = cd(0.0, -P->dt) * P->H[i];
     P->U = expm_taylor(X, P->M);
     build_classes(*P);
+    const auto t1 = std::chrono::steady_clock::now();
     if ((st = compute_eta(*P, *pr))) { delete P; return st; }
+    const auto t2 = std::chrono::steady_clock::now();
     build_tables(*P);
+    const auto t3 = std::chrono::steady_clock::now();
+    if (std::getenv("QUAPI_SETUP_TIMES"))
+        std::fprintf(stderr, "qp_plan_create: validate+U %.3f ms, eta %.3f ms, tables %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                     std::chrono::duration<double, std::milli>(t2 - t1).count(),
+                     std::chrono::duration<double, std::milli>(t3 - t2).count());
     P->ardm_entries = ipow(P->N, P->L);
     const double need = 16.0 * double(P->ardm_entries) + double(P->work_bytes);
     if (pr->max_bytes > 0 && need > double(pr->max_bytes)) {
