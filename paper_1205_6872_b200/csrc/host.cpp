@@ -598,24 +598,37 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     auto g_first = [&](int g) { return g == 0 ? 0 : v + (g - 1) * w; };
     auto g_size = [&](int g) { return g == 0 ? v : std::min(w, hi - (g - 1) * w); };
     // outer digit group tables: per sub-step s, kind kap, exponent over the group's digits
+    // entry x of group g is exp(delta_d sum_t psi(digit_t of x; lag of digit t)) = the product of per-digit
+    // factors exp(delta_d psi(digit; lag)) (kap 0: eta of the lag, propagate; kap 1: E of the lag, terminal)
     ls.Etab.assign((size_t)S * 2 * G * D * X, make_double2(1.0, 0.0));
     for (int st = 0; st < S; ++st)
         for (int g = 0; g < G; ++g) {
             const int i0 = g_first(g), nd = g_size(g);
-            for (int x = 0; x < (int)ipow(N, nd); ++x) {
-                cd Ps[2] = {0.0, 0.0};
-                int r = x;
-                for (int t = 0; t < nd; ++t) {
-                    const int dig = r % N;
-                    r /= N;
-                    const int lag = ((p0 + st - outer[i0 + t]) % L + L) % L;  // 1..L-1
-                    Ps[0] += psi(P, dig, P.eta[lag]);  // propagate: partner interior
-                    Ps[1] += psi(P, dig, P.E[lag]);    // terminal (readout) edge class
-                }
-                for (int kap = 0; kap < 2; ++kap)
-                    for (int d = 0; d < D; ++d)
-                        ls.Etab[((((size_t)st * 2 + kap) * G + g) * D + d) * X + x] = d2(std::exp(P.delta[d] * Ps[kap]));
+            std::vector<cd> fac((size_t)2 * D * nd * N);  // [kap][d][t][dig]
+            for (int t = 0; t < nd; ++t) {
+                const int lag = ((p0 + st - outer[i0 + t]) % L + L) % L;  // 1..L-1
+                for (int dig = 0; dig < N; ++dig)
+                    for (int kap = 0; kap < 2; ++kap)
+                        for (int d = 0; d < D; ++d)
+                            fac[(((size_t)kap * D + d) * nd + t) * N + dig] =
+                                std::exp(P.delta[d] * psi(P, dig, kap == 0 ? P.eta[lag] : P.E[lag]));
             }
+            for (int kap = 0; kap < 2; ++kap)
+                for (int d = 0; d < D; ++d) {
+                    const cd *fk = fac.data() + ((size_t)kap * D + d) * nd * N;
+                    double2 *out = ls.Etab.data() + ((((size_t)st * 2 + kap) * G + g) * D + d) * X;
+                    for (int x = 0; x < (int)ipow(N, nd); ++x) {
+                        double er = 1.0, ei = 0.0;  // plain complex products (no __muldc3 special-value path)
+                        int r = x;
+                        for (int t = 0; t < nd; ++t, r /= N) {
+                            const cd f = fk[(size_t)t * N + r % N];
+                            const double nr = er * f.real() - ei * f.imag();
+                            ei = er * f.imag() + ei * f.real();
+                            er = nr;
+                        }
+                        out[x] = make_double2(er, ei);
+                    }
+                }
         }
     // inner-slot factors: sub-step st, inner digit i != st (new value if i < st, old if i > st)
     ls.inner.assign((size_t)S * S * 2 * D * N, make_double2(1.0, 0.0));
