@@ -697,7 +697,8 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
         const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2);
         ls.E0r.clear();
         ls.e0r_F = 0;
-        if (T % F == 0 && F % 2 == 0 && !std::getenv("QUAPI_E0_SLICES")) {
+        // (per-warp staging, F = 8, reads the factors only from E0r: QUAPI_E0_SLICES does not apply)
+        if (T % F == 0 && F % 2 == 0 && (F == 8 || !std::getenv("QUAPI_E0_SLICES"))) {
             const int R = T / F, Q = S * 2 * D;
             const size_t blk = (size_t)Q * F + F / 2;
             ls.E0r.assign((size_t)R * blk, make_double2(0.0, 0.0));

@@ -919,8 +919,11 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const void *tmap, unsigne
 template <bool SYM, int MAP, int BLOCK, int MINB, int PFM, bool RO, int VW = -1>
 __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ FusedArgs a) {
     constexpr int M = 2, N = 4, S = 3, Q = 16, D = 2;
-    constexpr bool PF = PFM == 1, TM = PFM == 2, CA = PFM == 3, STG = TM || CA;
+    // PFM 5 (TW): TMA staging per warp -- each warp's 8 fibres of a round are its own box on its own
+    // mbarrier, refilled by the warp as soon as its lanes have read it (no CTA barrier per round)
+    constexpr bool PF = PFM == 1, TW = PFM == 5, TM = PFM == 2 || TW, CA = PFM == 3, STG = TM || CA;
     constexpr int F = 8 * (BLOCK / 32);  // outer fibres per round
+    constexpr int FS = TW ? 8 : F;       // fibres per TMA box / stage read pattern
     constexpr int NK = RO ? 2 : 1;
     constexpr int W = BLOCK / 32;
     constexpr bool LAT = false;
@@ -941,7 +944,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     double2 *sE0 = dyn_smem_raw + (STG ? F * 64 : 0);
     int2 *sLo = reinterpret_cast<int2 *>(sE0 + (STG ? 2 * S * 2 * D * F : 0));
     double2 *dyn_smem = sE0 + (STG ? 2 * S * 2 * D * F + F : 0);
-    __shared__ __align__(8) unsigned long long sFull;
+    __shared__ __align__(8) unsigned long long sFullW[TW ? BLOCK / 32 : 1];
+    unsigned long long &sFull = sFullW[TW ? (threadIdx.x >> 5) : 0];
     auto accS = reinterpret_cast<double2(*)[RO ? N : 1][RO ? BLOCK : 1]>(dyn_smem + W * 16 * 8);
     for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
     for (int i = threadIdx.x; i < S * S * 2 * D * N; i += BLOCK) (&sIn[0][0][0][0][0])[i] = a.inner[i];
@@ -1064,21 +1068,26 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     // TM: one stage; thread 0 issues the TMA box of unit (tau, rd): outer fibres G = tau T + rd F
     // E0r (TM): the round's factors and offsets are one contiguous block of E0B entries (one bulk copy);
     // the two buffers then are [2][E0B] over the same shared-memory region
-    constexpr int E0B = S * 2 * D * F + F / 2;
-    const bool e0r = STG && a.E0r != nullptr;
+    // TW: E0r blocks are per (round, warp) of FS = 8 fibres; warp w's two buffers at sE0 + 2 w E0B
+    constexpr int E0B = S * 2 * D * FS + FS / 2;
+    const bool e0r = TW || (STG && a.E0r != nullptr);
+    const int sfib = TW ? (lane & 7) : fib;  // fibre index within the stage / E0 block
+    double2 *const sE0w = TW ? sE0 + (size_t)warp * 2 * E0B : sE0;
+    double2 *const stg = TW ? stage + (size_t)warp * FS * 64 : stage;
     auto e0_at = [&](int buf, int q) -> double2 {  // q = (s, kap, d)
-        return e0r ? sE0[buf * E0B + q * F + fib] : sE0[(buf * S * 2 * D + q) * F + fib];
+        return e0r ? sE0w[buf * E0B + q * FS + sfib] : sE0[(buf * S * 2 * D + q) * F + fib];
     };
     auto lo_at = [&](int buf) -> int2 {
-        return e0r ? reinterpret_cast<const int2 *>(sE0 + buf * E0B + S * 2 * D * F)[fib] : sLo[buf * F + fib];
+        return e0r ? reinterpret_cast<const int2 *>(sE0w + buf * E0B + S * 2 * D * FS)[sfib] : sLo[buf * F + fib];
     };
     auto tma_issue = [&](int tau, int rd, int buf) {
-        const long long G = (long long)tau * a.T + (long long)rd * F;
+        const int rw = TW ? rd * (BLOCK / 32) + warp : rd;  // TW: the warp's 8-fibre unit of round rd
+        const long long G = (long long)tau * a.T + (long long)rw * FS;
         fence_proxy_async();
-        mbar_expect_tx(&sFull, F * 64 * 16 + S * 2 * D * F * 16 + F * 8);
-        tma_load_5d(stage, &a.tmap, &sFull, (int)(a.tma_c0m * (G % a.tma_nA)), (int)(a.tma_c1m * (G / a.tma_nA)));
+        mbar_expect_tx(&sFull, FS * 64 * 16 + S * 2 * D * FS * 16 + FS * 8);
+        tma_load_5d(stg, &a.tmap, &sFull, (int)(a.tma_c0m * (G % a.tma_nA)), (int)(a.tma_c1m * (G / a.tma_nA)));
         if (e0r) {
-            bulk_g2s(sE0 + buf * E0B, a.E0r + (size_t)rd * E0B, E0B * 16, &sFull);
+            bulk_g2s(sE0w + buf * E0B, a.E0r + (size_t)rw * E0B, E0B * 16, &sFull);
             return;
         }
         for (int q = 0; q < S * 2 * D; ++q) {  // q = (s, kap, d): Etab[s][kap][g = 0][d][t0 ..]
@@ -1120,12 +1129,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
     if constexpr (CA)
         if (t_begin < t_end) ca_issue(t_begin, 0, 0);
     if constexpr (TM) {
-        if (threadIdx.x == 0) {
+        if (TW ? lane == 0 : threadIdx.x == 0) {
             mbar_init(&sFull, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
-        if (threadIdx.x == 0 && t_begin < t_end) tma_issue(t_begin, 0, 0);
+        if ((TW ? lane == 0 : threadIdx.x == 0) && t_begin < t_end) tma_issue(t_begin, 0, 0);
     }
 
     for (int tau = t_begin; tau < t_end; ++tau) {
@@ -1175,27 +1184,32 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
 #pragma unroll
                     for (int d0 = 0; d0 < N; ++d0) {
                         if (swz == 1) {  // view B: row r of 8 entries (fibre parity, d2); chunk XOR (r & 7)
-                            const int r = (d1 * N + d0) * (F / 2) + (fib >> 1);
-                            X[d1][d0] = stage[r * 8 + ((((fib & 1) << 2) | j) ^ (r & 7))];
+                            const int r = (d1 * N + d0) * (FS / 2) + (sfib >> 1);
+                            X[d1][d0] = stg[r * 8 + ((((sfib & 1) << 2) | j) ^ (r & 7))];
                         } else if (swz == 4) {  // view D: 128-B row r = (d2, d1 / 2, f) of entries (d1 & 1, d0)
-                            const int r = (j * 2 + (d1 >> 1)) * F + fib;
-                            X[d1][d0] = stage[r * 8 + ((((d1 & 1) << 2) | d0) ^ (r & 7))];
+                            const int r = (j * 2 + (d1 >> 1)) * FS + sfib;
+                            X[d1][d0] = stg[r * 8 + ((((d1 & 1) << 2) | d0) ^ (r & 7))];
                         } else if (swz == 3) {  // view D, 64-B rows: row r = (d2, d1, f) of the d0 entries
-                            const int r = (j * N + d1) * F + fib;
-                            X[d1][d0] = stage[r * 4 + (d0 ^ ((r >> 1) & 3))];
+                            const int r = (j * N + d1) * FS + sfib;
+                            X[d1][d0] = stg[r * 4 + (d0 ^ ((r >> 1) & 3))];
                         } else if (swz == 5) {  // view C: 128-B row r = (d0, d2 / 2, f) of entries (d2 & 1, d1)
-                            const int r = (d0 * 2 + (j >> 1)) * F + fib;
-                            X[d1][d0] = stage[r * 8 + ((((j & 1) << 2) | d1) ^ (r & 7))];
+                            const int r = (d0 * 2 + (j >> 1)) * FS + sfib;
+                            X[d1][d0] = stg[r * 8 + ((((j & 1) << 2) | d1) ^ (r & 7))];
                         } else if (swz == 2) {  // view C, fibre-major rows: row r of 8 entries (d2 parity, d1)
-                            const int r = d0 * 2 * F + 2 * fib + (j >> 1);
-                            X[d1][d0] = stage[r * 8 + ((((j & 1) << 2) | d1) ^ (r & 7))];
+                            const int r = d0 * 2 * FS + 2 * sfib + (j >> 1);
+                            X[d1][d0] = stg[r * 8 + ((((j & 1) << 2) | d1) ^ (r & 7))];
                         } else {
-                            X[d1][d0] = stage[fib * a.tma_sf + d0 * a.tma_s[0] + d1 * a.tma_s[1] + j * a.tma_s[2]];
+                            X[d1][d0] = stg[sfib * a.tma_sf + d0 * a.tma_s[0] + d1 * a.tma_s[1] + j * a.tma_s[2]];
                         }
                     }
-                __syncthreads();  // stage free: refill it with the next unit
                 const int rn = rd + 1 < rounds ? rd + 1 : 0, taun = rd + 1 < rounds ? tau : tau + 1;
-                if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
+                if constexpr (TW) {
+                    __syncwarp();  // the warp's stage is free: refill it with the warp's next unit
+                    if (lane == 0 && taun < t_end) tma_issue(taun, rn, phase);
+                } else {
+                    __syncthreads();  // stage free: refill it with the next unit
+                    if (threadIdx.x == 0 && taun < t_end) tma_issue(taun, rn, phase);
+                }
             } else if constexpr (CA) {  // the stage holds this unit (copied one unit ago)
                 cp_async_wait<0>();
                 __syncthreads();
@@ -1636,10 +1650,12 @@ static int eff_kind(int M, int S, int kind) { return kind == 4 ? ((M == 2 && S =
 #define QP_F3_CFGS(X)                                                                              \
     X(0, 0, 256, 2, 0) X(1, 0, 192, 2, 0) X(2, 0, 128, 3, 0) X(3, 1, 128, 3, 0) X(4, 1, 256, 1, 0) \
     X(5, 1, 384, 1, 0) X(6, 1, 128, 2, 1) X(7, 3, 128, 2, 2) X(8, 3, 256, 1, 2) X(9, 2, 128, 2, 2)              \
-    X(10, 2, 256, 1, 2) X(11, 4, 128, 2, 3) X(12, 2, 256, 2, 4) X(13, 2, 128, 4, 4)
+    X(10, 2, 256, 1, 2) X(11, 4, 128, 2, 3) X(12, 2, 256, 2, 4) X(13, 2, 128, 4, 4) X(14, 2, 128, 2, 5)
 static int f3_mode(const FusedArgs &a) { return a.use_tma == 2 ? 4 : (a.lane_map & 1) + (a.use_tma ? 2 : 0); }
 static int f3_variant(int mode, bool view_a = true) {
-    const int def = mode == 0 ? 1 : (mode == 1 ? 3 : (mode == 2 ? 9 : (mode == 3 ? 7 : 11)));
+    // mode 2 (TMA, lane map 0): per-warp staging (14) -- measured 1.917-1.946 vs 1.988-2.001 ms mean
+    // launch on cfg3 for the CTA-wide stage (9, QUAPI_F3=9)
+    const int def = mode == 0 ? 1 : (mode == 1 ? 3 : (mode == 2 ? 14 : (mode == 3 ? 7 : 11)));
     const char *e = std::getenv("QUAPI_F3");
     if (!e) return def;
     const int v = std::atoi(e);
@@ -1651,7 +1667,7 @@ static int f3_variant(int mode, bool view_a = true) {
 }
 int fused3_round_fibres(int mode) {
     const int v = f3_variant(mode);
-#define X(I, MD, B, MB, PM) if (v == I) return PM == 4 ? 32 : B / 4;
+#define X(I, MD, B, MB, PM) if (v == I) return PM == 4 ? 32 : (PM == 5 ? 8 : B / 4);
     QP_F3_CFGS(X)
 #undef X
     return 32;
@@ -1812,7 +1828,7 @@ static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t 
         kern<<<grid, BLOCK, dyn, s>>>(a);
     };
     // the default TMA variant (lane map 0, 128 threads) gets one instantiation per stage view
-    constexpr bool spec = PF == 2 && MAP == 0 && BLOCK == 128 && MINB == 2;
+    constexpr bool spec = (PF == 2 || PF == 5) && MAP == 0 && BLOCK == 128 && MINB == 2;
     if (spec && a.use_tma == 1) {
         switch (a.tma_swz) {
         case 0: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 0 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 0 : -1>); break;

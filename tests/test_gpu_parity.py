@@ -235,7 +235,7 @@ def test_fusion_grouping_independent_of_segments():
                                  {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "1"}, {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "0"},
                                  {"QUAPI_F3": "0"}, {"QUAPI_F3": "2"}, {"QUAPI_F3": "6"}, {"QUAPI_F3": "10"},
                                  {"QUAPI_CA": "1"}, {"QUAPI_F3": "12"}, {"QUAPI_F3": "12", "QUAPI_NO_VIEWB": "1"},
-                                 {"QUAPI_VIEWD64": "1"}, {"QUAPI_VIEWC_OLD": "1"}, {"QUAPI_E0_SLICES": "1"}])
+                                 {"QUAPI_VIEWD64": "1"}, {"QUAPI_VIEWC_OLD": "1"}, {"QUAPI_E0_SLICES": "1"}, {"QUAPI_F3": "9"}, {"QUAPI_F3": "9", "QUAPI_E0_SLICES": "1"}, {"QUAPI_VIEWD64": "1", "QUAPI_VIEWC_OLD": "1"}])
 @pytest.mark.parametrize("L,n", [(8, 37), (9, 30)])
 def test_fused3_load_paths(env, L, n, monkeypatch):
     """k_fused3's load paths (TMA-staged rounds in views A and B, plain loads in lane maps 0 and 1,
