@@ -694,7 +694,7 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
         const char *e = std::getenv("QUAPI_F3TMAP");
         a.lane_map = (e && e[0] == '1') ? 1 : 0;
         // per-round contiguous copy of the group-0 factors and offsets (one bulk copy per round)
-        const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2);
+        const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2, ls.tma_a > 0);
         ls.E0r.clear();
         ls.e0r_F = 0;
         // (per-warp staging, F = 8, reads the factors only from E0r: QUAPI_E0_SLICES does not apply)
@@ -1115,10 +1115,10 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             a.small = small;
             a.use_tma = ls.stg_ca ? 2 : 0;
             if (ls.tma_a != -1 && P->kind == 4 && S == 3 &&
-                encode_f3_tmap(*P, ls, A, qp::fused3_round_fibres((a.lane_map & 1) + 2))) {
+                encode_f3_tmap(*P, ls, A, qp::fused3_round_fibres((a.lane_map & 1) + 2, ls.tma_a > 0))) {
                 a.use_tma = 1;
                 a.tmap = ls.tmap;
-                const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2);
+                const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2, ls.tma_a > 0);
                 // TMA box coordinates of round G: c0 = tma_c0m (G mod tma_nA), c1 = G / tma_nA
                 // view B: c0 = 0, c1 = G / 2 (rows of two fibres); view C: c1 = 2 G (two rows per fibre)
                 a.tma_nA = ls.tma_a > 0 ? ipow(P->N, ls.tma_a) : (ls.tma_a == 0 ? 2 : 1);

@@ -1665,8 +1665,8 @@ static int f3_variant(int mode, bool view_a = true) {
 #undef X
     return def;
 }
-int fused3_round_fibres(int mode) {
-    const int v = f3_variant(mode);
+int fused3_round_fibres(int mode, bool view_a) {
+    const int v = f3_variant(mode, view_a);  // the variant launch_fused will pick for this launch set
 #define X(I, MD, B, MB, PM) if (v == I) return PM == 4 ? 32 : (PM == 5 ? 8 : B / 4);
     QP_F3_CFGS(X)
 #undef X

@@ -127,7 +127,9 @@ int fused_block(int M, int S, int kind);
 // Launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool readout, int grid, cudaStream_t s);
 // mode (k_fused3): lane map + 2 x TMA staging; 4 = cp.async staging (lane map 0)
-int fused3_round_fibres(int mode);  // outer fibres per round (BLOCK / 4) of the mode's k_fused3 variant
+// outer fibres per TMA box / round of the k_fused3 variant launch_fused picks for the mode (view_a: the
+// launch set's TMA view is view A, FusedArgs::tma_sf == 1)
+int fused3_round_fibres(int mode, bool view_a = true);
 int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int mode = 0);  // resident CTAs per SM (needs a device)
 cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaStream_t s);
 
