@@ -1088,14 +1088,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
         tma_load_5d(stg, &a.tmap, &sFull, (int)(a.tma_c0m * (G % a.tma_nA)), (int)(a.tma_c1m * (G / a.tma_nA)));
         if (e0r) {
             bulk_g2s(sE0w + buf * E0B, a.E0r + (size_t)rw * E0B, E0B * 16, &sFull);
-            return;
+        } else if constexpr (!TW) {  // per-slice copies: q = (s, kap, d): Etab[s][kap][g = 0][d][t0 ..]
+            for (int q = 0; q < S * 2 * D; ++q) {
+                const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
+                bulk_g2s(sE0 + ((size_t)buf * S * 2 * D + q) * F,
+                         a.Etab + ((((size_t)st * 2 + kap) * a.G) * D + d) * a.X + rd * F, F * 16, &sFull);
+            }
+            bulk_g2s(sLo + buf * F, a.lofs + rd * F, F * 8, &sFull);
         }
-        for (int q = 0; q < S * 2 * D; ++q) {  // q = (s, kap, d): Etab[s][kap][g = 0][d][t0 ..]
-            const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
-            bulk_g2s(sE0 + ((size_t)buf * S * 2 * D + q) * F,
-                     a.Etab + ((((size_t)st * 2 + kap) * a.G) * D + d) * a.X + rd * F, F * 16, &sFull);
-        }
-        bulk_g2s(sLo + buf * F, a.lofs + rd * F, F * 8, &sFull);
     };
     // CA: every thread copies 16-B chunks of the round with cp.async: chunk q enumerates the round in
     // HBM order (fields sorted by stride: a.stg_lg[i] = log2 radix, a.stg_g[i] global stride, a.stg_s[i]
