@@ -1828,7 +1828,9 @@ static cudaError_t fused3_t(const FusedArgs &a, bool ro, int grid, cudaStream_t 
         kern<<<grid, BLOCK, dyn, s>>>(a);
     };
     // the default TMA variant (lane map 0, 128 threads) gets one instantiation per stage view
-    constexpr bool spec = (PF == 2 || PF == 5) && MAP == 0 && BLOCK == 128 && MINB == 2;
+    // (the default per-warp variant only: instantiating the CTA-stage variant per view as well costs a
+    // minute of build time for a non-default path)
+    constexpr bool spec = PF == 5 && MAP == 0 && BLOCK == 128 && MINB == 2;
     if (spec && a.use_tma == 1) {
         switch (a.tma_swz) {
         case 0: ro ? go(k_fused3<SYM, MAP, BLOCK, MINB, PF, true, spec ? 0 : -1>) : go(k_fused3<SYM, MAP, BLOCK, MINB, PF, false, spec ? 0 : -1>); break;
