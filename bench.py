@@ -103,7 +103,7 @@ def cpu_baseline(cfg: int, max_slide: int = 3):
     import oracle as O
     from paper_1205_6872_b200 import workloads as W
     w = W.CONFIGS[cfg]
-    n = w.L + max_slide - 1
+    n = w.L + max_slide  # steps L..L+max_slide contract: >= max_slide timed slide steps whatever the count convention
     p = O.Problem(s=w.s, H=w.H, rho0=w.rho0, kind=w.kind, coupling=w.coupling, omega_c=w.omega_c,
                   kT=w.kT, dt=w.dt, n_steps=n, L=w.L)
     cores = os.cpu_count() or 1
