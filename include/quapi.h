@@ -80,12 +80,27 @@ typedef struct {
     const qp_c64 *G_in;      /* QP_J_G_TABLE only: [2*dkmax+3] values G(m dt/2)                 */
     double dt;               /* time step > 0                                                    */
     int64_t n_steps;         /* N_t >= 0: last time index; t = n_steps * dt                     */
-    int32_t dkmax;           /* L = Delta k_max >= 1                                             */
+    int32_t dkmax;           /* L = Delta k_max, 2 <= L <= 40 (N^L <= 4e12 entries)              */
     const int64_t *out_steps;/* sorted unique step indices in [0, n_steps]; NULL => all         */
-    int64_t n_out;           /* length of out_steps (ignored when out_steps == NULL)            */
-    int64_t max_bytes;       /* capacity budget for ARDM + workspace; 0 => no budget check      */
+    int64_t n_out;           /* length of out_steps, >= 0 (ignored when out_steps == NULL)      */
+    int64_t max_bytes;       /* capacity budget for ARDM + workspace: > 0 => this many bytes;
+                                0 => the free memory of the current CUDA device at plan creation
+                                (no check when no device is visible); < 0 => no check           */
     const qp_c64 *eta_in;    /* QP_J_ETA_TABLE only: [3*dkmax+2] eta classes, qp_plan_eta order   */
+    int32_t fuse_steps;      /* cap on the time steps fused into one pass over the ARDM, 0..3;
+                                0 => the library's choice (3 for M = 2, 1 for M = 3, 4).  Results
+                                agree to rounding for every choice.                              */
+    uint32_t flags;          /* QP_FLAG_* below; 0 for the default plan                          */
 } qp_problem;
+
+/* Plan options (qp_problem.flags).  They select among equivalent kernel paths (same result to
+   rounding) and exist for testing and measurement:
+   QP_FLAG_NO_TMA           -- M = 2, 3 fused steps: plain loads instead of the per-warp TMA-staged
+                               rounds;
+   QP_FLAG_GENERIC_MOMENTS  -- M = 2, s = (+s, -s): the generic per-class moments instead of the
+                               symmetric four-sum moments. */
+#define QP_FLAG_NO_TMA 1u
+#define QP_FLAG_GENERIC_MOMENTS 2u
 
 typedef struct qp_plan qp_plan;
 
@@ -105,6 +120,7 @@ typedef struct {
     double setup_seconds;    /* host time spent in qp_plan_create (validation, U, eta, tables)  */
     int64_t init_h2d_bytes;  /* bytes qp_init copies host->device (tables, A_0, rho(0))         */
     int32_t fuse_steps;      /* time steps fused into one pass over the ARDM (slide kernel)      */
+    double setup_ms[3];      /* host setup phases: validate + U, eta quadrature, factor tables    */
 } qp_sizes;
 
 /* Host only (no GPU needed): validate (a1), U = e^{-iH dt} and the pair propagator K (a2),
@@ -121,21 +137,30 @@ qp_status qp_plan_eta(const qp_plan *plan, qp_c64 *out, int64_t cap);
 /* U = e^{-iH dt} [M*M] as used by the plan. */
 qp_status qp_plan_propagator(const qp_plan *plan, qp_c64 *U_out);
 
-/* Enqueue: copy the plan's tables into d_work (H2D) and write A_0 into d_ardm.
-   d_ardm: >= ardm_bytes, 16-byte aligned; d_work: >= work_bytes, 256-byte aligned. */
+/* Enqueue: copy the plan's tables into d_work (H2D) and write A_0 into d_ardm:
+   A_0(sigma_0) = rho0(sigma_0) I(sigma_0, sigma_0; eta_00)  -- the k = 0 term of Eq. 8
+   with the end-point self class of Eq. 13 (reading C.3-2); rho(t_0) = rho0 (reading C.3-8).
+   d_ardm: >= ardm_bytes, 16-byte aligned; d_work: >= work_bytes, 256-byte aligned.  Both device,
+   caller-owned.  Errors: QP_ERR_ARG (NULL / misaligned), QP_ERR_CUDA. */
 qp_status qp_init(qp_plan *plan, void *d_ardm, void *d_work, void *stream);
-/* Enqueue time steps k = k_begin .. k_end-1 (1 <= k_begin <= k_end <= n_steps+1): step k turns
-   A_{k-1} into A_k in place (growth for k < L, slide for k >= L) and, when k is an output step,
-   reduces rho(t_k) from A_{k-1} in the same pass (fused readout).  Slide steps are fused in
-   groups of fuse_steps (aligned on k - L) into one kernel launch, i.e. one pass over the ARDM.
-   Steps must be enqueued in order after qp_init.  Returns the number of kernels launched in
-   *n_launch (may be NULL). */
+/* Enqueue time steps k = k_begin .. k_end-1 (1 <= k_begin <= k_end <= n_steps+1) of the iterative
+   tensor propagator -- the evaluation of Eq. 8 with the influence functional of Eq. 9
+    by propagating the augmented reduced density matrix (Makri-Makarov), the
+   propagation the paper's GPU program runs with BSXFUN.  Step k turns
+   A_{k-1} into A_k in place (growth for k < L: the tensor gains digit k; slide for k >= L: the
+   oldest point sigma_{k-L} is summed out) and, when k is an output step, reduces rho(t_k) from
+   A_{k-1} in the same pass -- the summation the paper times separately ("line 169").
+   Slide steps are fused in groups of fuse_steps (aligned on k - L) into one kernel launch, i.e.
+   one pass over the ARDM.  Steps must be enqueued in order after qp_init.  Returns the number of
+   kernels launched in *n_launch (may be NULL).  Errors: QP_ERR_ARG (order, NULL), QP_ERR_CUDA. */
 qp_status qp_steps(qp_plan *plan, int64_t k_begin, int64_t k_end, void *d_ardm, void *d_work, void *stream,
                    int64_t *n_launch);
-/* [sync] Copy every requested rho(t_k) to the host: rho_out[n_out][M][M].  Outputs whose step
-   has not been enqueued yet are undefined. */
+/* [sync] Copy every requested rho(t_k) to the host: rho_out[n_out][M][M] (caller-owned, row-major),
+   the paper's output "at all time points or just the final one" (allPointsOrJustFinalPoint,
+   P:444-449, generalised to a list).  Outputs whose step has not been enqueued yet are undefined. */
 qp_status qp_read_rho(const qp_plan *plan, const void *d_work, qp_c64 *rho_out, void *stream);
-/* [sync] Whole run: qp_init + qp_steps(1, n_steps+1) + qp_read_rho. */
+/* [sync] Whole run -- the paper's program from its inputs to rho(t) at the
+   requested times: qp_init + qp_steps(1, n_steps+1) + qp_read_rho. */
 qp_status qp_run(qp_plan *plan, void *d_ardm, void *d_work, void *stream, qp_c64 *rho_out);
 
 /* ---------------------------------------------------------------- sharded execution (multi-GPU)

@@ -11,8 +11,6 @@
 //   out[new] = K'(new, last) exp(Ds(new) Psi(mid)) sum_old exp(Ds(new) psi_L(old)) a[old]
 // with the Eq. 9 exponents evaluated directly from the per-lag psi tables (Psi = sum over the kept
 // partners, one complex exp per Delta-s class), so no per-launch-set factor tables are needed.
-#include <cstdlib>
-
 #include "qp_internal.h"
 
 namespace qp {
@@ -326,13 +324,11 @@ template <int M>
 cudaError_t batch_t(const BatchArgs &a, int B, cudaStream_t s) {
     const size_t tab = batch_dyn_smem(M, a.L, a.D);
     const size_t full = tab + (size_t)a.NL * sizeof(double2);
-    const bool smem = full <= kBatchSmemArdmMax && !std::getenv("QUAPI_BATCH_GLOBAL");
+    const bool smem = full <= kBatchSmemArdmMax;
     // M = 2: 3 CTAs (24 warps, 80 registers) per SM for the shared-memory-resident ARDM, 2 CTAs (128
     // registers, no spills) when the ARDM stays in global memory (measured: L = 5 13.8 vs 15.0 ms, L = 7
-    // 0.198 vs 0.177 s for 1024 problems x 1000 steps); QUAPI_BATCH_MINB=2|3 overrides
-    const char *mb = std::getenv("QUAPI_BATCH_MINB");
-    const bool three = mb ? mb[0] == '3' : smem;
-    if (M == 2 && three)
+    // 0.198 vs 0.177 s for 1024 problems x 1000 steps)
+    if (M == 2 && smem)
         return smem ? batch_launch<M, true, 3>(a, B, full, s) : batch_launch<M, false, 3>(a, B, tab, s);
     return smem ? batch_launch<M, true, M == 2 ? 2 : 1>(a, B, full, s) : batch_launch<M, false, M == 2 ? 2 : 1>(a, B, tab, s);
 }

@@ -316,7 +316,7 @@ struct qp_plan {
     int M = 0, N = 0, L = 0, D = 0;
     bool lattice = false;        // class map used by the kernels
     bool sym = false;            // M = 2 with s = (+s, -s): symmetric-moment kernel
-    int kind = 1;                // fused kernel variant: 1 = register super-fibre where available, 0 = warp-mapped
+    uint32_t flags = 0;          // qp_problem.flags (QP_FLAG_*)
     double dt = 0.0;
     int64_t n_steps = 0;
     std::vector<int64_t> out_steps;
@@ -344,17 +344,19 @@ struct qp_plan {
         // run B = the tma_b slots above the inner ones.  View B (p0 = L-2, tma_a = 0): inner digit 2 is
         // slot 0 and the outer slots 1..L-3 are one run.
         int tma_a = -1, tma_b = 0;
-        bool stg_ca = false;           // cp.async-staged rounds (p0 = 0, L-2, L-1; see build_launch_set)
         mutable const void *tma_A = nullptr;  // ARDM pointer the cached tensor map was encoded for
         mutable CUtensorMap tmap{};
     };
-    qp::FusedShape shape{};
+    int group_w = 1;                   // digits per outer digit group (g >= 1) of the factor tables
     int Smax = 1;
     std::vector<LaunchSet> sets;       // index p0 * Smax + (S - 1)
     size_t off_small = 0, off_part = 0, off_rho = 0, off_cnt = 0, tables_end = 0, work_bytes = 0;
     int64_t ardm_entries = 0;
     int grid[qp::kMaxS + 1] = {0};
-    int occ[qp::kMaxS + 1][5] = {};    // resident CTAs per SM of the fused kernel per (S, k_fused3 mode)
+    int block = 0;
+    double setup_ms[3] = {0, 0, 0};    // validate + U, eta, tables (qp_sizes)
+    int64_t max_bytes = 0;             // qp_problem.max_bytes (capacity budget)
+    int occ[qp::kMaxS + 1][3] = {};    // resident CTAs per SM of the slide kernel per (S, load path)
     int sms = 0;
     int64_t next_k = 1;
     bool inited = false;
@@ -403,7 +405,7 @@ void build_classes(qp_plan &P) {
             if (std::fabs(P.s[a] - (P.s[0] + a * u)) > 1e-15 * std::max(1.0, std::fabs(P.s[a]))) lat = false;
     }
     P.lattice = lat;
-    P.sym = (M == 2) && P.s[0] == -P.s[1] && P.s[0] != 0.0 && !std::getenv("QUAPI_NO_SYM");
+    P.sym = (M == 2) && P.s[0] == -P.s[1] && P.s[0] != 0.0 && !(P.flags & QP_FLAG_GENERIC_MOMENTS);
     P.D = qp::n_classes(M, lat);
     P.delta.assign(P.D, 0.0);
     for (int a = 0; a < M; ++a)
@@ -490,17 +492,11 @@ static EncodeTiledFn encode_tiled() {
 // k_fused3's TMA view of the ARDM for launch set ls: 5-D tensor of FP64 (run A as 2 x N^a doubles,
 // run B, inner d0, d1, d2), box = one round of F outer fibres x N^3 inner entries.  Returns false
 // (the kernel then loads with plain LDG) if the driver cannot encode it.
-// view D (p0 = 0) with the original 64-B rows + 64-B swizzle instead of 128-B rows (QUAPI_VIEWD64=1)
-static bool f3_view_d64() { return std::getenv("QUAPI_VIEWD64") != nullptr; }
-// view C (p0 = L-1) with the original fibre-major row order (2-way bank conflicts; QUAPI_VIEWC_OLD=1)
-static bool f3_view_c_old() { return std::getenv("QUAPI_VIEWC_OLD") != nullptr; }
-
 static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, double2 *A, int F) {
     if (ls.tma_A == A) return true;
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return false;
     const int p0 = ls.p0, L = P.L;
-    const bool d64 = f3_view_d64();
     cuuint64_t gdim[5], gstr[4];
     cuuint32_t box[5];
     if (ls.tma_a > 0) {  // view A: (run A as doubles, run B, d0, d1, d2); stage [d2][d1][d0][f]
@@ -512,13 +508,6 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
                                   16ull * ipow(P.N, p0 + 2)};
         const cuuint32_t bx[5] = {(cuuint32_t)(2 * boxA), (cuuint32_t)(F / boxA), 4, 4, 4};
         std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
-    } else if (ls.tma_a == -3 && d64) {  // view D, 64-B rows (p0 = 0): (d0 = slot 0 as doubles, f, d1, d2),
-              // 64-B swizzle.  stage [d2][d1][f] rows of the 4 d0 entries, chunk XOR ((row >> 1) & 3)
-        if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F) return false;
-        const cuuint64_t gd[5] = {8, (cuuint64_t)ipow(P.N, L - 3), 4, 4, 1};
-        const cuuint64_t gs[4] = {16ull * 64, 16ull * 4, 16ull * 16, 16ull * ipow(P.N, L)};
-        const cuuint32_t bx[5] = {8, (cuuint32_t)F, 4, 4, 1};
-        std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
     } else if (ls.tma_a == -3) {  // view D (p0 = 0): 128-B rows of the 8 entries (d1 & 1, d0), then f,
               // d1 / 2, d2; 128-B swizzle.  stage [d2][d1 / 2][f] rows, 16-B chunk XOR (row & 7)
         if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F) return false;
@@ -526,20 +515,13 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
         const cuuint64_t gs[4] = {16ull * 64, 16ull * 8, 16ull * 16, 16ull * ipow(P.N, L)};
         const cuuint32_t bx[5] = {16, (cuuint32_t)F, 2, 4, 1};
         std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
-    } else if (ls.tma_a == -2 && !f3_view_c_old()) {  // view C (p0 = L-1): 128-B rows of the 8 entries
+    } else if (ls.tma_a == -2) {  // view C (p0 = L-1): 128-B rows of the 8 entries
               // (d1, d2 & 1), then f, d2 / 2, d0 = slot L-1; 128-B swizzle.  stage [d0][d2 / 2][f] rows,
               // 16-B chunk XOR (row & 7): the 8 fibres of a quarter-warp hit 8 distinct chunks
         if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F) return false;
         const cuuint64_t gd[5] = {16, (cuuint64_t)ipow(P.N, L - 3), 2, 4, 1};
         const cuuint64_t gs[4] = {256, 128, 16ull * ipow(P.N, L - 1), 16ull * ipow(P.N, L)};
         const cuuint32_t bx[5] = {16, (cuuint32_t)F, 2, 4, 1};
-        std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
-    } else if (ls.tma_a == -2) {  // view C, fibre-major rows (p0 = L-1): slots 0..L-2 (= d1 + 4 d2 + 16 f) as 128-B rows
-              // (d1, d2 & 1), two rows per fibre, then d0 = slot L-1; 128-B swizzle.  stage [d0][2 f + d2/2][8]
-        if ((cuuint64_t)ipow(P.N, L - 3) < (cuuint64_t)F || 2 * F > 256) return false;
-        const cuuint64_t gd[5] = {16, (cuuint64_t)ipow(P.N, L - 1) / 8, 4, 1, 1};
-        const cuuint64_t gs[4] = {128, 16ull * ipow(P.N, L - 1), 16ull * ipow(P.N, L), 16ull * ipow(P.N, L)};
-        const cuuint32_t bx[5] = {16, (cuuint32_t)(2 * F), 4, 1, 1};
         std::copy(gd, gd + 5, gdim), std::copy(gs, gs + 4, gstr), std::copy(bx, bx + 5, box);
     } else {  // view B: slots 0..L-3 (= d2 + 4 f) as 128-B rows of two fibres, d0, d1; 128-B swizzle.
               // stage [d1][d0][f/2] rows of 8 entries (f & 1, d2), 16-B chunk XOR (row & 7)
@@ -551,7 +533,7 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
     }
     const cuuint32_t es[5] = {1, 1, 1, 1, 1};
     if (enc(&ls.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)A, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            ls.tma_a > 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : (ls.tma_a == -3 && d64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
+            ls.tma_a > 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
@@ -561,11 +543,20 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
 
 // Persistent grid of one fused launch: fixed per (plan, launch set, device type), so the readout
 // order (block partials) is deterministic.
+static int slide_path(int S, const qp::FusedArgs &a) { return S == 3 ? (a.use_tma ? 2 : (a.lane_map & 1)) : 0; }
+static int slide_occupancy(const qp_plan &P, int S, int path) {
+    if (P.M == 2 && S == 3) return qp::fused3_occupancy(P.sym, path & 1, path == 2);
+    return qp::fused_r_occupancy(P.M, P.lattice, P.sym, S);
+}
 static int launch_grid(qp_plan *P, int S, const qp::FusedArgs &a) {
-    const int mode = a.use_tma == 2 ? 4 : (a.lane_map & 1) + (a.use_tma ? 2 : 0);
-    int &o = P->occ[S][mode];
-    if (o == 0) o = std::max(1, qp::fused_occupancy(P->M, P->lattice, P->sym, P->kind, S, mode));
+    const int path = slide_path(S, a);
+    int &o = P->occ[S][path];
+    if (o == 0) o = std::max(1, slide_occupancy(*P, S, path));
     return std::max(1, std::min<int>({a.n_tiles, P->sms * o, qp::kPartialsMax}));
+}
+static cudaError_t launch_slide(const qp_plan &P, int S, const qp::FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    if (P.M == 2 && S == 3) return qp::launch_fused3(P.sym, a, ro, grid, s);
+    return qp::launch_fused_r(P.M, P.lattice, P.sym, S, a, ro, grid, s);
 }
 
 // Tables of one fused launch over inner slots p0..p0+S-1 (mod L) of a local layout from which the
@@ -586,10 +577,11 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     const int nout = (int)outer.size();
     // tile digits: the kernel's preferred v, lowered (not below its minimum) so that small problems
     // still have >= ~2 tiles per SM of a 148-SM B200 to spread over the persistent grid
-    int v = std::min(qp::fused_tile_digits(M, S, P.kind), nout);
-    const int vmin = std::min(qp::fused_tile_digits_min(M, S, P.kind), nout);
+    const bool f3 = (M == 2 && S == 3);
+    int v = std::min(f3 ? qp::kFused3TileDigits : qp::fused_r_tile_digits(M, S), nout);
+    const int vmin = std::min(f3 ? qp::kFused3TileDigitsMin : (N >= 9 ? 2 : 3), nout);
     while (v > vmin && std::pow((double)N, nout - v) < 2.0 * 148) --v;
-    const int w = std::max(1, P.shape.w);
+    const int w = std::max(1, P.group_w);
     const int hi = nout - v;
     const int G = 1 + (hi + w - 1) / w;
     const int T = (int)ipow(N, v);
@@ -675,76 +667,40 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     }
     a.last_div = (ilast >= v && ilast < nout) ? (int)ipow(N, ilast - v) : -1;
     a.fixed_last = -1;  // set per launch when sub-step 0's 'last' slot is a shard slot
-    // k_fused3 lane map 1 (32 consecutive fibres per warp load) when fibres t, t+1 are adjacent
+    // k_fused3 plain loads: lane map 1 (32 consecutive fibres per warp load) when fibres t, t+1 are adjacent
     a.lane_map = (T >= 64 && ls.lofs[1].x == 1) ? 1 : 0;
-    if (const char *e = std::getenv("QUAPI_F3MAP")) a.lane_map = (e[0] == '1' && T >= 64) ? 1 : 0;
-    // TMA staging (k_fused3, unsharded, lane map 1 with slot 0 the lowest outer slot): the outer
-    // slots are two runs of consecutive slots, A = 0 .. p0-1 and B = p0+3 .. L-1
-    ls.tma_a = -1;  // (-1: no TMA view; 0: view B; -2: view C; -3: view D)
-    if (P.kind == 4 && M == 2 && S == 3 && removed.empty() && T >= 64 && !std::getenv("QUAPI_NO_TMA")) {
+    // per-warp TMA staging (k_fused3, unsharded): the view follows from where ring slot 0 sits.
+    // View A: slot 0 is the lowest outer slot, the outer slots are two runs of consecutive slots,
+    // A = 0 .. p0-1 and B = p0+3 .. L-1; views B/C/D: inner digit 2/1/0 is slot 0 (p0 = L-2/L-1/0)
+    ls.tma_a = -1;  // (-1: no TMA view; > 0: view A; 0: view B; -2: view C; -3: view D)
+    if (f3 && removed.empty() && T >= 64 && !(P.flags & QP_FLAG_NO_TMA)) {
         if (a.lane_map == 1 && p0 >= 1 && p0 + S <= L) ls.tma_a = p0, ls.tma_b = L - p0 - S;
-        else if (p0 == L - 2 && L >= 6 && !std::getenv("QUAPI_NO_VIEWB")) ls.tma_a = 0, ls.tma_b = 0;
-        else if (p0 == L - 1 && L >= 6 && !std::getenv("QUAPI_NO_VIEWC")) ls.tma_a = -2, ls.tma_b = 0;
-        else if (p0 == 0 && L >= 6 && !std::getenv("QUAPI_NO_VIEWD")) ls.tma_a = -3, ls.tma_b = 0;
+        else if (p0 == L - 2 && L >= 6) ls.tma_a = 0, ls.tma_b = 0;
+        else if (p0 == L - 1 && L >= 6) ls.tma_a = -2, ls.tma_b = 0;
+        else if (p0 == 0 && L >= 6) ls.tma_a = -3, ls.tma_b = 0;
     }
-    // TMA-staged sets read the stage with lane map 0 by default (quarters of a super-fibre in one warp:
-    // the digit transpose needs no CTA barrier); QUAPI_F3TMAP=1 selects map 1.  If the tensor map
-    // cannot be encoded the launch falls back to plain loads with this lane map.
+    ls.E0r.clear();
+    ls.e0r_F = 0;
     if (ls.tma_a != -1) {
-        const char *e = std::getenv("QUAPI_F3TMAP");
-        a.lane_map = (e && e[0] == '1') ? 1 : 0;
-        // per-round contiguous copy of the group-0 factors and offsets (one bulk copy per round)
-        const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2, ls.tma_a > 0);
-        ls.E0r.clear();
-        ls.e0r_F = 0;
-        // (per-warp staging, F = 8, reads the factors only from E0r: QUAPI_E0_SLICES does not apply)
-        if (T % F == 0 && F % 2 == 0 && (F == 8 || !std::getenv("QUAPI_E0_SLICES"))) {
-            const int R = T / F, Q = S * 2 * D;
-            const size_t blk = (size_t)Q * F + F / 2;
-            ls.E0r.assign((size_t)R * blk, make_double2(0.0, 0.0));
-            for (int rd = 0; rd < R; ++rd) {
-                double2 *b = ls.E0r.data() + rd * blk;
-                for (int q = 0; q < Q; ++q) {  // q = (st, kap, d): Etab[st][kap][g = 0][d][rd F + f]
-                    const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
-                    for (int f = 0; f < F; ++f) b[(size_t)q * F + f] = ls.Etab[((((size_t)st * 2 + kap) * G) * D + d) * X + rd * F + f];
-                }
-                std::memcpy(b + (size_t)Q * F, ls.lofs.data() + (size_t)rd * F, F * sizeof(int2));
+        // the stage is read with lane map 0 (the quarters of a super-fibre in one warp); per (round, warp)
+        // unit of F = 8 fibres one contiguous block of the group-0 factors [S][2][D][F] and the F
+        // tile-local offsets (one bulk copy per unit)
+        a.lane_map = 0;
+        const int F = 8;
+        const int R = T / F, Q = S * 2 * D;
+        const size_t blk = (size_t)Q * F + F / 2;
+        ls.E0r.assign((size_t)R * blk, make_double2(0.0, 0.0));
+        for (int rd = 0; rd < R; ++rd) {
+            double2 *b = ls.E0r.data() + rd * blk;
+            for (int q = 0; q < Q; ++q) {  // q = (st, kap, d): Etab[st][kap][g = 0][d][rd F + f]
+                const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
+                for (int f = 0; f < F; ++f) b[(size_t)q * F + f] = ls.Etab[((((size_t)st * 2 + kap) * G) * D + d) * X + rd * F + f];
             }
-            ls.e0r_F = F;
+            std::memcpy(b + (size_t)Q * F, ls.lofs.data() + (size_t)rd * F, F * sizeof(int2));
         }
+        ls.e0r_F = F;
     }
-    // cp.async-staged rounds for the remaining slots of k_fused3 (an inner digit is ring slot 0, so no
-    // TMA box with slot 0 innermost gives conflict-free stage reads): the round's F fibres are
-    // uniformly strided (the lowest outer slots are consecutive); the copy walks the round in HBM
-    // order and the stage keeps that order, XOR-swizzled by fibre when fibres are >= 8 units apart.
-    ls.stg_ca = false;
     a.use_tma = 0;
-    // Off by default: measured slower than plain 32-B loads on cfg3 (p0 = 0 / 12 / 13: 3.13 / 2.92 /
-    // 2.95 ms vs 2.93 / 2.43 / 2.62 ms); QUAPI_CA=1 enables it.
-    if (P.kind == 4 && M == 2 && S == 3 && removed.empty() && T >= 64 && ls.tma_a == -1 && std::getenv("QUAPI_CA")) {
-        const int F = qp::fused3_round_fibres(4);
-        const long long sfib = ipow(N, pos[outer[0]]);
-        bool uniform = true;  // fibres 0..F-1 of a round at stride sfib
-        for (int f = 0; f < F && uniform; ++f) uniform = ls.lofs[f].x == (long long)f * sfib;
-        if (uniform && T % F == 0) {
-            struct Fld { long long g; int lg, id; };
-            Fld fl[4] = {{a.pw_in[0], 2, 0}, {a.pw_in[1], 2, 1}, {a.pw_in[2], 2, 2}, {sfib, 0, 3}};
-            for (int lgF = 1; (1 << lgF) <= F; ++lgF) fl[3].lg = lgF;
-            std::sort(fl, fl + 4, [](const Fld &x, const Fld &y) { return x.g < y.g; });
-            int sst = 1, sf = 0, sd[3] = {0, 0, 0};
-            for (int i = 0; i < 4; ++i) {
-                a.stg_lg[i] = fl[i].lg;
-                a.stg_g[i] = fl[i].g;
-                a.stg_s[i] = sst;
-                if (fl[i].id == 3) a.stg_fi = i, sf = sst; else sd[fl[i].id] = sst;
-                sst <<= fl[i].lg;
-            }
-            a.tma_sf = sf, a.tma_s[0] = sd[0], a.tma_s[1] = sd[1], a.tma_s[2] = sd[2];
-            a.stg_swz = (sf % 8 == 0) ? 1 : 0;
-            ls.stg_ca = true;
-            a.lane_map = 0;
-        }
-    }
     for (int st = 0; st < qp::kMaxS; ++st)
         for (int kap = 0; kap < 2; ++kap)
             for (int d = 0; d < qp::kMaxD; ++d) a.fixfac[st][kap][d] = make_double2(1.0, 0.0);
@@ -771,7 +727,7 @@ void compute_layout(qp_plan &P) {
     P.work_bytes = off;
 }
 
-void build_tables(qp_plan &P) {
+void build_tables(qp_plan &P, int fuse_cap) {
     const int N = P.N, M = P.M, L = P.L, D = P.D;
     // ---- K and self-factor-weighted K'
     P.K.assign(N * N, 0.0);
@@ -807,13 +763,11 @@ void build_tables(qp_plan &P) {
         }
     // ---- fused launch sets: for every start slot p0 and fusion depth S, the super-fibres of the
     //      inner slots p0..p0+S-1 and the factor / address tables of the L-S outer slots
-    P.shape = qp::fused_shape(M);
-    // default: three fused steps per pass for M = 2 (k_fused3), else the register kernel
-    P.kind = (M == 2) ? 4 : 1;
-    if (const char *ek = std::getenv("QUAPI_FUSED_KIND")) P.kind = (ek[0] == 'w') ? 0 : (ek[0] == 'a' ? 2 : (ek[0] == 's' ? 3 : (ek[0] == '3' ? 4 : 1)));
-    P.Smax = std::max(1, std::min(P.shape.S, L - 1));
-    if (P.kind == 4 && M == 2) P.Smax = std::max(1, std::min(3, L - 1));
-    if (const char *ev = std::getenv("QUAPI_FUSE_S")) P.Smax = std::max(1, std::min(P.Smax, std::atoi(ev)));
+    // fusion depth: three steps per pass for M = 2 (k_fused3), one for M = 3, 4 (k_fused_r); the
+    // caller may cap it (qp_problem.fuse_steps)
+    P.group_w = (M == 2) ? 4 : (M == 3 ? 3 : 2);
+    P.Smax = std::max(1, std::min(M == 2 ? 3 : 1, L - 1));
+    if (fuse_cap > 0) P.Smax = std::min(P.Smax, fuse_cap);
     P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
     {  // the L * Smax launch sets are independent (read-only plan, own tables): build them on host threads
         const int nset = L * P.Smax;
@@ -831,6 +785,29 @@ void build_tables(qp_plan &P) {
     P.A0.assign(N, 0.0);
     for (int sg = 0; sg < N; ++sg) P.A0[sg] = P.rho0[sg] * std::exp(dsig(P, sg) * psi(P, sg, P.self_end));
     compute_layout(P);
+}
+
+// Capacity (a1): need bytes against the caller's budget (max_bytes > 0), or against the free memory
+// of the current CUDA device (max_bytes == 0; no check when no device is visible), or no check
+// (max_bytes < 0).
+qp_status check_capacity(int64_t max_bytes, double need, const char *what) {
+    double budget = -1.0;
+    const char *src = "budget";
+    if (max_bytes > 0) {
+        budget = (double)max_bytes;
+    } else if (max_bytes == 0) {
+        int n = 0;
+        size_t fr = 0, tot = 0;
+        if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+            budget = (double)fr;
+            src = "free device memory";
+        } else {
+            cudaGetLastError();  // no device visible: nothing to check against
+        }
+    }
+    if (budget >= 0.0 && need > budget)
+        return err(QP_ERR_CAPACITY, "capacity: need %.0f B (%s) > %s %.0f B", need, what, src, budget);
+    return QP_OK;
 }
 
 qp_status validate(const qp_problem *pr) {
@@ -877,7 +854,11 @@ qp_status validate(const qp_problem *pr) {
         break;
     default: return err(QP_ERR_CONFIG, "config: unknown bath kind %d", pr->kind);
     }
+    if (pr->fuse_steps < 0 || pr->fuse_steps > 3) return err(QP_ERR_CONFIG, "config: fuse_steps must be in [0, 3] (got %d)", pr->fuse_steps);
+    if (pr->flags & ~(uint32_t)(QP_FLAG_NO_TMA | QP_FLAG_GENERIC_MOMENTS))
+        return err(QP_ERR_CONFIG, "config: unknown flags 0x%x", pr->flags);
     if (pr->out_steps) {
+        if (pr->n_out < 0) return err(QP_ERR_CONFIG, "config: n_out must be >= 0 (got %lld)", (long long)pr->n_out);
         for (int64_t o = 0; o < pr->n_out; ++o) {
             const int64_t k = pr->out_steps[o];
             if (k < 0 || k > pr->n_steps || (o > 0 && k <= pr->out_steps[o - 1]))
@@ -911,6 +892,7 @@ qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
     P->L = pr->dkmax;
     P->dt = pr->dt;
     P->n_steps = pr->n_steps;
+    P->flags = pr->flags;
     if (pr->out_steps) P->out_steps.assign(pr->out_steps, pr->out_steps + pr->n_out);
     else for (int64_t k = 0; k <= pr->n_steps; ++k) P->out_steps.push_back(k);
     P->s.assign(pr->s, pr->s + P->M);
@@ -927,19 +909,17 @@ qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
     const auto t1 = std::chrono::steady_clock::now();
     if ((st = compute_eta(*P, *pr))) { delete P; return st; }
     const auto t2 = std::chrono::steady_clock::now();
-    build_tables(*P);
+    build_tables(*P, pr->fuse_steps);
     const auto t3 = std::chrono::steady_clock::now();
-    if (std::getenv("QUAPI_SETUP_TIMES"))
-        std::fprintf(stderr, "qp_plan_create: validate+U %.3f ms, eta %.3f ms, tables %.3f ms\n",
-                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                     std::chrono::duration<double, std::milli>(t2 - t1).count(),
-                     std::chrono::duration<double, std::milli>(t3 - t2).count());
+    P->setup_ms[0] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    P->setup_ms[1] = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    P->setup_ms[2] = std::chrono::duration<double, std::milli>(t3 - t2).count();
     P->ardm_entries = ipow(P->N, P->L);
+    P->max_bytes = pr->max_bytes;
     const double need = 16.0 * double(P->ardm_entries) + double(P->work_bytes);
-    if (pr->max_bytes > 0 && need > double(pr->max_bytes)) {
+    if ((st = check_capacity(pr->max_bytes, need, "ARDM + workspace"))) {
         delete P;
-        return err(QP_ERR_CAPACITY, "capacity: need %.0f B (ARDM %.0f B + workspace) > budget %lld B", need,
-                   16.0 * std::pow(double(pr->M * pr->M), pr->dkmax), (long long)pr->max_bytes);
+        return st;
     }
     P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = P;
@@ -961,10 +941,11 @@ qp_status qp_plan_query(const qp_plan *P, qp_sizes *o) {
     o->lattice = P->lattice;
     o->n_classes = P->D;
     o->grid = P->grid[P->Smax];
-    o->block = qp::fused_block(P->M, P->Smax, P->kind);
+    o->block = P->block;
     o->tile_fibres = P->sets.empty() ? 0 : P->sets[(size_t)P->Smax - 1].args.T;
     o->fuse_steps = P->Smax;
     o->setup_seconds = P->setup_seconds;
+    for (int i = 0; i < 3; ++i) o->setup_ms[i] = P->setup_ms[i];
     o->init_h2d_bytes = (int64_t)(P->tables_end + 2 * P->N * sizeof(double2));
     return QP_OK;
 }
@@ -1061,11 +1042,13 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
     }
     // the host vectors above are pageable: cudaMemcpyAsync from pageable memory returns after the
     // source has been staged, so they may go out of scope.
-    // persistent slide grid: fixed per (plan, device type) => deterministic readout order
-    for (int S = 1; S <= P->Smax; ++S) {
-        const int occ = std::max(1, qp::fused_occupancy(P->M, P->lattice, P->sym, P->kind, S));
-        const int nt = P->sets[(size_t)S - 1].args.n_tiles;  // same for every p0
-        P->grid[S] = std::max(1, std::min<int>({nt, P->sms * occ, qp::kPartialsMax}));
+    // persistent slide grid of the launch set p0 = 1 (the common view-A path for M = 2), for qp_plan_query
+    {
+        const qp_plan::LaunchSet &ls = P->sets[(size_t)std::min(1, P->L - 1) * P->Smax + P->Smax - 1];
+        qp::FusedArgs a = ls.args;
+        a.use_tma = ls.tma_a != -1;
+        P->grid[P->Smax] = launch_grid(P, P->Smax, a);
+        P->block = (P->M == 2 && P->Smax == 3) ? qp::fused3_block(a.lane_map, a.use_tma) : qp::fused_r_block(P->M, P->Smax);
     }
     P->next_k = 1;
     P->sh.seg = 0;
@@ -1113,21 +1096,16 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             qp::FusedArgs a = ls.args;
             a.A = A;
             a.small = small;
-            a.use_tma = ls.stg_ca ? 2 : 0;
-            if (ls.tma_a != -1 && P->kind == 4 && S == 3 &&
-                encode_f3_tmap(*P, ls, A, qp::fused3_round_fibres((a.lane_map & 1) + 2, ls.tma_a > 0))) {
+            a.use_tma = 0;
+            if (ls.tma_a != -1 && S == 3 && encode_f3_tmap(*P, ls, A, ls.e0r_F)) {
                 a.use_tma = 1;
                 a.tmap = ls.tmap;
-                const int F = qp::fused3_round_fibres((a.lane_map & 1) + 2, ls.tma_a > 0);
-                // TMA box coordinates of round G: c0 = tma_c0m (G mod tma_nA), c1 = G / tma_nA
-                // view B: c0 = 0, c1 = G / 2 (rows of two fibres); view C: c1 = 2 G (two rows per fibre)
+                // TMA box coordinates of unit G (first outer fibre): c0 = tma_c0m (G mod tma_nA), c1 = G / tma_nA
+                // (view A: run A as doubles; view B: rows of two fibres; views C, D: one fibre per row group)
                 a.tma_nA = ls.tma_a > 0 ? ipow(P->N, ls.tma_a) : (ls.tma_a == 0 ? 2 : 1);
                 a.tma_c0m = ls.tma_a > 0 ? 2 : 0;
-                a.tma_c1m = (ls.tma_a == -2 && f3_view_c_old()) ? 2 : 1;
-                a.tma_swz = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? (f3_view_c_old() ? 2 : 5) : (f3_view_d64() ? 3 : 4)));
-                if (ls.tma_a > 0) a.tma_sf = 1, a.tma_s[0] = F, a.tma_s[1] = 4 * F, a.tma_s[2] = 16 * F;
-                else a.tma_sf = 4, a.tma_s[0] = 4 * F, a.tma_s[1] = 16 * F, a.tma_s[2] = 1;
-                a.E0r = (ls.e0r_F == F) ? (const double2 *)(w + ls.off_E0r) : nullptr;
+                a.tma_view = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? 2 : 3));
+                a.E0r = (const double2 *)(w + ls.off_E0r);
             }
             a.inner = (const double2 *)(w + ls.off_inner);
             a.Etab = (const double2 *)(w + ls.off_E);
@@ -1154,7 +1132,7 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
                     }
                 }
             }
-            e = qp::launch_fused(P->M, P->lattice, P->sym, P->kind, S, a, ro, launch_grid(P, S, a), s);
+            e = launch_slide(*P, S, a, ro, launch_grid(P, S, a), s);
             adv = S;
         }
         if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
@@ -1213,6 +1191,7 @@ extern "C" {
 qp_status qp_shard_configure(qp_plan *P, int32_t n_ranks, int32_t rank) {
     if (!P) return err(QP_ERR_ARG, "arg: NULL plan");
     if (n_ranks < 2 || rank < 0 || rank >= n_ranks) return err(QP_ERR_ARG, "arg: need n_ranks >= 2 and 0 <= rank < n_ranks");
+    if (P->inited || P->sh.on) return err(QP_ERR_ARG, "arg: qp_shard_configure must be called once, before qp_init");
     const int L = P->L, N = P->N;
     // smallest z with at most 10% load imbalance of the N^z combos over the ranks
     // (segments need 2z <= L - 1 so that consecutive shard-slot sets are disjoint); else the smallest
@@ -1442,7 +1421,7 @@ qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_loc
             a.fixed_last = -1;
             for (int i = 0; i < sh.z; ++i)
                 if (Z[i] == qlast) a.fixed_last = dig[i];
-            const cudaError_t e = qp::launch_fused(P->M, P->lattice, P->sym, P->kind, S, a, ro, launch_grid(P, S, a), s);
+            const cudaError_t e = launch_slide(*P, S, a, ro, launch_grid(P, S, a), s);
             if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: shard launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
             ++launched;
         }

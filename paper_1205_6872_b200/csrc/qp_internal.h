@@ -1,5 +1,5 @@
 // qp_internal.h -- structures shared by the host setup (host.cpp) and the sm_100a kernels
-// (kernels.cu).  Not part of the public ABI (include/quapi.h).
+// (slide_r.cu, slide3.cu, grow.cu, batch.cu, eta.cu).  Not part of the public ABI (include/quapi.h).
 #pragma once
 #include <cuda.h>  // CUtensorMap (the encode entry point is fetched at run time; no -lcuda)
 #include <cuda_runtime.h>
@@ -64,16 +64,11 @@ struct FusedArgs {
     int last_div;            // sub-step 0 'last' digit is a tile digit: (tau / last_div) % N; else -1
     int fixed_last;          // sub-step 0 'last' slot is a (fixed) shard slot: its value; else -1
     int rho_accumulate;      // 1: rho[n] += sum (several shard blocks contribute to one step)
-    int lane_map;            // k_fused3 lane map (kernels.cu): 1 when tile fibres t, t+1 are adjacent in HBM
-    int use_tma;             // k_fused3 (unsharded): rounds staged by TMA through `tmap` (1) or cp.async (2)
-    long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view (view B: 1)
-    int tma_c0m;             // TMA coordinate 0 = tma_c0m x (G mod tma_nA) doubles
-    int tma_swz;             // 1 / 5 / 4: view-B / view-C / view-D stage (128-B rows, 128-B swizzle); 2, 3:
-                             // view C fibre-major rows, view D 64-B rows (kernels.cu k_fused3)
-    int tma_c1m;             // TMA coordinate 1 = tma_c1m x (G / tma_nA)
-    int tma_sf, tma_s[3];    // stage strides (entries) of the round's fibre f and inner digits d0, d1, d2
-    int stg_lg[4], stg_s[4], stg_fi, stg_swz;  // cp.async staging (use_tma = 2): fields in HBM order, kernels.cu
-    long long stg_g[4];
+    int lane_map;            // k_fused3 plain loads: 1 when tile fibres t, t+1 are adjacent in HBM (slide3.cu)
+    int use_tma;             // k_fused3: rounds staged per warp by TMA through `tmap` (unsharded launch sets)
+    int tma_view;            // k_fused3 stage view: 0 = A, 1 = B, 2 = C, 3 = D (slide3.cu, host.cpp encode_f3_tmap)
+    long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view (view B: 2, views C/D: 1)
+    int tma_c0m;             // TMA coordinate 0 = tma_c0m x (G mod tma_nA) doubles, coordinate 1 = G / tma_nA
     alignas(64) CUtensorMap tmap;
     int var[kMaxS];          // beta variant per sub-step: 1 for the first slide step k == L (initial-edge
                              // classes of the partner sigma_0), else 0 (SmallLayout::beta)
@@ -83,12 +78,8 @@ struct FusedArgs {
     double2 fixfac[kMaxS][2][kMaxD];
 };
 
-// Fused-kernel shape for one M: max fused steps and outer digit-group size w.
-struct FusedShape {
-    int S, w;
-};
 
-// Generic digit-permutation copy for the re-shard (kernels.cu: k_permute).
+// Generic digit-permutation copy for the re-shard (grow.cu: k_permute).
 constexpr int kMaxFields = kMaxL + 4;
 struct PermuteArgs {
     double2 *dst;
@@ -116,22 +107,20 @@ struct GrowArgs {
     int L;
     double delta[kMaxD];     // Delta s of each class (index d-1)
 };
-
-FusedShape fused_shape(int M);
-// kind: 0 = warp-mapped k_fused, 1 = register k_fused_r, 2 = k_fused_r with cp.async staging
-// (kinds 1/2 where a config exists for (M, S), else the warp-mapped kernel)
-bool has_reg_variant(int M, int S, int kind);
-int fused_tile_digits(int M, int S, int kind);      // preferred v: T = N^v outer fibres per tile
-int fused_tile_digits_min(int M, int S, int kind);  // smallest v the kernel supports
-int fused_block(int M, int S, int kind);
-// Launchers (kernels.cu).  Return cudaError_t of the launch.
-cudaError_t launch_fused(int M, bool lattice, bool sym, int kind, int S, const FusedArgs &a, bool readout, int grid, cudaStream_t s);
-// mode (k_fused3): lane map + 2 x TMA staging; 4 = cp.async staging (lane map 0)
-// outer fibres per TMA box / round of the k_fused3 variant launch_fused picks for the mode (view_a: the
-// launch set's TMA view is view A, FusedArgs::tma_sf == 1)
-int fused3_round_fibres(int mode, bool view_a = true);
-int fused_occupancy(int M, bool lattice, bool sym, int kind, int S, int mode = 0);  // resident CTAs per SM (needs a device)
 cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaStream_t s);
+
+// Slide kernels.  k_fused_r (slide_r.cu): S <= 2 steps per pass, one thread per super-fibre, for
+// (M, S) in {(2,1), (2,2), (3,1), (4,1)}.  k_fused3 (slide3.cu): M = 2, S = 3.
+bool fused_r_has(int M, int S);
+int fused_r_tile_digits(int M, int S);   // preferred v: T = N^v outer fibres per tile
+int fused_r_block(int M, int S);
+int fused_r_occupancy(int M, bool lattice, bool sym, int S);  // resident CTAs per SM (needs a device)
+cudaError_t launch_fused_r(int M, bool lattice, bool sym, int S, const FusedArgs &a, bool ro, int grid, cudaStream_t s);
+constexpr int kFused3TileDigits = 5, kFused3TileDigitsMin = 3;  // a round is 8 fibres x W warps
+int fused3_block(int lane_map, bool tma);
+int fused3_round_fibres(int lane_map, bool tma);  // outer fibres per round (8 per warp)
+int fused3_occupancy(bool sym, int lane_map, bool tma);
+cudaError_t launch_fused3(bool sym, const FusedArgs &a, bool ro, int grid, cudaStream_t s);
 
 // Batched sweeps (batch.cu): B independent problems, one CTA each, every step in one launch.
 // Table image (double2 entries) at `tab`: psi_eta[L+1][N], psi_E[L+1][N], psi_TI[L+1][N] (lag j = 1..L;

@@ -18,10 +18,11 @@ import numpy as np
 from . import workloads as W
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.environ.get("QUAPI_SO") or os.path.join(_HERE, "lib", "libquapi.so")  # QUAPI_SO: A/B builds
+SO_PATH = os.path.join(_HERE, "lib", "libquapi.so")
 
 QP_OK, QP_ERR_ARG, QP_ERR_CONFIG, QP_ERR_CAPACITY, QP_ERR_QUADRATURE, QP_ERR_CUDA, QP_ERR_COMM = 0, 1, 2, 3, 4, 6, 7
 QP_J_CALLBACK, QP_J_G_TABLE, QP_J_ETA_TABLE = 4, 5, 6
+QP_FLAG_NO_TMA, QP_FLAG_GENERIC_MOMENTS = 1, 2  # qp_problem.flags
 
 _JFUNC = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
 
@@ -51,6 +52,8 @@ class qp_problem(ctypes.Structure):
         ("n_out", ctypes.c_int64),
         ("max_bytes", ctypes.c_int64),
         ("eta_in", ctypes.POINTER(qp_c64)),
+        ("fuse_steps", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
     ]
 
 
@@ -67,6 +70,7 @@ class qp_sizes(ctypes.Structure):
         ("bytes_per_step", ctypes.c_int64), ("lattice", ctypes.c_int32), ("n_classes", ctypes.c_int32),
         ("grid", ctypes.c_int32), ("block", ctypes.c_int32), ("tile_fibres", ctypes.c_int32),
         ("setup_seconds", ctypes.c_double), ("init_h2d_bytes", ctypes.c_int64), ("fuse_steps", ctypes.c_int32),
+        ("setup_ms", ctypes.c_double * 3),
     ]
 
 
@@ -199,10 +203,11 @@ class Sizes:
     setup_seconds: float
     init_h2d_bytes: int
     fuse_steps: int
+    setup_ms: tuple  # host setup phases (ms): validate + U, eta quadrature, factor tables
 
 
 def _problem(w: W.Workload, keep: list, out_steps=None, J=None, J_cutoff: float = 0.0, G_in=None,
-             max_bytes: int = 0, eta_in=None) -> qp_problem:
+             max_bytes: int = 0, eta_in=None, fuse_steps: int = 0, flags: int = 0) -> qp_problem:
     """Marshal a Workload into a ``qp_problem`` (host arrays kept alive in ``keep``)."""
     s = np.ascontiguousarray(w.s, dtype=np.float64)
     H, rho0 = _c64_array(w.H), _c64_array(w.rho0)
@@ -234,6 +239,7 @@ def _problem(w: W.Workload, keep: list, out_steps=None, J=None, J_cutoff: float 
         pr.out_steps = o.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
         pr.n_out = len(o)
     pr.max_bytes = int(max_bytes)
+    pr.fuse_steps, pr.flags = int(fuse_steps), int(flags)
     return pr
 
 
@@ -243,9 +249,10 @@ class Plan:
     def __init__(self, w: W.Workload, out_steps: Optional[Sequence[int]] = None,
                  J: Optional[Callable[[float], float]] = None, J_cutoff: float = 0.0,
                  G_in: Optional[np.ndarray] = None, max_bytes: int = 0, eta_in: Optional[np.ndarray] = None,
-                 eta_setup: str = "host"):
+                 eta_setup: str = "host", fuse_steps: int = 0, flags: int = 0):
         """``eta_setup="device"``: the eta classes (host-setup step a3) come from ``eta_device`` on the
-        current CUDA device instead of the host quadrature (analytic bath families only)."""
+        current CUDA device instead of the host quadrature (analytic bath families only).
+        ``fuse_steps`` / ``flags``: plan options of ``qp_problem`` (include/quapi.h)."""
         L = lib()
         self.w = w
         self._keep = []
@@ -253,7 +260,7 @@ class Plan:
             eta_in = eta_device([bath_of(w)], w.dt, w.L)[0]
         elif eta_setup not in ("host", "device"):
             raise ValueError(f"eta_setup must be 'host' or 'device', got {eta_setup!r}")
-        pr = _problem(w, self._keep, out_steps, J, J_cutoff, G_in, max_bytes, eta_in)
+        pr = _problem(w, self._keep, out_steps, J, J_cutoff, G_in, max_bytes, eta_in, fuse_steps, flags)
         h = ctypes.c_void_p()
         _check(L.qp_plan_create(ctypes.byref(pr), ctypes.byref(h)))
         self._h = h
@@ -270,7 +277,9 @@ class Plan:
     def sizes(self) -> Sizes:
         o = qp_sizes()
         _check(lib().qp_plan_query(self._h, ctypes.byref(o)))
-        return Sizes(*(getattr(o, f) for f, _ in qp_sizes._fields_))
+        v = [getattr(o, f) for f, _ in qp_sizes._fields_]
+        v[-1] = tuple(v[-1])
+        return Sizes(*v)
 
     def eta(self) -> dict:
         Lm = self.w.L

@@ -116,43 +116,10 @@ def test_step_segments_equal_whole_run():
 
 
 # ----------------------------------------------------------------------------- full BASELINE sizes
-def test_cfg3_full_size_parity_with_oracle():
-    """Config 3 at its full size (4^14 entries, the bench workload and launch configuration):
-    every rho(t_k) for k <= L + 6 against the oracle (which holds 2 x 4.3 GB on the host)."""
-    w = W.CONFIGS[3].with_(n_steps=W.CONFIGS[3].L + 6)
-    rg, plan, _ = gpu_run(w)
-    ro = O.run(P(w))
-    check(rg, ro)
-    assert plan.sizes.ardm_entries == 4 ** 14
-
-
-@pytest.mark.slow
-def test_cfg4_full_size_parity_with_oracle():
-    w = W.CONFIGS[4].with_(n_steps=W.CONFIGS[4].L + 3)
-    rg, _, _ = gpu_run(w)
-    check(rg, O.run(P(w)))
-
-
+# (oracle parity at full size for cfg3 / cfg4 / cfg5: tests/test_gpu_fullsize.py)
 def test_cfg3_full_run_invariants():
     """All 500 steps of config 3: trace and Hermiticity at every step; physical populations."""
     rg, _, _ = gpu_run(W.CONFIGS[3])
-    assert np.abs(np.einsum("kii->k", rg) - 1).max() <= TR_TOL
-    assert np.abs(rg - rg.conj().transpose(0, 2, 1)).max() <= 1e-13
-    pops = np.einsum("kii->ki", rg).real
-    assert pops.min() > -1e-9 and pops.max() < 1 + 1e-9
-
-
-def test_cfg5_full_size_on_one_gpu_invariants():
-    """Config 5 (4^16 entries = 69 GB, L = 16) on one B200 (180 GB HBM): trace and Hermiticity at every
-    step, and the first steps against the oracle's closed-form-pinned zero-coupling limit is covered
-    elsewhere; here the full-size fused path (all 16 ring slots, every TMA view) runs 40 steps."""
-    if torch.cuda.get_device_properties(0).total_memory < 80e9:
-        pytest.skip("needs > 80 GB of device memory")
-    w = W.CONFIGS[5].with_(n_steps=40)
-    rg, plan, ardm = gpu_run(w)
-    assert plan.sizes.ardm_entries == 4 ** 16
-    del ardm
-    torch.cuda.empty_cache()
     assert np.abs(np.einsum("kii->k", rg) - 1).max() <= TR_TOL
     assert np.abs(rg - rg.conj().transpose(0, 2, 1)).max() <= 1e-13
     pops = np.einsum("kii->ki", rg).real
@@ -195,25 +162,20 @@ def test_sigma_x_symmetry_full_size():
     assert np.abs(b - X @ a @ X).max() < 1e-12
 
 
-@pytest.mark.parametrize("kind", ["reg", "warp", "async", "split", "3"])
-@pytest.mark.parametrize("nosym", [False, True])
+@pytest.mark.parametrize("generic", [False, True])
 @pytest.mark.parametrize("fuse", [1, 2, 3])
 @pytest.mark.parametrize("M,L,n", [(2, 2, 9), (2, 3, 12), (2, 5, 17), (2, 7, 20), (2, 8, 23), (3, 4, 11), (4, 3, 8)])
-def test_fusion_depths(fuse, M, L, n, nosym, kind, monkeypatch):
-    """k_fused with 1 and 2 time steps per HBM pass (QUAPI_FUSE_S caps the depth) against the oracle;
+def test_fusion_depths(fuse, M, L, n, generic):
+    """1, 2 and 3 time steps per HBM pass (qp_problem.fuse_steps caps the depth) against the oracle;
     odd n and L exercise partial groups and super-fibres that wrap around the ring.  For M = 2 with
-    s = (+1, -1) the symmetric-moment kernel runs unless QUAPI_NO_SYM is set."""
-    if nosym and M != 2:
+    s = (+1, -1) the symmetric-moment kernels run unless QP_FLAG_GENERIC_MOMENTS is set."""
+    if generic and M != 2:
         pytest.skip("symmetric moments are M = 2 only")
-    monkeypatch.setenv("QUAPI_FUSE_S", str(fuse))
-    monkeypatch.setenv("QUAPI_FUSED_KIND", kind)
-    if nosym:
-        monkeypatch.setenv("QUAPI_NO_SYM", "1")
+    flags = Q.QP_FLAG_GENERIC_MOMENTS if generic else 0
     for lat in (True, False) if M > 2 else (True,):
         w = W.random_problem(300 + 10 * M + L, M, L, n, kind=W.J_DEBYE, lattice_s=lat)
-        rg, plan, _ = gpu_run(w)
-        assert plan.sizes.fuse_steps == (min(fuse, L - 1, 3 if kind == "3" else 2) if M == 2 else 1)
-    # default plan (no QUAPI_FUSED_KIND): three fused steps per pass for M = 2
+        rg, plan, _ = gpu_run(w, fuse_steps=fuse, flags=flags)
+        assert plan.sizes.fuse_steps == (min(fuse, L - 1) if M == 2 else 1)
         check(rg, O.run(P(w)))
 
 
@@ -231,19 +193,15 @@ def test_fusion_grouping_independent_of_segments():
     assert np.array_equal(plan.read_rho(work), whole)
 
 
-@pytest.mark.parametrize("env", [{}, {"QUAPI_NO_TMA": "1"}, {"QUAPI_F3TMAP": "1"}, {"QUAPI_NO_VIEWB": "1"}, {"QUAPI_NO_VIEWC": "1"}, {"QUAPI_NO_VIEWD": "1"},
-                                 {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "1"}, {"QUAPI_NO_TMA": "1", "QUAPI_F3MAP": "0"},
-                                 {"QUAPI_F3": "0"}, {"QUAPI_F3": "2"}, {"QUAPI_F3": "6"}, {"QUAPI_F3": "10"},
-                                 {"QUAPI_CA": "1"}, {"QUAPI_F3": "12"}, {"QUAPI_F3": "12", "QUAPI_NO_VIEWB": "1"},
-                                 {"QUAPI_VIEWD64": "1"}, {"QUAPI_VIEWC_OLD": "1"}, {"QUAPI_E0_SLICES": "1"}, {"QUAPI_F3": "9"}, {"QUAPI_F3": "9", "QUAPI_E0_SLICES": "1"}, {"QUAPI_VIEWD64": "1", "QUAPI_VIEWC_OLD": "1"}])
-@pytest.mark.parametrize("L,n", [(8, 37), (9, 30)])
-def test_fused3_load_paths(env, L, n, monkeypatch):
-    """k_fused3's load paths (TMA-staged rounds in views A and B, plain loads in lane maps 0 and 1,
-    32-byte loads/stores along ring slot 0, register prefetch) and launch variants against the
-    oracle; L >= 8 so that every start slot p0 (TMA views included) occurs."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+@pytest.mark.parametrize("flags", [0, Q.QP_FLAG_NO_TMA, Q.QP_FLAG_GENERIC_MOMENTS,
+                                   Q.QP_FLAG_NO_TMA | Q.QP_FLAG_GENERIC_MOMENTS])
+@pytest.mark.parametrize("L,n", [(6, 31), (8, 37), (9, 30)])
+def test_fused3_load_paths(flags, L, n):
+    """k_fused3's load paths against the oracle: per-warp TMA-staged rounds in all four stage views
+    (A: 1 <= p0 <= L-3, B: p0 = L-2, C: p0 = L-1, D: p0 = 0) and plain loads in lane maps 0 and 1
+    (QP_FLAG_NO_TMA), 32-byte loads/stores along ring slot 0, symmetric and generic moments;
+    L >= 6 so that every start slot p0 occurs."""
     w = W.random_problem(500 + L, 2, L, n, kind=W.J_OHMIC_EXP)
-    rg, plan, _ = gpu_run(w)
+    rg, plan, _ = gpu_run(w, flags=flags)
     assert plan.sizes.fuse_steps == 3
     check(rg, O.run(P(w)))
