@@ -87,16 +87,17 @@ typedef struct {
                                 0 => the free memory of the current CUDA device at plan creation
                                 (no check when no device is visible); < 0 => no check           */
     const qp_c64 *eta_in;    /* QP_J_ETA_TABLE only: [3*dkmax+2] eta classes, qp_plan_eta order   */
-    int32_t fuse_steps;      /* cap on the time steps fused into one pass over the ARDM, 0..3;
-                                0 => the library's choice (3 for M = 2, 1 for M = 3, 4).  Results
+    int32_t fuse_steps;      /* cap on the time steps fused into one pass over the ARDM, 0..4;
+                                0 => the library's choice (4 for M = 2 with L >= 6, else 3; 1 for
+                                M = 3, 4).  Results
                                 agree to rounding for every choice.                              */
     uint32_t flags;          /* QP_FLAG_* below; 0 for the default plan                          */
 } qp_problem;
 
 /* Plan options (qp_problem.flags).  They select among equivalent kernel paths (same result to
    rounding) and exist for testing and measurement:
-   QP_FLAG_NO_TMA           -- M = 2, 3 fused steps: plain loads instead of the per-warp TMA-staged
-                               rounds;
+   QP_FLAG_NO_TMA           -- M = 2: no TMA-staged kernels: at most 3 fused steps, plain loads
+                               instead of the per-warp TMA-staged rounds;
    QP_FLAG_GENERIC_MOMENTS  -- M = 2, s = (+s, -s): the generic per-class moments instead of the
                                symmetric four-sum moments. */
 #define QP_FLAG_NO_TMA 1u

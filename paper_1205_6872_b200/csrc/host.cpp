@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <tuple>
 #include <string>
@@ -312,6 +313,19 @@ qp_status eta_class(const Bath &b, const WinClass &c, cd *out, const char *name,
 }  // namespace
 
 // ===================================================================================== plan
+// One k_fused4 tensor map (slide4.cu): the order of the 11 box bits in the shared-memory stage
+// (bit 2 i + b = bit b of inner digit i, 8..10 = bits of the round's fibre index), the TMA
+// dimensions built from it, and which dimensions carry the round's outer-fibre coordinate.
+struct F4Map {
+    int pos[11];
+    int lane_swap = 0;       // lane mapping of the phase this map serves (FusedArgs::f4_q1swap / f4_q2swap)
+    int ndim = 0;
+    cuuint64_t gdim[5];
+    cuuint64_t gstr[4];
+    cuuint32_t box[5];
+    int cdimA = -1, cdimB = -1;
+};
+
 struct qp_plan {
     int M = 0, N = 0, L = 0, D = 0;
     bool lattice = false;        // class map used by the kernels
@@ -346,6 +360,14 @@ struct qp_plan {
         int tma_a = -1, tma_b = 0;
         mutable const void *tma_A = nullptr;  // ARDM pointer the cached tensor map was encoded for
         mutable CUtensorMap tmap{};
+        // k_fused4 (S = 4): load / store tensor maps of the 8-fibre rounds (f4_layout)
+        bool f4 = false;
+        F4Map f4map[2];                // [0] load (phase-1 reads conflict-free), [1] store (phase-2 writes)
+        int f4_col = 0;                // slot 0 outer: fibres are the 16-B chunks of a stage row
+        int f4_swz = 1;                // 128-B swizzle (both maps), else dense stage
+        long long f4_nA = 1;
+        int f4_c0m = 1;
+        mutable CUtensorMap tmapS{};
     };
     int group_w = 1;                   // digits per outer digit group (g >= 1) of the factor tables
     int Smax = 1;
@@ -545,6 +567,7 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
 // order (block partials) is deterministic.
 static int slide_path(int S, const qp::FusedArgs &a) { return S == 3 ? (a.use_tma ? 2 : (a.lane_map & 1)) : 0; }
 static int slide_occupancy(const qp_plan &P, int S, int path) {
+    if (P.M == 2 && S == 4) return qp::fused4_occupancy(P.sym);
     if (P.M == 2 && S == 3) return qp::fused3_occupancy(P.sym, path & 1, path == 2);
     return qp::fused_r_occupancy(P.M, P.lattice, P.sym, S);
 }
@@ -555,8 +578,211 @@ static int launch_grid(qp_plan *P, int S, const qp::FusedArgs &a) {
     return std::max(1, std::min<int>({a.n_tiles, P->sms * o, qp::kPartialsMax}));
 }
 static cudaError_t launch_slide(const qp_plan &P, int S, const qp::FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    if (P.M == 2 && S == 4) return qp::launch_fused4(P.sym, a, ro, grid, s);
     if (P.M == 2 && S == 3) return qp::launch_fused3(P.sym, a, ro, grid, s);
     return qp::launch_fused_r(P.M, P.lattice, P.sym, S, a, ro, grid, s);
+}
+
+// ---- k_fused4 stage layouts.  A stage holds one round: 8 outer fibres x the 256 entries of the inner
+// digits d0..d3, as 11 box bits.  Under the 128-B swizzle a 16-B access at stage offset o (16-B units)
+// hits bank group (o ^ (o >> 3)) & 7, so a quarter-warp (8 lanes) is conflict-free iff the three box
+// bits its lanes vary map invertibly (over GF(2)) onto (bit i) ^ (bit i+3), i = 0..2, of the offset.
+// Phase 1 (loads): lanes vary (d2, d3 & 1) (q = d2 + 4 d3) or (d3, d2 & 1) (q = d3 + 4 d2); phase 2
+// (stores): (d0, d1 & 1) or (d1, d0 & 1).  The fibre bits sit at stage bits 0-2 when ring slot 0 (stride
+// 1) is an outer slot, else at bits 8-10; the search orders the inner bits so that the load map serves
+// phase 1 and the store map phase 2 with at most 5 TMA dimensions.
+static bool gf2_invertible3(const int (&m)[3][3]) {
+    int r[3];
+    for (int i = 0; i < 3; ++i) r[i] = m[i][0] | (m[i][1] << 1) | (m[i][2] << 2);
+    for (int c = 0; c < 3; ++c) {
+        int piv = -1;
+        for (int i = c; i < 3; ++i)
+            if (r[i] >> c & 1) { piv = i; break; }
+        if (piv < 0) return false;
+        std::swap(r[c], r[piv]);
+        for (int i = 0; i < 3; ++i)
+            if (i != c && (r[i] >> c & 1)) r[i] ^= r[c];
+    }
+    return true;
+}
+
+bool f4_layout(const qp_plan &P, qp_plan::LaunchSet &ls, const std::vector<int> &pos, const std::vector<int> &inner,
+               const std::vector<int> &outer) {
+    const int N = P.N;
+    if ((int)inner.size() != 4 || outer.size() < 2) return false;
+    long long hs[11];  // HBM stride (entries) of each box bit
+    for (int i = 0; i < 4; ++i)
+        for (int b = 0; b < 2; ++b) hs[2 * i + b] = ipow(N, pos[inner[i]]) << b;
+    hs[8] = ipow(N, pos[outer[0]]), hs[9] = 2 * hs[8], hs[10] = ipow(N, pos[outer[1]]);
+    // outer runs: consecutive local positions
+    std::vector<int> op;
+    for (int q : outer) op.push_back(pos[q]);
+    std::vector<std::pair<int, int>> runs;  // (first position, length)
+    for (size_t i = 0; i < op.size(); ++i) {
+        if (i && op[i] == op[i - 1] + 1) runs.back().second++;
+        else runs.push_back({op[i], 1});
+    }
+    const bool typeA = op[0] == 0;
+    if (typeA ? runs.size() > 2 : runs.size() != 1) return false;
+    const long long nA = typeA ? ipow(N, runs[0].second) : (1ll << 62);
+    if (typeA && nA < 4) return false;
+    // the inner bits with HBM stride 1, 2, 4 (type I: the lowest 128 B of a fibre)
+    int z[3] = {-1, -1, -1};
+    for (int r = 0; r < 8; ++r)
+        for (int k = 0; k < 3; ++k)
+            if (hs[r] == (1ll << k)) z[k] = r;
+    if (!typeA && (z[0] < 0 || z[1] < 0)) return false;
+    // 128-B swizzle only with 128-B inner box rows (8 HBM-contiguous entries: 8 fibres, or three inner
+    // bits); otherwise no swizzle (dense stage, possibly bank-conflicted: odd L only, p0 = 1 or L - 3)
+    const bool swz = typeA ? nA >= 8 : z[2] >= 0;
+    for (int which = 0; which < 2; ++which) {
+        F4Map best{};
+        int best_nd = 99;
+        for (int swap = 0; swap < (swz ? 2 : 1); ++swap) {
+            int qa[3];  // quarter-varying box bits of the phase this map serves
+            if (which == 0) { if (swap) qa[0] = 6, qa[1] = 7, qa[2] = 4; else qa[0] = 4, qa[1] = 5, qa[2] = 6; }
+            else { if (swap) qa[0] = 2, qa[1] = 3, qa[2] = 0; else qa[0] = 0, qa[1] = 1, qa[2] = 2; }
+            // fixed positions: type A fibre bits 0..2; type I (swizzled) the three lowest inner bits 0..2,
+            // (unswizzled) nothing but the stride-1 bit at 0; fibre bits at 8..10.  Positions first..5 are
+            // chosen (they decide the banks), the rest follow in HBM-stride order.
+            std::vector<int> fixed;
+            if (typeA) fixed = {8, 9, 10};
+            else if (swz) fixed = {z[0], z[1], z[2]};
+            else fixed = {z[0]};
+            const int first = (int)fixed.size();
+            const int nchoose = swz ? 6 - first : 0;
+            std::vector<int> cand;
+            for (int r = 0; r < 8; ++r)
+                if (std::find(fixed.begin(), fixed.end(), r) == fixed.end()) cand.push_back(r);
+            std::vector<int> pick(nchoose, 0);
+            std::function<void(int, unsigned)> rec = [&](int k, unsigned used) {
+                if (k < nchoose) {
+                    for (size_t c = 0; c < cand.size(); ++c)
+                        if (!(used >> c & 1)) { pick[k] = (int)c; rec(k + 1, used | (1u << c)); }
+                    return;
+                }
+                int order[11];
+                for (int t = 0; t < first; ++t) order[t] = fixed[t];
+                unsigned used2 = 0;
+                for (int t = 0; t < nchoose; ++t) order[first + t] = cand[pick[t]], used2 |= 1u << pick[t];
+                std::vector<int> rest;
+                for (size_t c = 0; c < cand.size(); ++c)
+                    if (!(used2 >> c & 1)) rest.push_back(cand[c]);
+                std::sort(rest.begin(), rest.end(), [&](int x, int y) { return hs[x] < hs[y]; });
+                for (size_t t = 0; t < rest.size(); ++t) order[first + nchoose + t] = rest[t];
+                if (!typeA) order[8] = 8, order[9] = 9, order[10] = 10;
+                if (swz) {  // bank condition
+                    int m[3][3];
+                    for (int i = 0; i < 3; ++i)
+                        for (int j = 0; j < 3; ++j) m[i][j] = (order[i] == qa[j]) ^ (order[i + 3] == qa[j]);
+                    if (!gf2_invertible3(m)) return;
+                }
+                // TMA dims
+                F4Map mp{};
+                for (int t = 0; t < 11; ++t) mp.pos[order[t]] = t;
+                mp.lane_swap = swap;
+                int nd = 0;
+                auto add = [&](cuuint64_t g, cuuint32_t bx, long long stride_entries) {
+                    if (nd >= 5) { nd = 6; return; }
+                    mp.gdim[nd] = g, mp.box[nd] = bx;
+                    if (nd > 0) mp.gstr[nd - 1] = (cuuint64_t)stride_entries * 16;
+                    ++nd;
+                };
+                int t0 = 0;
+                if (typeA) {
+                    add((cuuint64_t)(2 * nA), (cuuint32_t)(2 * std::min<long long>(nA, 8)), 0);
+                    mp.cdimA = 0;
+                    if (nA < 8) {  // fibre bit 2 is the first bit of run B
+                        if (runs.size() < 2) return;
+                        add((cuuint64_t)ipow(N, runs[1].second), (cuuint32_t)(8 / nA), ipow(N, runs[1].first));
+                        mp.cdimB = 1;
+                    }
+                    t0 = 3;
+                }
+                const int tend = typeA ? 11 : 8;
+                for (int t = t0; t < tend;) {  // inner bits: merge runs of doubling stride (dim 0 <= 128 B)
+                    int u = t + 1;
+                    while (u < tend && hs[order[u]] == 2 * hs[order[u - 1]] && !(!typeA && t == 0 && u - t >= 3)) ++u;
+                    const cuuint64_t sz = 1ull << (u - t);
+                    if (!typeA && t == 0) add(2 * sz, (cuuint32_t)(2 * sz), 0);  // dim 0 in doubles
+                    else add(sz, (cuuint32_t)sz, hs[order[t]]);
+                    t = u;
+                }
+                if (!typeA) {
+                    mp.cdimA = nd;
+                    add((cuuint64_t)ipow(N, runs[0].second), 8, ipow(N, runs[0].first));
+                } else if (nA >= 8 && runs.size() > 1) {
+                    mp.cdimB = nd;
+                    add((cuuint64_t)ipow(N, runs[1].second), 1, ipow(N, runs[1].first));
+                }
+                if (nd > 5) return;
+                mp.ndim = nd;
+                if (nd < best_nd) best = mp, best_nd = nd;
+            };
+            rec(0, 0);
+        }
+        if (best_nd > 5) return false;
+        for (int d = best.ndim; d < 5; ++d) {  // pad to 5-D with unit dims
+            best.gdim[d] = 1, best.box[d] = 1;
+            best.gstr[d - 1] = 16;
+        }
+        ls.f4map[which] = best;
+    }
+    ls.f4_col = typeA ? 1 : 0;
+    ls.f4_swz = swz ? 1 : 0;
+    ls.f4_nA = nA;
+    ls.f4_c0m = typeA ? 2 : 1;
+    return true;
+}
+
+static bool encode_f4_tmaps(const qp_plan::LaunchSet &ls, double2 *A) {
+    if (ls.tma_A == A) return true;
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    for (int w = 0; w < 2; ++w) {
+        const F4Map &m = ls.f4map[w];
+        CUtensorMap *dst = w == 0 ? &ls.tmap : &ls.tmapS;
+        if (enc(dst, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)A, m.gdim, m.gstr, m.box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                ls.f4_swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    ls.tma_A = A;
+    return true;
+}
+
+// TMA fields of one launch of set ls on the ARDM (or local shard block) A; d_work w holds the tables.
+static qp_status set_tma(const qp_plan &P, const qp_plan::LaunchSet &ls, qp::FusedArgs &a, double2 *A, char *w) {
+    a.use_tma = 0;
+    if (ls.S == 4) {
+        if (!ls.f4 || !encode_f4_tmaps(ls, A)) return err(QP_ERR_CUDA, "cuda: cannot encode the k_fused4 tensor maps (p0 = %d)", ls.p0);
+        a.use_tma = 1;
+        a.tmap = ls.tmap;
+        a.tmapS = ls.tmapS;
+        for (int i = 0; i < 11; ++i) a.f4_lpos[i] = ls.f4map[0].pos[i], a.f4_spos[i] = ls.f4map[1].pos[i];
+        a.f4_q1swap = ls.f4map[0].lane_swap;
+        a.f4_q2swap = ls.f4map[1].lane_swap;
+        a.f4_colregion = ls.f4_col;
+        a.f4_swz = ls.f4_swz;
+        a.f4_layout = qp::fused4_layout_type(a.f4_lpos, a.f4_spos, a.f4_q1swap, a.f4_q2swap, a.f4_swz);
+        for (int m = 0; m < 2; ++m) a.f4_cdimA[m] = ls.f4map[m].cdimA, a.f4_cdimB[m] = ls.f4map[m].cdimB;
+        a.tma_nA = ls.f4_nA;
+        a.tma_c0m = ls.f4_c0m;
+        a.E0r = (const double2 *)(w + ls.off_E0r);
+        return QP_OK;
+    }
+    if (ls.tma_a != -1 && ls.S == 3 && encode_f3_tmap(P, ls, A, ls.e0r_F)) {
+        a.use_tma = 1;
+        a.tmap = ls.tmap;
+        // TMA box coordinates of unit G (first outer fibre): c0 = tma_c0m (G mod tma_nA), c1 = G / tma_nA
+        // (view A: run A as doubles; view B: rows of two fibres; views C, D: one fibre per row group)
+        a.tma_nA = ls.tma_a > 0 ? ipow(P.N, ls.tma_a) : (ls.tma_a == 0 ? 2 : 1);
+        a.tma_c0m = ls.tma_a > 0 ? 2 : 0;
+        a.tma_view = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? 2 : 3));
+        a.E0r = (const double2 *)(w + ls.off_E0r);
+    }
+    return QP_OK;
 }
 
 // Tables of one fused launch over inner slots p0..p0+S-1 (mod L) of a local layout from which the
@@ -577,9 +803,9 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     const int nout = (int)outer.size();
     // tile digits: the kernel's preferred v, lowered (not below its minimum) so that small problems
     // still have >= ~2 tiles per SM of a 148-SM B200 to spread over the persistent grid
-    const bool f3 = (M == 2 && S == 3);
-    int v = std::min(f3 ? qp::kFused3TileDigits : qp::fused_r_tile_digits(M, S), nout);
-    const int vmin = std::min(f3 ? qp::kFused3TileDigitsMin : (N >= 9 ? 2 : 3), nout);
+    const bool f3 = (M == 2 && S == 3), f4 = (M == 2 && S == 4);
+    int v = std::min(f4 ? 4 : (f3 ? qp::kFused3TileDigits : qp::fused_r_tile_digits(M, S)), nout);
+    const int vmin = std::min(f4 ? 2 : (f3 ? qp::kFused3TileDigitsMin : (N >= 9 ? 2 : 3)), nout);
     while (v > vmin && std::pow((double)N, nout - v) < 2.0 * 148) --v;
     const int w = std::max(1, P.group_w);
     const int hi = nout - v;
@@ -701,6 +927,25 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
         ls.e0r_F = F;
     }
     a.use_tma = 0;
+    ls.f4 = false;
+    if (f4) {
+        // k_fused4: one E0 block per 8-fibre round of a tile: factors [s][kap][c][f] + the 8 lofs (int2)
+        if (f4_layout(P, ls, pos, inner, outer) && T % 8 == 0) {
+            ls.f4 = true;
+            const int F = 8, R = T / F, Q = S * 2 * D;
+            const size_t blk = (size_t)Q * F + F / 2;
+            ls.E0r.assign((size_t)R * blk, make_double2(0.0, 0.0));
+            for (int rd = 0; rd < R; ++rd) {
+                double2 *b = ls.E0r.data() + rd * blk;
+                for (int q = 0; q < Q; ++q) {
+                    const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
+                    for (int f = 0; f < F; ++f) b[(size_t)q * F + f] = ls.Etab[((((size_t)st * 2 + kap) * G) * D + d) * X + rd * F + f];
+                }
+                std::memcpy(b + (size_t)Q * F, ls.lofs.data() + (size_t)rd * F, F * sizeof(int2));
+            }
+            ls.e0r_F = F;
+        }
+    }
     for (int st = 0; st < qp::kMaxS; ++st)
         for (int kap = 0; kap < 2; ++kap)
             for (int d = 0; d < qp::kMaxD; ++d) a.fixfac[st][kap][d] = make_double2(1.0, 0.0);
@@ -766,7 +1011,10 @@ void build_tables(qp_plan &P, int fuse_cap) {
     // fusion depth: three steps per pass for M = 2 (k_fused3), one for M = 3, 4 (k_fused_r); the
     // caller may cap it (qp_problem.fuse_steps)
     P.group_w = (M == 2) ? 4 : (M == 3 ? 3 : 2);
-    P.Smax = std::max(1, std::min(M == 2 ? 3 : 1, L - 1));
+    // M = 2: four fused steps per pass (k_fused4, TMA load and store) when the outer slots hold at
+    // least two digits (L >= 6), else three (k_fused3)
+    const int s2 = (L >= 6 && !(P.flags & QP_FLAG_NO_TMA)) ? 4 : 3;
+    P.Smax = std::max(1, std::min(M == 2 ? s2 : 1, L - 1));
     if (fuse_cap > 0) P.Smax = std::min(P.Smax, fuse_cap);
     P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
     {  // the L * Smax launch sets are independent (read-only plan, own tables): build them on host threads
@@ -854,7 +1102,7 @@ qp_status validate(const qp_problem *pr) {
         break;
     default: return err(QP_ERR_CONFIG, "config: unknown bath kind %d", pr->kind);
     }
-    if (pr->fuse_steps < 0 || pr->fuse_steps > 3) return err(QP_ERR_CONFIG, "config: fuse_steps must be in [0, 3] (got %d)", pr->fuse_steps);
+    if (pr->fuse_steps < 0 || pr->fuse_steps > 4) return err(QP_ERR_CONFIG, "config: fuse_steps must be in [0, 4] (got %d)", pr->fuse_steps);
     if (pr->flags & ~(uint32_t)(QP_FLAG_NO_TMA | QP_FLAG_GENERIC_MOMENTS))
         return err(QP_ERR_CONFIG, "config: unknown flags 0x%x", pr->flags);
     if (pr->out_steps) {
@@ -910,6 +1158,12 @@ qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
     if ((st = compute_eta(*P, *pr))) { delete P; return st; }
     const auto t2 = std::chrono::steady_clock::now();
     build_tables(*P, pr->fuse_steps);
+    for (const auto &ls : P->sets)
+        if (ls.S == 4 && !ls.f4) {
+            const int p0 = ls.p0;
+            delete P;
+            return err(QP_ERR_CONFIG, "internal: no k_fused4 stage layout for p0 = %d", p0);
+        }
     const auto t3 = std::chrono::steady_clock::now();
     P->setup_ms[0] = std::chrono::duration<double, std::milli>(t1 - t0).count();
     P->setup_ms[1] = std::chrono::duration<double, std::milli>(t2 - t1).count();
@@ -1048,7 +1302,8 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
         qp::FusedArgs a = ls.args;
         a.use_tma = ls.tma_a != -1;
         P->grid[P->Smax] = launch_grid(P, P->Smax, a);
-        P->block = (P->M == 2 && P->Smax == 3) ? qp::fused3_block(a.lane_map, a.use_tma) : qp::fused_r_block(P->M, P->Smax);
+        P->block = (P->M == 2 && P->Smax == 4) ? qp::fused4_block()
+                   : (P->M == 2 && P->Smax == 3) ? qp::fused3_block(a.lane_map, a.use_tma) : qp::fused_r_block(P->M, P->Smax);
     }
     P->next_k = 1;
     P->sh.seg = 0;
@@ -1096,17 +1351,7 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             qp::FusedArgs a = ls.args;
             a.A = A;
             a.small = small;
-            a.use_tma = 0;
-            if (ls.tma_a != -1 && S == 3 && encode_f3_tmap(*P, ls, A, ls.e0r_F)) {
-                a.use_tma = 1;
-                a.tmap = ls.tmap;
-                // TMA box coordinates of unit G (first outer fibre): c0 = tma_c0m (G mod tma_nA), c1 = G / tma_nA
-                // (view A: run A as doubles; view B: rows of two fibres; views C, D: one fibre per row group)
-                a.tma_nA = ls.tma_a > 0 ? ipow(P->N, ls.tma_a) : (ls.tma_a == 0 ? 2 : 1);
-                a.tma_c0m = ls.tma_a > 0 ? 2 : 0;
-                a.tma_view = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? 2 : 3));
-                a.E0r = (const double2 *)(w + ls.off_E0r);
-            }
+            if (qp_status st = set_tma(*P, ls, a, A, w)) return st;
             a.inner = (const double2 *)(w + ls.off_inner);
             a.Etab = (const double2 *)(w + ls.off_E);
             a.goff = (const long long *)(w + ls.off_goff);
@@ -1388,6 +1633,7 @@ qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_loc
             a.partials = (double2 *)(w + P->off_part);
             a.counter = (unsigned *)(w + P->off_cnt);
             a.rho_accumulate = b > 0 ? 1 : 0;
+            if (qp_status st = set_tma(*P, ls, a, a.A, w)) return st;
             int dig[8];
             shard_combo_digits(*P, sh.c_lo[sh.rank] + b, dig);
             bool ro = false;

@@ -69,7 +69,16 @@ struct FusedArgs {
     int tma_view;            // k_fused3 stage view: 0 = A, 1 = B, 2 = C, 3 = D (slide3.cu, host.cpp encode_f3_tmap)
     long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view (view B: 2, views C/D: 1)
     int tma_c0m;             // TMA coordinate 0 = tma_c0m x (G mod tma_nA) doubles, coordinate 1 = G / tma_nA
-    alignas(64) CUtensorMap tmap;
+    alignas(64) CUtensorMap tmap;   // k_fused3 / k_fused4 load map
+    alignas(64) CUtensorMap tmapS;  // k_fused4 store map
+    // k_fused4 stage layouts (slide4.cu, host.cpp f4_layout): smem bit position (16-B units) of each
+    // box bit: 2 i + b = bit b of inner digit i, 8..10 = bits of the round's fibre index
+    int f4_lpos[11], f4_spos[11];
+    int f4_q1swap, f4_q2swap;  // lane mappings: phase 1 q = d2 + 4 d3 (0) or d3 + 4 d2 (1); phase 2 q = d0 + 4 d1 / d1 + 4 d0
+    int f4_colregion;          // 1: the 8 fibres of a round are the 16-B chunks of each 128-B stage row (slot 0 outer)
+    int f4_swz;                // 1: both maps use the 128-B swizzle (128-B inner box rows), 0: dense stage
+    int f4_layout;             // k_fused4 instantiation with these layouts compiled in (1..3), 0: run-time layout
+    int f4_cdimA[2], f4_cdimB[2];  // per map (load, store): box dims whose coordinate is tma_c0m (G mod tma_nA) / G / tma_nA
     int var[kMaxS];          // beta variant per sub-step: 1 for the first slide step k == L (initial-edge
                              // classes of the partner sigma_0), else 0 (SmallLayout::beta)
     // M = 2, s = (+s, -s): beta_1 = (c, rho, 1/rho, conj c); {Re c, Im c, (rho+1/rho)/2, (rho-1/rho)/2}
@@ -121,6 +130,13 @@ int fused3_block(int lane_map, bool tma);
 int fused3_round_fibres(int lane_map, bool tma);  // outer fibres per round (8 per warp)
 int fused3_occupancy(bool sym, int lane_map, bool tma);
 cudaError_t launch_fused3(bool sym, const FusedArgs &a, bool ro, int grid, cudaStream_t s);
+// k_fused4 (slide4.cu): M = 2, S = 4, TMA load + store of 8-fibre rounds, warp-specialised
+int fused4_block();
+int fused4_round_fibres();
+int fused4_e0_block();  // double2 entries of one round's E0 block
+int fused4_occupancy(bool sym);
+int fused4_layout_type(const int (&lpos)[11], const int (&spos)[11], int q1swap, int q2swap, int swz);
+cudaError_t launch_fused4(bool sym, const FusedArgs &a, bool ro, int grid, cudaStream_t s);
 
 // Batched sweeps (batch.cu): B independent problems, one CTA each, every step in one launch.
 // Table image (double2 entries) at `tab`: psi_eta[L+1][N], psi_E[L+1][N], psi_TI[L+1][N] (lag j = 1..L;

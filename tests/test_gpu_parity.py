@@ -163,10 +163,10 @@ def test_sigma_x_symmetry_full_size():
 
 
 @pytest.mark.parametrize("generic", [False, True])
-@pytest.mark.parametrize("fuse", [1, 2, 3])
-@pytest.mark.parametrize("M,L,n", [(2, 2, 9), (2, 3, 12), (2, 5, 17), (2, 7, 20), (2, 8, 23), (3, 4, 11), (4, 3, 8)])
+@pytest.mark.parametrize("fuse", [1, 2, 3, 4])
+@pytest.mark.parametrize("M,L,n", [(2, 2, 9), (2, 3, 12), (2, 5, 17), (2, 6, 21), (2, 7, 20), (2, 8, 23), (3, 4, 11), (4, 3, 8)])
 def test_fusion_depths(fuse, M, L, n, generic):
-    """1, 2 and 3 time steps per HBM pass (qp_problem.fuse_steps caps the depth) against the oracle;
+    """1 to 4 time steps per HBM pass (qp_problem.fuse_steps caps the depth) against the oracle;
     odd n and L exercise partial groups and super-fibres that wrap around the ring.  For M = 2 with
     s = (+1, -1) the symmetric-moment kernels run unless QP_FLAG_GENERIC_MOMENTS is set."""
     if generic and M != 2:
@@ -175,7 +175,7 @@ def test_fusion_depths(fuse, M, L, n, generic):
     for lat in (True, False) if M > 2 else (True,):
         w = W.random_problem(300 + 10 * M + L, M, L, n, kind=W.J_DEBYE, lattice_s=lat)
         rg, plan, _ = gpu_run(w, fuse_steps=fuse, flags=flags)
-        assert plan.sizes.fuse_steps == (min(fuse, L - 1) if M == 2 else 1)
+        assert plan.sizes.fuse_steps == (min(fuse, L - 1, 4 if L >= 6 else 3) if M == 2 else 1)
         check(rg, O.run(P(w)))
 
 
@@ -202,6 +202,21 @@ def test_fused3_load_paths(flags, L, n):
     (QP_FLAG_NO_TMA), 32-byte loads/stores along ring slot 0, symmetric and generic moments;
     L >= 6 so that every start slot p0 occurs."""
     w = W.random_problem(500 + L, 2, L, n, kind=W.J_OHMIC_EXP)
-    rg, plan, _ = gpu_run(w, flags=flags)
+    rg, plan, _ = gpu_run(w, flags=flags, fuse_steps=3)
     assert plan.sizes.fuse_steps == 3
+    check(rg, O.run(P(w)))
+
+
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("L", [6, 7, 8, 9, 10, 11, 12, 13])
+def test_fused4_every_start_slot(L, generic):
+    """k_fused4 (four steps per pass, TMA load + store of 8-fibre rounds) against the oracle at every
+    start slot p0: odd L visit every residue, so all stage-layout types occur (slot 0 outer: fibres
+    as the chunks of a stage row; slot 0 = inner digit 0..3: fibres as row blocks), with run A of one
+    digit (p0 = 1, fibre bit 2 in run B) and the readout of every step."""
+    n = 2 * L + 4 * L + 3  # >= L start slots of four-step groups after the growth
+    w = W.random_problem(700 + L, 2, L, n, kind=W.J_DEBYE)
+    flags = Q.QP_FLAG_GENERIC_MOMENTS if generic else 0
+    rg, plan, _ = gpu_run(w, flags=flags)
+    assert plan.sizes.fuse_steps == 4
     check(rg, O.run(P(w)))
