@@ -249,10 +249,10 @@ def main():
                               if sz.ardm_bytes > 2 * 126e6 else
                               f"L2-resident ARDM ({sz.ardm_bytes / 1e6:.1f} MB): not flushed, not a roofline case"),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "kernel": ("k_fused3: 3 time steps per HBM pass, persistent grid, per-warp TMA-staged "
-                                  "rounds (one box + one mbarrier per warp), one instantiation per TMA view"
-                                  if sz.fuse_steps == 3 else
-                                  f"k_fused_r: {sz.fuse_steps} time step(s) per HBM pass"),
+                       "kernel": ({4: "k_fused4: 4 time steps per HBM pass, TMA load + TMA store of 8-fibre rounds "
+                                      "(2-stage ring, producer warp), persistent grid",
+                                   3: "k_fused3: 3 time steps per HBM pass, per-warp TMA-staged rounds"}
+                                  .get(sz.fuse_steps, f"k_fused_r: {sz.fuse_steps} time step(s) per HBM pass")),
                        "steps_per_launch": K / max(1, launches)},
             "achieved_gbs": achieved,
             "step_equivalent_gbs": step_equiv,

@@ -36,8 +36,8 @@ def _cuda():
     B.build()
 
 
-def gpu_rho(w, out_steps=None):
-    plan = Q.Plan(w, out_steps=out_steps)
+def gpu_rho(w, out_steps=None, **kw):
+    plan = Q.Plan(w, out_steps=out_steps, **kw)
     ardm, work = plan.alloc()
     rho = plan.run(ardm, work)
     sz = plan.sizes
@@ -60,11 +60,17 @@ def _need_hbm(gb):
 
 
 def test_cfg3_full_size_every_view_and_ring_wrap():
+    """The bench's launch configuration (four steps per pass, k_fused4) and the three-step kernel with
+    its four TMA stage views (k_fused3), both against one oracle run."""
     w = W.CONFIGS[3]
     w = w.with_(n_steps=2 * w.L + 3)
+    ro = O.run(P(w))
     rg, sz = gpu_rho(w)
-    assert sz.ardm_entries == 4 ** 14 and sz.fuse_steps == 3
-    check(rg, O.run(P(w)))
+    assert sz.ardm_entries == 4 ** 14 and sz.fuse_steps == 4
+    check(rg, ro)
+    rg3, sz3 = gpu_rho(w, fuse_steps=3)
+    assert sz3.fuse_steps == 3
+    check(rg3, ro)
 
 
 def test_cfg4_full_size_parity():
