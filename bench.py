@@ -7,8 +7,10 @@ A "step" is one QUAPI time step k >= L of the BASELINE workload (config 3: spin-
 Debye bath, Delta k_max = 14, ARDM of 4^14 complex FP64 entries = 4.3 GB, larger than L2):
 the in-place slide of the ARDM with the rho(t_k) readout fused (allPoints mode).  Our arm
 times K such steps after W warm-up steps with CUDA events on the launching stream (barrier +
-synchronize on both sides, max over ranks).  N > 1: independent replicas, one per GPU (weak
-scaling; the sharded config-5 path is DESIGN.md's next step).
+synchronize on both sides, max over ranks).  N > 1 (torchrun): by default one ARDM sharded over the
+ranks (strong scaling: shard-native growth, fused slide steps on each rank's shard, NCCL
+all_to_all_single re-shard every L - z steps inside the timed region); --mode replica runs
+independent replicas (weak scaling).  --cfg 5 is the sharded BASELINE case (L = 16).
 
 --impl reference: the CPU oracle (oracle/liboracle.so) on the host cores, same config/metric.
 """
@@ -288,7 +290,7 @@ def bench_sharded(args, base, world, rank, local):
     stream = torch.cuda.current_stream()
     me = SH.ShardRank(w, world, rank, device=f"cuda:{local}", stream=stream)
     ex = SH.dist_exchange()
-    me.growth_and_extract()
+    me.grow()  # shard-native growth: no rank holds the N^L ARDM
     SH.advance([me], L, L + Wm, ex)
     torch.cuda.synchronize()
     dist.barrier()
@@ -305,10 +307,7 @@ def bench_sharded(args, base, world, rank, local):
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    part = me.plan.read_rho(me.work, stream)
-    pt = torch.from_numpy(part.view(np.float64).copy()).cuda()
-    gathered = [torch.empty_like(pt) for _ in range(world)] if rank == 0 else None
-    dist.gather(pt, gathered, dst=0)
+    rho = SH.dist_rho(me)  # all-gather of the rho blocks, rank-ordered sum in the library (rank 0)
     sz = me.plan.sizes
     ssz = me.sizes
     del me
@@ -328,8 +327,6 @@ def bench_sharded(args, base, world, rank, local):
         if rank == 0:
             e2e["max_abs_trace_err"] = float(np.abs(np.einsum("kii->k", rho_e) - 1).max())
     if rank == 0:
-        parts = [g.cpu().numpy().view(np.complex128).reshape(part.shape) for g in gathered]
-        rho = SH.combine_rho(parts, np.arange(w.n_steps + 1), L)
         steps_per_s = K / (ms_max / 1e3)
         peak, peak_kind = _peaks()
         passes = K / max(1, sz.fuse_steps)

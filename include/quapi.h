@@ -127,8 +127,13 @@ typedef struct {
 /* Host only (no GPU needed): validate (a1), U = e^{-iH dt} and the pair propagator K (a2),
    eta by omega-quadrature (a3), factor tables and launch schedule (a4).  *out owned by caller,
    free with qp_plan_destroy.  Errors: QP_ERR_ARG, QP_ERR_CONFIG, QP_ERR_QUADRATURE,
-   QP_ERR_CAPACITY (only when max_bytes > 0). */
+   QP_ERR_CAPACITY (only when max_bytes > 0: ARDM + workspace exceed it). */
 qp_status qp_plan_create(const qp_problem *prob, qp_plan **out);
+/* Capacity (a1) of the plan as configured (unsharded: ARDM + workspace; sharded: two shard buffers +
+   workspace) against max_bytes (> 0), else the free memory of the current CUDA device (no check
+   when no device is visible, or max_bytes < 0).  Call before allocating.  Error: QP_ERR_CAPACITY
+   with the byte counts. */
+qp_status qp_plan_check(const qp_plan *plan);
 qp_status qp_plan_query(const qp_plan *plan, qp_sizes *out);
 
 /* eta classes used by the plan (units: the eta of Eqs. 10-16), written as
@@ -167,11 +172,21 @@ qp_status qp_run(qp_plan *plan, void *d_ardm, void *d_work, void *stream, qp_c64
 /* ---------------------------------------------------------------- sharded execution (multi-GPU)
    SURVEY §8(e): G ranks (one per GPU) each hold, during segment j, the ARDM entries whose z shard
    ring slots Z_j (the z most recently written slots at the segment start k_j = L + j (L - z)) take
-   one of the rank's owned value combos; the L - z steps of a segment never contract a shard slot and
-   run shard-locally.  Between segments the caller re-shards: qp_shard_pack -> all-to-all (NCCL,
-   counts from qp_shard_counts, ordered by rank) -> qp_shard_unpack.  Growth (k < L) runs
-   replicated on the full ARDM before qp_shard_extract.  Readouts of slide steps are this rank's
-   partial sums (sum over ranks in rank order for rho); growth readouts are complete on every rank. */
+   one of the rank's owned value combos (a fixed, balanced range c_lo .. c_lo + n_own - 1): one block
+   of N^(L-z) entries per combo, the other slots in ascending order.  The L - z slide steps of a
+   segment never contract a shard slot, so they run shard-locally with the combo's Eq. 9 factors
+   folded in.  No rank ever holds the N^L ARDM:
+     - qp_init(plan, d_xbuf, d_work): tables, A_0 into the exchange buffer;
+     - qp_shard_steps, k = 1 .. L-z-1: growth replicated in d_xbuf (N^(k+1) <= N^(L-z) entries);
+       k = L-z .. L-1: the growth steps that add the shard digits, computed for this rank's combos
+       only from the replicated A_{L-z-1} into d_local; k >= L: slide steps within the segment;
+     - between segments: qp_shard_pack (d_local -> d_xbuf, send order), the caller's all-to-all
+       (d_xbuf -> d_local, counts from qp_shard_counts, ordered by rank), qp_shard_unpack
+       (d_local -> d_xbuf, next layout); the CALLER THEN SWAPS d_local and d_xbuf.
+   Memory per rank: two buffers of local_entries (16 B each) + workspace (qp_plan_check).
+   Readouts: steps k <= L - z are complete on every rank; later steps are this rank's partial sums
+   (each prefix of the shard digits counted by exactly one rank); qp_shard_combine sums the ranks'
+   outputs in rank order on the device. */
 typedef struct {
     int32_t n_ranks, rank;
     int32_t shard_slots;       /* z                                                                 */
@@ -180,21 +195,34 @@ typedef struct {
     int64_t max_local_entries; /* over ranks                                                        */
     int64_t exchange_entries;  /* entries this rank sends (and receives) per re-shard               */
     int64_t work_bytes;        /* workspace including the shard launch tables                       */
+    int64_t xbuf_entries;      /* exchange buffer entries (>= local_entries, >= N^(L-z))            */
 } qp_shard_sizes;
 
-/* Host only; call before qp_init (the workspace grows: query work_bytes again). 2 <= n_ranks. */
+/* Host only; once, before qp_init (the workspace grows: query work_bytes again).  2 <= n_ranks.
+   Errors: QP_ERR_ARG (called twice or after qp_init), QP_ERR_CONFIG (L too small for n_ranks),
+   QP_ERR_CAPACITY (max_bytes > 0 and two shard buffers + workspace exceed it). */
 qp_status qp_shard_configure(qp_plan *plan, int32_t n_ranks, int32_t rank);
 qp_status qp_shard_query(const qp_plan *plan, qp_shard_sizes *out);
 /* entries sent to / received from every rank at each re-shard: [n_ranks] each */
 qp_status qp_shard_counts(const qp_plan *plan, int64_t *send_counts, int64_t *recv_counts);
-/* After qp_init + qp_steps(1, L) on the full ARDM: copy this rank's segment-0 blocks to d_local. */
-qp_status qp_shard_extract(qp_plan *plan, const void *d_full, void *d_local, void *stream);
-/* Steps k_begin..k_end-1 inside the current segment on the local blocks (fused, readout partials). */
-qp_status qp_shard_steps(qp_plan *plan, int64_t k_begin, int64_t k_end, void *d_local, void *d_work, void *stream,
-                         int64_t *n_launch);
-/* Re-shard from segment j to j+1: pack local -> send (rank-major), unpack recv -> local (advances j). */
-qp_status qp_shard_pack(qp_plan *plan, const void *d_local, void *d_send, void *stream);
-qp_status qp_shard_unpack(qp_plan *plan, const void *d_recv, void *d_local, void *stream);
+/* Enqueue steps k_begin .. k_end-1 in order: growth (k < L, not mixed with slide steps in one call)
+   or slide steps inside the current segment.  d_local, d_xbuf: device, local_entries / xbuf_entries
+   complex entries, caller-owned.  Errors: QP_ERR_ARG (order, segment bounds), QP_ERR_CUDA. */
+qp_status qp_shard_steps(qp_plan *plan, int64_t k_begin, int64_t k_end, void *d_local, void *d_xbuf, void *d_work,
+                         void *stream, int64_t *n_launch);
+/* Re-shard from segment j to j + 1 (at the segment's end): pack d_local -> d_xbuf in send order
+   [destination rank][my block][destination's combo of Z_{j+1}][other slots]; after the caller's
+   all-to-all into d_local, unpack d_local -> d_xbuf ([source rank][source's combo of Z_j][my new
+   block][other slots] -> the segment j+1 layout) and advance j.  The caller then swaps d_local and
+   d_xbuf. */
+qp_status qp_shard_pack(qp_plan *plan, const void *d_local, void *d_xbuf, void *stream);
+qp_status qp_shard_unpack(qp_plan *plan, const void *d_recv, void *d_xbuf, void *stream);
+/* [sync] rho of the whole sharded run: d_parts (device, [n_ranks][n_out][M*M], every rank's rho block
+   of its d_work in rank order, e.g. from an all-gather) -> rho_out (host [n_out][M][M]): rank 0's value
+   for steps k <= L - z, the rank-ordered sum for later steps (fixed order: deterministic). */
+qp_status qp_shard_combine(const qp_plan *plan, const void *d_parts, void *d_work, qp_c64 *rho_out, void *stream);
+/* Device address offset (bytes) of the rho block [n_out][M*M] inside d_work (for gathering it). */
+int64_t qp_rho_offset(const qp_plan *plan);
 
 /* ---------------------------------------------------------------- device eta setup
    Host-setup step a3 on the GPU: every eta class of Eqs. 10-16 (Strang windows, DESIGN.md

@@ -82,34 +82,173 @@ cudaError_t launch_grow(int M, bool lattice, const GrowArgs &a, int grid, cudaSt
     }
 }
 
-// ============================================================================================
-// Re-shard data movement (multi-GPU path): one generic digit-permutation copy.
-// The dense side index i is a mixed-radix number over `nf` fields (innermost first); field f has
-// radix rad[f] and contributes to the strided side's address either linearly (ncd[f] == 0:
-// value * str[f][0]) or as a combo of ncd[f] base-N digits of (lo[f] + value) with strides
-// str[f][0..ncd-1].  gather: dst[i] = src[addr(i)];  scatter: dst[addr(i)] = src[i].
-// ============================================================================================
-
-template <int N>
-__global__ void __launch_bounds__(256) k_permute(const PermuteArgs a) {
+// --------------------------------------------------------------------------------------------
+// Sharded growth (multi-GPU): the last z growth steps k = L-z .. L-1 add the z digits
+// that are the shard slots of segment 0, so a rank only produces the entries of its own combos c
+// (digits c_0..c_{z-1} of slots L-z..L-1).  Every launch reads the replicated A_{L-z-1} (N^(L-z)
+// entries, grown in the exchange buffer) and recomputes the chain of growth factors of the combo
+// prefix: step i (k = L-z+i) reduces the readout rho(t_k) from A_{k-1} -- for i = 0 the replicated
+// tensor (every rank holds the complete sum), for i >= 1 the entries with prefix (c_0..c_{i-1}),
+// counted on the rank owning the combo c = prefix (the smallest combo with that prefix) -- and the
+// last step writes the rank's blocks: local[c - c_lo][x] = A_{L-1}[x, c].  No rank ever holds N^L.
+// --------------------------------------------------------------------------------------------
+template <int M, bool LAT, bool RO>
+__global__ void __launch_bounds__(256) k_grow_shard(const __grid_constant__ GrowShardArgs a) {
+    constexpr int N = M * M;
+    constexpr int D = n_classes(M, LAT);
+    const SmallLayout lay{N, D, a.L};
+    __shared__ double2 sK[2][N][N];
+    for (int i = threadIdx.x; i < 2 * N * N; i += 256) (&sK[0][0][0])[i] = a.small[lay.kp(0) + i];
+    __syncthreads();
+    const int L = a.L, z = a.z, i = a.step, kb = L - z;  // this launch: step k = kb + i
+    double2 acc[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) acc[n] = make_double2(0.0, 0.0);
     const long long stride = (long long)gridDim.x * 256;
-    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < a.count; i += stride) {
-        long long rest = i, addr = a.base;
-        for (int f = 0; f < a.nf; ++f) {
-            const long long v = rest % a.rad[f];
-            rest /= a.rad[f];
-            if (a.ncd[f] == 0) {
-                addr += v * a.str[f][0];
+    for (long long x = (long long)blockIdx.x * 256 + threadIdx.x; x < a.nb; x += stride) {
+        const double2 base = a.Abase[x];
+        int dx[kMaxL];  // digits of x (positions 0 .. kb-1)
+        {
+            long long r = x;
+            for (int q = 0; q < kb; ++q) { dx[q] = (int)(r % N); r /= N; }
+        }
+        // Psi_k (kap 0: propagate, 1: terminal) over the partners at lags j = 1..k: position k - j
+        auto psi_of = [&](int k, int kap, const int *dc) {
+            double2 p = make_double2(0.0, 0.0);
+            for (int j = 1; j <= k; ++j) {
+                const int q = k - j;
+                const int d = q < kb ? dx[q] : dc[q - kb];
+                p = cadd(p, __ldg(&a.small[lay.psi(kap) + ((size_t)k * L + j) * N + d]));
+            }
+            return p;
+        };
+        // A_{kb-1+m}[x, c_0..c_{m-1}]: the growth chain of steps kb .. kb+m-1
+        auto chain = [&](const int *dc, int m) {
+            double2 v = base;
+            for (int t = 0; t < m; ++t) {
+                const int k = kb + t, nw = dc[t], last = t == 0 ? dx[kb - 1] : dc[t - 1];
+                const int c = class_of(M, LAT, nw / M, nw % M);
+                double2 f = sK[0][nw][last];
+                if (c > 0) {
+                    const double2 p = psi_of(k, 0, dc);
+                    f = cmul(f, cexp_(make_double2(a.delta[c - 1] * p.x, a.delta[c - 1] * p.y)));
+                }
+                v = cmul(f, v);
+            }
+            return v;
+        };
+        auto readout = [&](const int *dc, double2 v) {  // rho(t_k) contribution of A_{k-1} entry v
+            const int k = kb + i, last = i == 0 ? dx[kb - 1] : dc[i - 1];
+            const double2 p = psi_of(k, 1, dc);
+            double2 e[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) e[d] = cexp_(make_double2(a.delta[d] * p.x, a.delta[d] * p.y));
+#pragma unroll
+            for (int aa = 0; aa < M; ++aa)
+#pragma unroll
+                for (int bb = 0; bb < M; ++bb) {
+                    const int nw = aa * M + bb, c = class_of(M, LAT, aa, bb);
+                    const double2 ft = c == 0 ? sK[1][nw][last] : cmul(sK[1][nw][last], e[c > 0 ? c - 1 : 0]);
+                    acc[nw] = cfma(ft, v, acc[nw]);
+                }
+        };
+        int dc[4];
+        if (RO) {
+            if (i == 0) {
+                readout(dc, base);
             } else {
-                long long c = a.lo[f] + v;
-                for (int j = 0; j < a.ncd[f]; ++j) {
-                    addr += (c % N) * a.str[f][j];
-                    c /= N;
+                long long np = 1;
+                for (int t = 0; t < i; ++t) np *= N;
+                for (int c = a.c_lo; c < a.c_lo + a.n_own && c < np; ++c) {
+                    int r = c;
+                    for (int t = 0; t < z; ++t) { dc[t] = r % N; r /= N; }
+                    readout(dc, chain(dc, i));
                 }
             }
         }
-        if (a.scatter) a.dst[addr] = __ldcs(a.src + i);
-        else a.dst[i] = __ldcs(a.src + addr);
+        if (i == z - 1)
+            for (int b = 0; b < a.n_own; ++b) {
+                int r = a.c_lo + b;
+                for (int t = 0; t < z; ++t) { dc[t] = r % N; r /= N; }
+                a.local[(long long)b * a.nb + x] = chain(dc, z);
+            }
+    }
+    if (RO) reduce_finalize<N, 256>(acc, a.partials, a.rho, a.counter);
+}
+
+template <int M, bool LAT>
+static cudaError_t grow_shard_t(const GrowShardArgs &a, int grid, cudaStream_t s) {
+    if (a.rho) k_grow_shard<M, LAT, true><<<grid, 256, 0, s>>>(a);
+    else k_grow_shard<M, LAT, false><<<grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grow_shard(int M, bool lattice, const GrowShardArgs &a, int grid, cudaStream_t s) {
+    switch (M) {
+    case 2: return grow_shard_t<2, false>(a, grid, s);
+    case 3: return lattice ? grow_shard_t<3, true>(a, grid, s) : grow_shard_t<3, false>(a, grid, s);
+    case 4: return lattice ? grow_shard_t<4, true>(a, grid, s) : grow_shard_t<4, false>(a, grid, s);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+// Cross-rank readout (multi-GPU): parts[g][o][n] are the ranks' rho(t_k) of output o in rank order
+// (gathered by the caller); rho[o][n] = parts[0][o][n] for outputs complete on every rank (step
+// k <= L - z: replicated growth), else the sum over g = 0..G-1 in rank order (deterministic).
+__global__ void k_shard_combine(const double2 *parts, double2 *rho, const long long *steps, long long n_out, int N,
+                                int G, long long k_rep) {
+    const long long n = n_out * N;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+        double2 s = parts[t];
+        if (steps[t / N] > k_rep)
+            for (int g = 1; g < G; ++g) s = cadd(s, parts[(long long)g * n + t]);
+        rho[t] = s;
+    }
+}
+
+cudaError_t launch_shard_combine(const double2 *parts, double2 *rho, const long long *steps, long long n_out, int N, int G,
+                                 long long k_rep, cudaStream_t s) {
+    if (n_out <= 0) return cudaSuccess;
+    const int grid = (int)std::min<long long>((n_out * N + 255) / 256, 1024);
+    k_shard_combine<<<grid, 256, 0, s>>>(parts, rho, steps, n_out, N, G, k_rep);
+    return cudaGetLastError();
+}
+
+// ============================================================================================
+// Re-shard data movement (multi-GPU path): one digit-permutation copy.  The dense
+// side index i is a mixed-radix number: nd base-N digit fields (innermost first, division by the
+// compile-time N), then up to two combo fields of radix crad[c] whose value v is either a linear
+// field (cnd = 0: v * cstr[c][0]) or the base-N digits of (clo + v) with strides cstr[c][0..cnd-1].
+// gather: dst[i] = src[addr(i)];  scatter: dst[addr(i)] = src[i].  No runtime 64-bit division.
+// ============================================================================================
+
+template <int N>
+__global__ void __launch_bounds__(256) k_permute(const __grid_constant__ PermuteArgs a) {
+    const long long stride = (long long)gridDim.x * 256;
+    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < a.count; i += stride) {
+        long long addr = 0;
+        unsigned long long rest = (unsigned long long)i;
+        for (int f = 0; f < a.nd; ++f) {
+            const unsigned long long q = rest / N;  // compile-time N: multiply-high
+            addr += (long long)(rest - q * N) * a.dstr[f];
+            rest = q;
+        }
+        unsigned r32 = (unsigned)rest;  // combo fields: < 2^32 (checked on the host)
+        for (int c = 0; c < a.ncombo; ++c) {
+            const unsigned v = r32 % (unsigned)a.crad[c];
+            r32 /= (unsigned)a.crad[c];
+            if (a.cnd[c] == 0) {
+                addr += (long long)v * a.cstr[c][0];
+            } else {
+                unsigned cc = (unsigned)a.clo[c] + v;
+                for (int t = 0; t < a.cnd[c]; ++t) {
+                    addr += (long long)(cc % N) * a.cstr[c][t];
+                    cc /= N;
+                }
+            }
+        }
+        if (a.scatter) __stcs(a.dst + addr, __ldcs(a.src + i));
+        else __stcs(a.dst + i, __ldcs(a.src + addr));
     }
 }
 

@@ -392,7 +392,7 @@ struct qp_plan {
         std::vector<LaunchSet> sets;                 // shard launch sets
         std::map<std::tuple<int, int, int>, size_t> index;  // (zstart, p0, S) -> sets
         int64_t seg = 0;                             // current segment
-        bool extracted = false;
+        int Smax = 1;                                // fusion depth inside segments
     } sh;
     int64_t seg_begin(int64_t j) const { return L + j * sh.seg_len; }
     std::vector<int> zset(int64_t j) const {         // shard slots of segment j, ascending
@@ -1171,7 +1171,7 @@ qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
     P->ardm_entries = ipow(P->N, P->L);
     P->max_bytes = pr->max_bytes;
     const double need = 16.0 * double(P->ardm_entries) + double(P->work_bytes);
-    if ((st = check_capacity(pr->max_bytes, need, "ARDM + workspace"))) {
+    if (pr->max_bytes > 0 && (st = check_capacity(pr->max_bytes, need, "ARDM + workspace"))) {  // explicit budget
         delete P;
         return st;
     }
@@ -1181,6 +1181,13 @@ qp_status qp_plan_create(const qp_problem *pr, qp_plan **out) {
 }
 
 void qp_plan_destroy(qp_plan *P) { delete P; }
+
+qp_status qp_plan_check(const qp_plan *P) {
+    if (!P) return err(QP_ERR_ARG, "arg: NULL plan");
+    const double need = P->sh.on ? 2.0 * 16.0 * double(P->sh.n_own[P->sh.rank] * P->sh.blk) + double(P->work_bytes)
+                                 : 16.0 * double(P->ardm_entries) + double(P->work_bytes);
+    return check_capacity(P->max_bytes, need, P->sh.on ? "two shard buffers + workspace" : "ARDM + workspace");
+}
 
 qp_status qp_plan_query(const qp_plan *P, qp_sizes *o) {
     if (!P || !o) return err(QP_ERR_ARG, "arg: NULL plan or out");
@@ -1307,7 +1314,6 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
     }
     P->next_k = 1;
     P->sh.seg = 0;
-    P->sh.extracted = false;
     P->inited = true;
     return QP_OK;
 }
@@ -1317,6 +1323,7 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
     if (n_launch) *n_launch = 0;
     if (!P || !d_ardm || !d_work) return err(QP_ERR_ARG, "arg: NULL plan or device buffer");
     if (!P->inited) return err(QP_ERR_ARG, "arg: qp_init must be called before qp_steps");
+    if (P->sh.on) return err(QP_ERR_ARG, "arg: sharded plan: use qp_shard_steps");
     if (k_begin != P->next_k || k_end < k_begin || k_end > P->n_steps + 1)
         return err(QP_ERR_ARG, "arg: steps must be enqueued in order: expected k_begin = %lld, k_end <= %lld",
                    (long long)P->next_k, (long long)P->n_steps + 1);
@@ -1473,19 +1480,37 @@ qp_status qp_shard_configure(qp_plan *P, int32_t n_ranks, int32_t rank) {
         if (std::find(starts.begin(), starts.end(), zs) != starts.end()) break;
         starts.push_back(zs);
     }
-    for (int zs : starts) {
-        std::vector<int> Z;
-        for (int i = 0; i < z; ++i) Z.push_back(((zs - 1 - i) % L + L) % L);
-        std::sort(Z.begin(), Z.end());
-        for (int m = 0; m < sh.seg_len; ++m)
-            for (int S = 1; S <= P->Smax && m + S <= sh.seg_len; ++S) {
-                const int p0 = (zs + m) % L;
-                sh.index[std::make_tuple(zs, p0, S)] = sh.sets.size();
-                sh.sets.emplace_back();
-                build_launch_set(*P, p0, S, Z, sh.sets.back());
-            }
+    // fusion depth of the segments: the plan's, or 3 when a four-step shard set has no k_fused4 layout
+    // (fewer than two outer digits in the local layout)
+    sh.Smax = P->Smax;
+    for (bool retry = true; retry;) {
+        retry = false;
+        sh.sets.clear();
+        sh.index.clear();
+        for (int zs : starts) {
+            std::vector<int> Z;
+            for (int i = 0; i < z; ++i) Z.push_back(((zs - 1 - i) % L + L) % L);
+            std::sort(Z.begin(), Z.end());
+            for (int m = 0; m < sh.seg_len && !retry; ++m)
+                for (int S = 1; S <= sh.Smax && m + S <= sh.seg_len; ++S) {
+                    const int p0 = (zs + m) % L;
+                    sh.index[std::make_tuple(zs, p0, S)] = sh.sets.size();
+                    sh.sets.emplace_back();
+                    build_launch_set(*P, p0, S, Z, sh.sets.back());
+                    if (S == 4 && !sh.sets.back().f4) { sh.Smax = 3; retry = true; break; }
+                }
+        }
     }
     compute_layout(*P);
+    // capacity (a1) against an explicit budget: two buffers of this rank's shard (local + exchange) +
+    // workspace (qp_plan_check compares with the device's free memory)
+    const double need = 2.0 * 16.0 * double(sh.n_own[rank] * sh.blk) + double(P->work_bytes);
+    if (P->max_bytes > 0 && check_capacity(P->max_bytes, need, "two shard buffers + workspace")) {
+        const qp_status st = QP_ERR_CAPACITY;
+        sh = qp_plan::Shard{};
+        compute_layout(*P);
+        return st;
+    }
     return QP_OK;
 }
 
@@ -1502,6 +1527,7 @@ qp_status qp_shard_query(const qp_plan *P, qp_shard_sizes *o) {
     for (int r = 0; r < sh.G; ++r) mx = std::max(mx, sh.n_own[r]);
     o->max_local_entries = mx * sh.blk;
     o->exchange_entries = sh.n_own[sh.rank] * sh.blk;  // everything moves (incl. the part kept locally)
+    o->xbuf_entries = std::max(o->local_entries, o->exchange_entries);
     o->work_bytes = (int64_t)P->work_bytes;
     return QP_OK;
 }
@@ -1518,164 +1544,197 @@ qp_status qp_shard_counts(const qp_plan *P, int64_t *send_counts, int64_t *recv_
     return QP_OK;
 }
 
-qp_status qp_shard_extract(qp_plan *P, const void *d_full, void *d_local, void *stream) {
-    if (!P || !d_full || !d_local) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
-    if (!P->sh.on || !P->inited) return err(QP_ERR_ARG, "arg: plan not sharded / not initialised");
-    if (P->next_k != P->L) return err(QP_ERR_ARG, "arg: extract after the growth steps 1..L-1 (next step %lld)", (long long)P->next_k);
-    const auto &sh = P->sh;
-    const std::vector<int> Z = P->zset(0);
-    qp::PermuteArgs a{};
-    a.dst = (double2 *)d_local;
-    a.src = (const double2 *)d_full;
-    a.count = sh.n_own[sh.rank] * sh.blk;
-    a.scatter = 0;
-    int f = 0;
-    for (int q = 0; q < P->L; ++q)
-        if (std::find(Z.begin(), Z.end(), q) == Z.end()) { a.rad[f] = P->N; a.ncd[f] = 0; a.str[f][0] = ipow(P->N, q); ++f; }
-    a.rad[f] = sh.n_own[sh.rank]; a.lo[f] = sh.c_lo[sh.rank]; a.ncd[f] = sh.z;
-    for (int i = 0; i < sh.z; ++i) a.str[f][i] = ipow(P->N, Z[i]);
-    a.nf = f + 1;
-    QP_CUDA(qp::launch_permute(P->M, a, P->sms, (cudaStream_t)stream));
-    P->sh.extracted = true;
-    return QP_OK;
-}
-
-qp_status qp_shard_pack(qp_plan *P, const void *d_local, void *d_send, void *stream) {
-    if (!P || !d_local || !d_send) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
-    if (!P->sh.on || !P->sh.extracted) return err(QP_ERR_ARG, "arg: plan not sharded / no local data");
+// Re-shard from segment j to j + 1 through the caller's two buffers (local L, exchange X):
+//   qp_shard_pack:   L -> X in send order [dst rank][my Z_j block][dst's Z_{j+1} combo][other slots]
+//   caller:          all-to-all X -> L (L is free once packed)
+//   qp_shard_unpack: L (received, [src rank][src's Z_j combo][my Z_{j+1} block][other]) -> X in the
+//                    segment j + 1 layout; the caller then swaps the two buffers (X is the new local).
+static qp_status shard_permute(qp_plan *P, bool pack, const void *src, void *dst, cudaStream_t st) {
     const auto &sh = P->sh;
     const std::vector<int> Z0 = P->zset(sh.seg), Z1 = P->zset(sh.seg + 1);
-    const std::vector<int> pos = local_pos(*P, Z0);
+    const std::vector<int> pos = local_pos(*P, pack ? Z0 : Z1);
+    const int64_t R = ipow(P->N, P->L - 2 * sh.z), me = sh.rank;
     int64_t off = 0;
     for (int r = 0; r < sh.G; ++r) {
         qp::PermuteArgs a{};
-        a.dst = (double2 *)d_send + off;
-        a.src = (const double2 *)d_local;
-        a.scatter = 0;
-        int f = 0;
+        a.scatter = pack ? 0 : 1;
+        a.nd = 0;
         for (int q = 0; q < P->L; ++q)  // the other slots, ascending
-            if (std::find(Z0.begin(), Z0.end(), q) == Z0.end() && std::find(Z1.begin(), Z1.end(), q) == Z1.end()) {
-                a.rad[f] = P->N; a.ncd[f] = 0; a.str[f][0] = ipow(P->N, pos[q]); ++f;
-            }
-        a.rad[f] = sh.n_own[r]; a.lo[f] = sh.c_lo[r]; a.ncd[f] = sh.z;  // destination's combos of Z_{j+1}
-        for (int i = 0; i < sh.z; ++i) a.str[f][i] = ipow(P->N, pos[Z1[i]]);
-        ++f;
-        a.rad[f] = sh.n_own[sh.rank]; a.ncd[f] = 0; a.str[f][0] = sh.blk;  // my blocks (combos of Z_j)
-        a.nf = f + 1;
-        a.count = sh.n_own[sh.rank] * sh.n_own[r] * ipow(P->N, P->L - 2 * sh.z);
-        QP_CUDA(qp::launch_permute(P->M, a, P->sms, (cudaStream_t)stream));
+            if (std::find(Z0.begin(), Z0.end(), q) == Z0.end() && std::find(Z1.begin(), Z1.end(), q) == Z1.end())
+                a.dstr[a.nd++] = ipow(P->N, pos[q]);
+        a.ncombo = 2;
+        if (pack) {  // gather from local: dst's combos of Z_{j+1} (digits), then my blocks (linear)
+            a.crad[0] = (int)sh.n_own[r], a.clo[0] = (int)sh.c_lo[r], a.cnd[0] = sh.z;
+            for (int i = 0; i < sh.z; ++i) a.cstr[0][i] = ipow(P->N, pos[Z1[i]]);
+            a.crad[1] = (int)sh.n_own[me], a.clo[1] = 0, a.cnd[1] = 0, a.cstr[1][0] = sh.blk;
+            a.count = sh.n_own[me] * sh.n_own[r] * R;
+            a.src = (const double2 *)src;
+            a.dst = (double2 *)dst + off;
+        } else {  // scatter into the new local: my new blocks (linear), then src's combos of Z_j (digits)
+            a.crad[0] = (int)sh.n_own[me], a.clo[0] = 0, a.cnd[0] = 0, a.cstr[0][0] = sh.blk;
+            a.crad[1] = (int)sh.n_own[r], a.clo[1] = (int)sh.c_lo[r], a.cnd[1] = sh.z;
+            for (int i = 0; i < sh.z; ++i) a.cstr[1][i] = ipow(P->N, pos[Z0[i]]);
+            a.count = sh.n_own[r] * sh.n_own[me] * R;
+            a.src = (const double2 *)src + off;
+            a.dst = (double2 *)dst;
+        }
+        QP_CUDA(qp::launch_permute(P->M, a, P->sms, st));
         off += a.count;
     }
     return QP_OK;
 }
 
-qp_status qp_shard_unpack(qp_plan *P, const void *d_recv, void *d_local, void *stream) {
-    if (!P || !d_recv || !d_local) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
-    if (!P->sh.on || !P->sh.extracted) return err(QP_ERR_ARG, "arg: plan not sharded / no local data");
-    auto &sh = P->sh;
-    const std::vector<int> Z0 = P->zset(sh.seg), Z1 = P->zset(sh.seg + 1);
-    const std::vector<int> pos = local_pos(*P, Z1);
-    int64_t off = 0;
-    for (int r = 0; r < sh.G; ++r) {
-        qp::PermuteArgs a{};
-        a.dst = (double2 *)d_local;
-        a.src = (const double2 *)d_recv + off;
-        a.scatter = 1;
-        int f = 0;
-        for (int q = 0; q < P->L; ++q)
-            if (std::find(Z0.begin(), Z0.end(), q) == Z0.end() && std::find(Z1.begin(), Z1.end(), q) == Z1.end()) {
-                a.rad[f] = P->N; a.ncd[f] = 0; a.str[f][0] = ipow(P->N, pos[q]); ++f;
-            }
-        a.rad[f] = sh.n_own[sh.rank]; a.ncd[f] = 0; a.str[f][0] = sh.blk;  // my new blocks (combos of Z_{j+1})
-        ++f;
-        a.rad[f] = sh.n_own[r]; a.lo[f] = sh.c_lo[r]; a.ncd[f] = sh.z;  // source's combos of Z_j
-        for (int i = 0; i < sh.z; ++i) a.str[f][i] = ipow(P->N, pos[Z0[i]]);
-        a.nf = f + 1;
-        a.count = sh.n_own[r] * sh.n_own[sh.rank] * ipow(P->N, P->L - 2 * sh.z);
-        QP_CUDA(qp::launch_permute(P->M, a, P->sms, (cudaStream_t)stream));
-        off += a.count;
-    }
-    sh.seg += 1;
+qp_status qp_shard_pack(qp_plan *P, const void *d_local, void *d_xbuf, void *stream) {
+    if (!P || !d_local || !d_xbuf) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
+    if (!P->sh.on || !P->inited) return err(QP_ERR_ARG, "arg: plan not sharded / not initialised");
+    if (P->next_k != P->seg_begin(P->sh.seg + 1))
+        return err(QP_ERR_ARG, "arg: pack at the end of a segment (next step %lld, segment ends at %lld)",
+                   (long long)P->next_k, (long long)P->seg_begin(P->sh.seg + 1));
+    return shard_permute(P, true, d_local, d_xbuf, (cudaStream_t)stream);
+}
+
+qp_status qp_shard_unpack(qp_plan *P, const void *d_recv, void *d_xbuf, void *stream) {
+    if (!P || !d_recv || !d_xbuf) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
+    if (!P->sh.on || !P->inited) return err(QP_ERR_ARG, "arg: plan not sharded / not initialised");
+    if (P->next_k != P->seg_begin(P->sh.seg + 1)) return err(QP_ERR_ARG, "arg: unpack follows a pack");
+    if (qp_status st = shard_permute(P, false, d_recv, d_xbuf, (cudaStream_t)stream)) return st;
+    P->sh.seg += 1;
     return QP_OK;
 }
 
-qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_local, void *d_work, void *stream,
-                         int64_t *n_launch) {
+qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_local, void *d_xbuf, void *d_work,
+                         void *stream, int64_t *n_launch) {
     if (n_launch) *n_launch = 0;
-    if (!P || !d_local || !d_work) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
+    if (!P || !d_local || !d_xbuf || !d_work) return err(QP_ERR_ARG, "arg: NULL plan or buffer");
     auto &sh = P->sh;
-    if (!sh.on || !sh.extracted) return err(QP_ERR_ARG, "arg: plan not sharded / no local data (qp_shard_extract)");
-    const int64_t s0 = P->seg_begin(sh.seg), s1 = s0 + sh.seg_len;
-    if (k_begin != P->next_k || k_begin < s0 || k_end > s1 || k_end < k_begin || k_end > P->n_steps + 1)
-        return err(QP_ERR_ARG, "arg: shard steps must be in order within segment [%lld, %lld), next step %lld",
-                   (long long)s0, (long long)s1, (long long)P->next_k);
+    if (!sh.on || !P->inited) return err(QP_ERR_ARG, "arg: plan not sharded (qp_shard_configure) / not initialised (qp_init)");
+    const int L = P->L, N = P->N, kb = L - sh.z;
+    if (k_begin != P->next_k || k_end < k_begin || k_end > P->n_steps + 1)
+        return err(QP_ERR_ARG, "arg: shard steps must be enqueued in order: expected k_begin = %lld", (long long)P->next_k);
+    if (k_begin >= L) {
+        const int64_t s0 = P->seg_begin(sh.seg), s1 = s0 + sh.seg_len;
+        if (k_begin < s0 || k_end > s1)
+            return err(QP_ERR_ARG, "arg: slide steps stay within segment [%lld, %lld) (re-shard between segments)",
+                       (long long)s0, (long long)s1);
+    } else if (k_end > L) {
+        return err(QP_ERR_ARG, "arg: growth steps (k < %d) and slide steps in separate calls", L);
+    }
     cudaStream_t s = (cudaStream_t)stream;
     char *w = (char *)d_work;
-    const int L = P->L, N = P->N;
-    const std::vector<int> Z = P->zset(sh.seg);
-    const int zs = (int)(s0 % L);
+    const double2 *small = (const double2 *)(w + P->off_small);
+    double2 *part = (double2 *)(w + P->off_part);
+    unsigned *cnt = (unsigned *)(w + P->off_cnt);
     int64_t launched = 0;
     for (int64_t k = k_begin; k < k_end;) {
-        const int64_t grp_end = s0 + ((k - s0) / P->Smax + 1) * P->Smax;
-        const int S = (int)(std::min<int64_t>({grp_end, k_end, s1}) - k);
-        const int p0 = (int)(k % L);
-        const auto it = sh.index.find(std::make_tuple(zs, p0, S));
-        if (it == sh.index.end()) return err(QP_ERR_ARG, "internal: no shard launch set for (%d, %d, %d)", zs, p0, S);
-        const qp_plan::LaunchSet &ls = sh.sets[it->second];
-        for (int64_t b = 0; b < sh.n_own[sh.rank]; ++b) {
-            qp::FusedArgs a = ls.args;
-            a.A = (double2 *)d_local + b * sh.blk;
-            a.small = (const double2 *)(w + P->off_small);
-            a.inner = (const double2 *)(w + ls.off_inner);
-            a.Etab = (const double2 *)(w + ls.off_E);
-            a.goff = (const long long *)(w + ls.off_goff);
-            a.lofs = (const int2 *)(w + ls.off_lofs);
-            a.partials = (double2 *)(w + P->off_part);
-            a.counter = (unsigned *)(w + P->off_cnt);
-            a.rho_accumulate = b > 0 ? 1 : 0;
-            if (qp_status st = set_tma(*P, ls, a, a.A, w)) return st;
-            int dig[8];
-            shard_combo_digits(*P, sh.c_lo[sh.rank] + b, dig);
-            bool ro = false;
-            const qp::SmallLayout lay{N, P->D, L};
-            for (int st = 0; st < S; ++st) {
-                const int64_t slot = P->slot_of(k + st);
-                a.rho[st] = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * N : nullptr;
-                ro |= slot >= 0;
-                const int var = (k + st == L) ? 1 : 0;
-                a.var[st] = var;
-                if (P->sym)
-                    for (int kap = 0; kap < 2; ++kap) {
-                        const double2 c = P->small[lay.beta(var, kap) + 0];
-                        const double rho = P->small[lay.beta(var, kap) + 1].x;
-                        a.sym[st][kap][0] = c.x;
-                        a.sym[st][kap][1] = c.y;
-                        a.sym[st][kap][2] = 0.5 * (rho + 1.0 / rho);
-                        a.sym[st][kap][3] = 0.5 * (rho - 1.0 / rho);
-                    }
-                // fixed shard-slot digits: their Eq. 9 factor for this sub-step (propagate / terminal)
-                for (int kap = 0; kap < 2; ++kap) {
-                    cd Ps = 0.0;
-                    for (int i = 0; i < sh.z; ++i) {
-                        const int lag = ((p0 + st - Z[i]) % L + L) % L;
-                        Ps += psi(*P, dig[i], kap == 0 ? P->eta[lag] : P->E[lag]);
-                    }
-                    for (int d = 0; d < P->D; ++d) a.fixfac[st][kap][d] = d2(std::exp(P->delta[d] * Ps));
-                }
-            }
-            const int qlast = (p0 - 1 + L) % L;
-            a.fixed_last = -1;
-            for (int i = 0; i < sh.z; ++i)
-                if (Z[i] == qlast) a.fixed_last = dig[i];
-            const cudaError_t e = launch_slide(*P, S, a, ro, launch_grid(P, S, a), s);
-            if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: shard launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
+        if (k < kb) {  // replicated growth on the exchange buffer: N^(k+1) <= N^(L-z) entries
+            const int64_t slot = P->slot_of(k);
+            qp::GrowArgs g{};
+            g.A = (double2 *)d_xbuf; g.small = small; g.partials = part; g.counter = cnt;
+            g.rho = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * N : nullptr;
+            g.n_in = ipow(N, (int)k);
+            g.k = (int)k;
+            g.L = L;
+            for (int d = 0; d < P->D; ++d) g.delta[d] = P->delta[d];
+            const int grid = (int)std::min<int64_t>({(g.n_in + 255) / 256, (int64_t)P->sms * 8, (int64_t)qp::kPartialsMax});
+            QP_CUDA(qp::launch_grow(P->M, P->lattice, g, std::max(1, grid), s));
             ++launched;
+            ++k;
+        } else if (k < L) {  // the z growth steps that add the shard digits: this rank's combos only
+            const int64_t slot = P->slot_of(k);
+            qp::GrowShardArgs g{};
+            g.Abase = (const double2 *)d_xbuf;
+            g.local = (double2 *)d_local;
+            g.small = small; g.partials = part; g.counter = cnt;
+            g.rho = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * N : nullptr;
+            g.nb = sh.blk;
+            g.L = L, g.z = sh.z, g.step = (int)(k - kb), g.n_own = (int)sh.n_own[sh.rank], g.c_lo = (int)sh.c_lo[sh.rank];
+            for (int d = 0; d < P->D; ++d) g.delta[d] = P->delta[d];
+            const int grid = (int)std::min<int64_t>({(g.nb + 255) / 256, (int64_t)P->sms * 8, (int64_t)qp::kPartialsMax});
+            QP_CUDA(qp::launch_grow_shard(P->M, P->lattice, g, std::max(1, grid), s));
+            ++launched;
+            ++k;
+        } else {  // slide steps of the current segment, one launch per owned block
+            const int64_t s0 = P->seg_begin(sh.seg);
+            const int64_t grp_end = s0 + ((k - s0) / sh.Smax + 1) * sh.Smax;
+            const int S = (int)(std::min<int64_t>({grp_end, k_end, s0 + sh.seg_len}) - k);
+            const int p0 = (int)(k % L);
+            const std::vector<int> Z = P->zset(sh.seg);
+            const int zs = (int)(s0 % L);
+            const auto it = sh.index.find(std::make_tuple(zs, p0, S));
+            if (it == sh.index.end()) return err(QP_ERR_ARG, "internal: no shard launch set for (%d, %d, %d)", zs, p0, S);
+            const qp_plan::LaunchSet &ls = sh.sets[it->second];
+            for (int64_t b = 0; b < sh.n_own[sh.rank]; ++b) {
+                qp::FusedArgs a = ls.args;
+                a.A = (double2 *)d_local + b * sh.blk;
+                a.small = small;
+                a.inner = (const double2 *)(w + ls.off_inner);
+                a.Etab = (const double2 *)(w + ls.off_E);
+                a.goff = (const long long *)(w + ls.off_goff);
+                a.lofs = (const int2 *)(w + ls.off_lofs);
+                a.partials = part;
+                a.counter = cnt;
+                a.rho_accumulate = b > 0 ? 1 : 0;
+                if (qp_status st = set_tma(*P, ls, a, a.A, w)) return st;
+                int dig[8];
+                shard_combo_digits(*P, sh.c_lo[sh.rank] + b, dig);
+                bool ro = false;
+                const qp::SmallLayout lay{N, P->D, L};
+                for (int st = 0; st < S; ++st) {
+                    const int64_t slot = P->slot_of(k + st);
+                    a.rho[st] = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * N : nullptr;
+                    ro |= slot >= 0;
+                    const int var = (k + st == L) ? 1 : 0;
+                    a.var[st] = var;
+                    if (P->sym)
+                        for (int kap = 0; kap < 2; ++kap) {
+                            const double2 c = P->small[lay.beta(var, kap) + 0];
+                            const double rho = P->small[lay.beta(var, kap) + 1].x;
+                            a.sym[st][kap][0] = c.x;
+                            a.sym[st][kap][1] = c.y;
+                            a.sym[st][kap][2] = 0.5 * (rho + 1.0 / rho);
+                            a.sym[st][kap][3] = 0.5 * (rho - 1.0 / rho);
+                        }
+                    // fixed shard-slot digits: their Eq. 9 factor for this sub-step (propagate / terminal)
+                    for (int kap = 0; kap < 2; ++kap) {
+                        cd Ps = 0.0;
+                        for (int i = 0; i < sh.z; ++i) {
+                            const int lag = ((p0 + st - Z[i]) % L + L) % L;
+                            Ps += psi(*P, dig[i], kap == 0 ? P->eta[lag] : P->E[lag]);
+                        }
+                        for (int d = 0; d < P->D; ++d) a.fixfac[st][kap][d] = d2(std::exp(P->delta[d] * Ps));
+                    }
+                }
+                const int qlast = (p0 - 1 + L) % L;
+                a.fixed_last = -1;
+                for (int i = 0; i < sh.z; ++i)
+                    if (Z[i] == qlast) a.fixed_last = dig[i];
+                const cudaError_t e = launch_slide(*P, S, a, ro, launch_grid(P, S, a), s);
+                if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: shard launch of step %lld failed: %s", (long long)k, cudaGetErrorString(e));
+                ++launched;
+            }
+            k += S;
         }
-        k += S;
         P->next_k = k;
     }
     if (n_launch) *n_launch = launched;
     return QP_OK;
+}
+
+int64_t qp_rho_offset(const qp_plan *P) { return P ? (int64_t)P->off_rho : -1; }
+
+qp_status qp_shard_combine(const qp_plan *P, const void *d_parts, void *d_work, qp_c64 *rho_out, void *stream) {
+    if (!P || !d_parts || !d_work || !rho_out) return err(QP_ERR_ARG, "arg: NULL plan, buffer or output");
+    if (!P->sh.on) return err(QP_ERR_ARG, "arg: plan is not sharded");
+    cudaStream_t s = (cudaStream_t)stream;
+    char *w = (char *)d_work;
+    const int64_t n_out = (int64_t)P->out_steps.size();
+    if (n_out == 0) return QP_OK;
+    // out_steps on the device (after the rho block), then the rank-ordered sum into the rho block
+    long long *d_steps = (long long *)(w + P->off_cnt + 256);
+    QP_CUDA(cudaMemcpyAsync(d_steps, P->out_steps.data(), n_out * sizeof(long long), cudaMemcpyHostToDevice, s));
+    QP_CUDA(qp::launch_shard_combine((const double2 *)d_parts, (double2 *)(w + P->off_rho), d_steps, n_out, P->N, P->sh.G,
+                                     P->L - P->sh.z, s));
+    return qp_read_rho(P, d_work, rho_out, s);
 }
 
 }  // extern "C"

@@ -88,21 +88,37 @@ struct FusedArgs {
 };
 
 
-// Generic digit-permutation copy for the re-shard (grow.cu: k_permute).
+// Digit-permutation copy for the re-shard (grow.cu: k_permute): nd base-N digit fields, then up to
+// two combo fields (radix crad, value lo + v as cnd base-N digits, or cnd = 0: linear stride).
 constexpr int kMaxFields = kMaxL + 4;
 struct PermuteArgs {
     double2 *dst;
     const double2 *src;
     long long count;         // dense-side entries
-    long long base;          // address offset on the strided side
-    int nf;                  // fields, innermost first
     int scatter;             // 0: dst[i] = src[addr(i)], 1: dst[addr(i)] = src[i]
-    long long rad[kMaxFields];
-    long long lo[kMaxFields];
-    int ncd[kMaxFields];     // 0 = linear field, else number of base-N digits of the combo (lo + value)
-    long long str[kMaxFields][4];
+    int nd;                  // digit fields, innermost first
+    long long dstr[kMaxFields];
+    int ncombo;
+    int crad[2], clo[2], cnd[2];
+    long long cstr[2][4];
 };
 cudaError_t launch_permute(int M, const PermuteArgs &a, int sms, cudaStream_t s);
+
+// Sharded growth (grow.cu: k_grow_shard): step k = L - z + step from the replicated A_{L-z-1}.
+struct GrowShardArgs {
+    const double2 *Abase;    // A_{L-z-1}: N^(L-z) entries
+    double2 *local;          // [n_own][N^(L-z)] (written by the last step)
+    const double2 *small;
+    double2 *partials;
+    double2 *rho;            // readout of step k, or nullptr
+    unsigned *counter;
+    long long nb;            // N^(L-z)
+    int L, z, step, n_own, c_lo;
+    double delta[kMaxD];
+};
+cudaError_t launch_grow_shard(int M, bool lattice, const GrowShardArgs &a, int grid, cudaStream_t s);
+cudaError_t launch_shard_combine(const double2 *parts, double2 *rho, const long long *steps, long long n_out, int N, int G,
+                                 long long k_rep, cudaStream_t s);
 
 // Per-launch arguments of the growth step k (1 <= k < L): A_{k-1} (N^k) -> A_k (N^(k+1)).
 struct GrowArgs {

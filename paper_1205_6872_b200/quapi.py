@@ -78,7 +78,7 @@ class qp_shard_sizes(ctypes.Structure):
     _fields_ = [
         ("n_ranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("shard_slots", ctypes.c_int32),
         ("segment_steps", ctypes.c_int32), ("local_entries", ctypes.c_int64), ("max_local_entries", ctypes.c_int64),
-        ("exchange_entries", ctypes.c_int64), ("work_bytes", ctypes.c_int64),
+        ("exchange_entries", ctypes.c_int64), ("work_bytes", ctypes.c_int64), ("xbuf_entries", ctypes.c_int64),
     ]
 
 
@@ -102,8 +102,8 @@ class qp_batch_sizes(ctypes.Structure):
 # Every symbol include/quapi.h declares (tests check the library exports all of them).
 EXPORTS = ("qp_plan_create", "qp_plan_query", "qp_plan_eta", "qp_plan_propagator", "qp_init", "qp_steps",
            "qp_read_rho", "qp_run", "qp_last_error", "qp_plan_destroy", "qp_version",
-           "qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_extract", "qp_shard_steps",
-           "qp_shard_pack", "qp_shard_unpack", "qp_batch_create", "qp_batch_query", "qp_batch_run",
+           "qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_steps",
+           "qp_shard_pack", "qp_shard_unpack", "qp_shard_combine", "qp_rho_offset", "qp_plan_check", "qp_batch_create", "qp_batch_query", "qp_batch_run",
            "qp_batch_destroy", "qp_eta_device")
 
 _lib = None
@@ -137,12 +137,15 @@ def lib() -> ctypes.CDLL:
         L.qp_shard_configure.argtypes = [vp, ctypes.c_int32, ctypes.c_int32]
         L.qp_shard_query.argtypes = [vp, ctypes.POINTER(qp_shard_sizes)]
         L.qp_shard_counts.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
-        L.qp_shard_extract.argtypes = [vp, vp, vp, vp]
-        L.qp_shard_steps.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp, ctypes.POINTER(ctypes.c_int64)]
+        L.qp_shard_steps.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_int64)]
         L.qp_shard_pack.argtypes = [vp, vp, vp, vp]
         L.qp_shard_unpack.argtypes = [vp, vp, vp, vp]
-        for f in ("qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_extract", "qp_shard_steps",
-                  "qp_shard_pack", "qp_shard_unpack"):
+        L.qp_shard_combine.argtypes = [vp, vp, vp, ctypes.POINTER(qp_c64), vp]
+        L.qp_rho_offset.argtypes = [vp]
+        L.qp_rho_offset.restype = ctypes.c_int64
+        L.qp_plan_check.argtypes = [vp]
+        for f in ("qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_steps",
+                  "qp_shard_pack", "qp_shard_unpack", "qp_shard_combine", "qp_plan_check"):
             getattr(L, f).restype = ctypes.c_int
         L.qp_batch_create.argtypes = [ctypes.POINTER(qp_batch), PP]
         L.qp_batch_query.argtypes = [vp, ctypes.POINTER(qp_batch_sizes)]
@@ -294,9 +297,14 @@ class Plan:
         _check(lib().qp_plan_propagator(self._h, buf))
         return _to_numpy(buf, (self.w.M, self.w.M))
 
+    def check(self):
+        """Capacity (a1) of the plan as configured against max_bytes or the device's free memory."""
+        _check(lib().qp_plan_check(self._h))
+
     # ---- device-side calls (PyTorch tensors own the memory; the caller's stream is passed through)
     def alloc(self, device="cuda"):
         import torch
+        self.check()
         sz = self.sizes
         ardm = torch.empty(sz.ardm_entries * 2, dtype=torch.float64, device=device)
         work = torch.empty((sz.work_bytes + 7) // 8, dtype=torch.float64, device=device)
@@ -353,25 +361,35 @@ class Plan:
         _check(lib().qp_shard_counts(self._h, snd, rcv))
         return list(snd), list(rcv)
 
-    def shard_extract(self, full, local, stream=None):
-        _check(lib().qp_shard_extract(self._h, ctypes.c_void_p(full.data_ptr()), ctypes.c_void_p(local.data_ptr()),
-                                      ctypes.c_void_p(self._stream_ptr(stream))))
-
-    def shard_steps(self, k_begin: int, k_end: int, local, work, stream=None) -> int:
+    def shard_steps(self, k_begin: int, k_end: int, local, xbuf, work, stream=None) -> int:
         n = ctypes.c_int64(0)
         _check(lib().qp_shard_steps(self._h, int(k_begin), int(k_end), ctypes.c_void_p(local.data_ptr()),
-                                    ctypes.c_void_p(work.data_ptr()), ctypes.c_void_p(self._stream_ptr(stream)),
-                                    ctypes.byref(n)))
+                                    ctypes.c_void_p(xbuf.data_ptr()), ctypes.c_void_p(work.data_ptr()),
+                                    ctypes.c_void_p(self._stream_ptr(stream)), ctypes.byref(n)))
         self.launches += n.value
         return n.value
 
-    def shard_pack(self, local, send, stream=None):
-        _check(lib().qp_shard_pack(self._h, ctypes.c_void_p(local.data_ptr()), ctypes.c_void_p(send.data_ptr()),
+    def shard_pack(self, local, xbuf, stream=None):
+        _check(lib().qp_shard_pack(self._h, ctypes.c_void_p(local.data_ptr()), ctypes.c_void_p(xbuf.data_ptr()),
                                    ctypes.c_void_p(self._stream_ptr(stream))))
 
-    def shard_unpack(self, recv, local, stream=None):
-        _check(lib().qp_shard_unpack(self._h, ctypes.c_void_p(recv.data_ptr()), ctypes.c_void_p(local.data_ptr()),
+    def shard_unpack(self, recv, xbuf, stream=None):
+        _check(lib().qp_shard_unpack(self._h, ctypes.c_void_p(recv.data_ptr()), ctypes.c_void_p(xbuf.data_ptr()),
                                      ctypes.c_void_p(self._stream_ptr(stream))))
+
+    def rho_block(self, work):
+        """Device view (float64, 2 * n_out * N) of the plan's rho outputs inside the workspace."""
+        off = lib().qp_rho_offset(self._h) // 8
+        n = 2 * len(self.out_steps) * self.w.N
+        return work[off:off + n]
+
+    def shard_combine(self, parts, work, stream=None) -> np.ndarray:
+        """rho of a sharded run from every rank's rho block (device tensor [n_ranks, 2 n_out N] in rank order)."""
+        n = len(self.out_steps)
+        buf = (qp_c64 * max(1, n * self.w.N))()
+        _check(lib().qp_shard_combine(self._h, ctypes.c_void_p(parts.data_ptr()), ctypes.c_void_p(work.data_ptr()), buf,
+                                      ctypes.c_void_p(self._stream_ptr(stream))))
+        return _to_numpy(buf, (n, self.w.M, self.w.M))[:n]
 
 
 class BatchPlan:

@@ -176,3 +176,38 @@ def test_batch_per_problem_bath_validation():
         Q.BatchPlan(w, 2, baths=[(1, 0.1, 7.5, 0.2)])
     bp = Q.BatchPlan(w, 2, baths=[(1, 0.1, 7.5, 0.2), (2, 0.1, 7.5, 0.2)])
     assert bp.sizes.work_bytes > Q.BatchPlan(w, 2).sizes.work_bytes
+
+
+def test_shard_plan_L17_over_8_ranks_fits_two_shard_buffers():
+    """L = 17 (4^17 entries, 275 GB) is the smallest M = 2 case that needs sharding.  Over 8
+    ranks each holds two shard buffers of 4^17 / 8 entries (~69 GB) + workspace -- never the full ARDM."""
+    w = W.spin_boson(L=17, n_steps=40)
+    for rank in (0, 7):
+        pl = Q.Plan(w)
+        s = pl.shard(8, rank)
+        assert s.shard_slots == 2 and s.segment_steps == 15
+        assert s.local_entries == 4 ** 17 // 8 and s.xbuf_entries == s.local_entries
+        per_rank = 2 * 16 * s.local_entries + s.work_bytes
+        assert per_rank < 2 * 16 * 4 ** 17 / 8 * 1.01
+        snd, rcv = pl.shard_counts()
+        assert sum(snd) == sum(rcv) == s.local_entries
+
+
+def test_shard_configure_misuse_is_an_error():
+    """qp_shard_configure is host setup: twice, or after qp_init, returns QP_ERR_ARG (no silent
+    re-layout of an initialised workspace)."""
+    pl = Q.Plan(W.random_problem(3, 2, 6, 20))
+    pl.shard(2, 0)
+    with pytest.raises(Q.QuapiError) as ei:
+        pl.shard(2, 1)
+    assert ei.value.status == Q.QP_ERR_ARG
+
+
+def test_negative_n_out_is_rejected():
+    import ctypes
+    w = W.random_problem(3, 2, 4, 10)
+    keep = []
+    pr = Q._problem(w, keep, out_steps=[1, 2])
+    pr.n_out = -1
+    h = ctypes.c_void_p()
+    assert Q.lib().qp_plan_create(ctypes.byref(pr), ctypes.byref(h)) == Q.QP_ERR_CONFIG
