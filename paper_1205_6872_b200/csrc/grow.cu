@@ -222,14 +222,19 @@ cudaError_t launch_shard_combine(const double2 *parts, double2 *rho, const long 
 // gather: dst[i] = src[addr(i)];  scatter: dst[addr(i)] = src[i].  No runtime 64-bit division.
 // ============================================================================================
 
+// One thread per row = the N entries of the innermost digit field: the dense side is contiguous
+// (32-byte vector accesses), the strided side steps by dstr[0] (also 32-byte pairs when dstr[0] == 1);
+// the row's strided address is decomposed once per N entries.
 template <int N>
 __global__ void __launch_bounds__(256) k_permute(const __grid_constant__ PermuteArgs a) {
+    const long long rows = a.count / N;
     const long long stride = (long long)gridDim.x * 256;
-    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < a.count; i += stride) {
+    const long long s0 = a.dstr[0];
+    for (long long row = (long long)blockIdx.x * 256 + threadIdx.x; row < rows; row += stride) {
         long long addr = 0;
-        unsigned long long rest = (unsigned long long)i;
-        for (int f = 0; f < a.nd; ++f) {
-            const unsigned long long q = rest / N;  // compile-time N: multiply-high
+        unsigned long long rest = (unsigned long long)row;
+        for (int f = 1; f < a.nd; ++f) {
+            const unsigned long long q = rest / N;  // compile-time N: multiply-high / shift
             addr += (long long)(rest - q * N) * a.dstr[f];
             rest = q;
         }
@@ -247,14 +252,45 @@ __global__ void __launch_bounds__(256) k_permute(const __grid_constant__ Permute
                 }
             }
         }
-        if (a.scatter) __stcs(a.dst + addr, __ldcs(a.src + i));
-        else __stcs(a.dst + i, __ldcs(a.src + addr));
+        const long long dense = row * N;
+        if constexpr (N % 2 == 0) {
+            if (s0 == 1) {  // both sides contiguous along the row
+                const double2 *src = a.src + (a.scatter ? dense : addr);
+                double2 *dst = a.dst + (a.scatter ? addr : dense);
+#pragma unroll
+                for (int v = 0; v < N; v += 2) {
+                    double2 x, y;
+                    ld2_cs(src + v, x, y);
+                    st2_cs(dst + v, x, y);
+                }
+                continue;
+            }
+            double2 buf[N];
+            if (a.scatter) {
+#pragma unroll
+                for (int v = 0; v < N; v += 2) ld2_cs(a.src + dense + v, buf[v], buf[v + 1]);
+#pragma unroll
+                for (int v = 0; v < N; ++v) __stcs(a.dst + addr + v * s0, buf[v]);
+            } else {
+#pragma unroll
+                for (int v = 0; v < N; ++v) buf[v] = __ldcs(a.src + addr + v * s0);
+#pragma unroll
+                for (int v = 0; v < N; v += 2) st2_cs(a.dst + dense + v, buf[v], buf[v + 1]);
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < N; ++v) {
+                if (a.scatter) __stcs(a.dst + addr + v * s0, __ldcs(a.src + dense + v));
+                else __stcs(a.dst + dense + v, __ldcs(a.src + addr + v * s0));
+            }
+        }
     }
 }
 
 cudaError_t launch_permute(int M, const PermuteArgs &a, int sms, cudaStream_t s) {
     if (a.count <= 0) return cudaSuccess;
-    const int grid = (int)std::min<long long>((a.count + 255) / 256, (long long)sms * 16);
+    if (a.nd < 1 || a.count % (M * M)) return cudaErrorInvalidValue;  // rows of the innermost digit field
+    const int grid = (int)std::min<long long>((a.count / (M * M) + 255) / 256, (long long)sms * 16);
     switch (M) {
     case 2: k_permute<4><<<grid, 256, 0, s>>>(a); break;
     case 3: k_permute<9><<<grid, 256, 0, s>>>(a); break;
