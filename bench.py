@@ -143,6 +143,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=3)
+    ap.add_argument("--fuse-steps", type=int, default=0, help="cap on the steps fused per pass (0: the library's choice)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -177,7 +178,7 @@ def main():
     K, Wm, L = args.steps, max(args.warmup, 3), base.L
     n_total = L - 1 + Wm + K  # growth steps, then W warm-up and K timed slide steps
     w = base.with_(n_steps=n_total)
-    plan = Q.Plan(w)  # allPoints readout: every step reduces rho(t_k)
+    plan = Q.Plan(w, fuse_steps=args.fuse_steps)  # allPoints readout: every step reduces rho(t_k)
     sz = plan.sizes
     ardm, work = plan.alloc()
     stream = torch.cuda.current_stream()

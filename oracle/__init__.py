@@ -55,6 +55,8 @@ class _Problem(ctypes.Structure):
         ("G_in", ctypes.POINTER(ctypes.c_double)),
         ("reading", ctypes.c_int32),
         ("H_t", ctypes.POINTER(ctypes.c_double)),
+        ("filter_theta", ctypes.c_double),
+        ("kept", ctypes.POINTER(ctypes.c_int64)),
     ]
 
 
@@ -109,6 +111,8 @@ class Problem:
     G_in: Optional[np.ndarray] = None
     reading: int = READING_STRANG
     H_t: Optional[np.ndarray] = None  # [n_steps, M, M]: H on interval (t_{k-1}, t_k] of step k
+    filter_theta: float = 0.0         # path filtering threshold (0: none); reading C.3-15
+    kept: Optional[np.ndarray] = None  # int64 [n_steps + 1] output: nonzero entries of A_k after filtering
     _keep: list = field(default_factory=list, repr=False)
 
     @property
@@ -132,11 +136,16 @@ class Problem:
                 raise ValueError("H_t must have shape [n_steps, M, M]")
             keep.append(ha)
             ht = _dptr(ha)
+        kp = None
+        if self.kept is not None:
+            if self.kept.dtype != np.int64 or self.kept.size != int(self.n_steps) + 1:
+                raise ValueError("kept must be int64 [n_steps + 1]")
+            kp = self.kept.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
         self._keep = keep
         return _Problem(
             self.M, _dptr(s), _dptr(H), _dptr(r), int(self.kind), float(self.coupling),
             float(self.omega_c), float(self.kT), float(self.dt), int(self.n_steps), int(self.L),
-            g, int(self.reading), ht,
+            g, int(self.reading), ht, float(self.filter_theta), kp,
         )
 
 

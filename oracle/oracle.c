@@ -610,6 +610,11 @@ int or_run(const or_problem *p, const int64_t *out_steps, int64_t n_out, double 
     }
     /* A_0(sigma_0) = rho0(sigma_0) I(sigma_0, sigma_0; eta_00),  eta_00 = G(1/2) (Eq. 13, reading C.3-2) */
     for (int sg = 0; sg < N; ++sg) A[sg] = c.rho0[sg] * infl(&c, sg, sg, eta_of(&ec, 0, 0, INT64_MAX));
+    if (p->kept) {
+        int64_t nz = 0;
+        for (int sg = 0; sg < N; ++sg) nz += (A[sg] != 0);
+        p->kept[0] = nz;
+    }
     double t_setup = now_s() - t0, t_grow = 0.0, t_slide = 0.0;
     int64_t n_slide = 0;
     int w_old = 1;
@@ -659,6 +664,21 @@ int or_run(const or_problem *p, const int64_t *out_steps, int64_t n_out, double 
                     B[y] = f * s;
                 }
             }
+        }
+        /* path filtering (reading C.3-15): drop the entries of A_k below theta in magnitude */
+        if (p->filter_theta > 0.0) {
+            const double th2 = p->filter_theta * p->filter_theta;
+#pragma omp parallel for schedule(static)
+            for (int64_t y = 0; y < n_new; ++y) {
+                const double re = creal(B[y]), im = cimag(B[y]);
+                if (re * re + im * im < th2) B[y] = 0;
+            }
+        }
+        if (p->kept) {
+            int64_t nz = 0;
+#pragma omp parallel for schedule(static) reduction(+ : nz)
+            for (int64_t y = 0; y < n_new; ++y) nz += (B[y] != 0);
+            p->kept[k] = nz;
         }
         cplx *tmp = A; A = B; B = tmp;
         w_old = w_new;

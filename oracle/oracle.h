@@ -40,6 +40,12 @@ typedef struct {
     const double *H_t;     /* optional [n_steps][M*M*2]: time-dependent Hamiltonian, H_t[k-1] acts on
                               the interval (t_{k-1}, t_k] of step k (the driven model of Sec. III,
                               Omega(t) of P:288); NULL => H on every interval        */
+    double filter_theta;   /* path filtering (Sim's on-the-fly filtered propagator, cited P:99-103,
+                              invited P:265-271; reading C.3-15): after every
+                              propagation step k >= 1 the entries of A_k with |A|^2 < theta^2 are set
+                              to 0.  0 => no filtering (bit-identical to the plain run)             */
+    int64_t *kept;         /* optional [n_steps + 1]: kept[k] = nonzero entries of A_k after filtering
+                              (k = 0 .. the last propagated step; rho(t_n) needs A_{n-1} only)      */
 } or_problem;
 
 /* G(tau) = int_0^tau dt' int_0^t' dt'' alpha(t'-t'')  (Eq. 4 integrated twice). */
