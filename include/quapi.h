@@ -224,6 +224,23 @@ qp_status qp_shard_combine(const qp_plan *plan, const void *d_parts, void *d_wor
 /* Device address offset (bytes) of the rho block [n_out][M*M] inside d_work (for gathering it). */
 int64_t qp_rho_offset(const qp_plan *plan);
 
+/* ---------------------------------------------------------------- path filtering
+   Sim's on-the-fly filtering of paths, cited by the paper as the way to cut the tensor propagator's
+   memory, absent from its program and invited.  Reading C.3-15
+   (DESIGN.md): after every step k >= 1 the entries of A_k with |A|^2 < theta^2 are dropped; rho(t_k)
+   is read from the filtered A_{k-1}; theta = 0 keeps every entry.  The ARDM is a compacted list of
+   (index, value) of the kept entries (24 B each, ping-pong) instead of the dense 16 N^L B: growth and
+   slide steps are count / scan / scatter passes over the list (ofpf.cu). */
+/* Device bytes of the filter buffer for a list of up to `capacity` entries. */
+qp_status qp_filter_query(const qp_plan *plan, int64_t capacity, int64_t *bytes);
+/* [sync] Whole filtered run (init, steps 1..n_steps, readouts): d_buf (device, buf_bytes, caller-owned)
+   holds the list, d_work (work_bytes) the plan's tables and outputs; rho_out host [n_out][M][M];
+   kept_out (host [n_steps + 1] or NULL): entries of the list after each step (kept_out[0]: the nonzero
+   entries of A_0).  Errors: QP_ERR_ARG, QP_ERR_CAPACITY (the list outgrew the buffer: message names the
+   step), QP_ERR_CUDA. */
+qp_status qp_filter_run(qp_plan *plan, double theta, void *d_buf, int64_t buf_bytes, void *d_work, void *stream,
+                        qp_c64 *rho_out, int64_t *kept_out);
+
 /* ---------------------------------------------------------------- device eta setup
    Host-setup step a3 on the GPU: every eta class of Eqs. 10-16 (Strang windows, DESIGN.md
    reading C.3-1) for B baths at once -- the setup the paper names as the bottleneck once propagation

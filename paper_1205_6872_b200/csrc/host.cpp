@@ -1722,6 +1722,135 @@ qp_status qp_shard_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_loc
 
 int64_t qp_rho_offset(const qp_plan *P) { return P ? (int64_t)P->off_rho : -1; }
 
+// ===================================================================================== path filtering
+// SURVEY 8(f3), reading C.3-15 (ofpf.cu): the ARDM as a compacted (key, value) list of the entries with
+// |A|^2 >= theta^2, ping-ponged between two halves of the caller's buffer.
+namespace {
+struct FilterLayout {
+    size_t key[2], val[2], flags, blkcnt, blkbase, tab, ctr, kept, total;
+};
+FilterLayout filter_layout(const qp_plan *P, int64_t cap, int nblk) {
+    FilterLayout f{};
+    size_t off = 0;
+    for (int h = 0; h < 2; ++h) { f.key[h] = off; off = align256(off + (size_t)cap * 8); }
+    for (int h = 0; h < 2; ++h) { f.val[h] = off; off = align256(off + (size_t)cap * 16); }
+    f.flags = off;   off = align256(off + (size_t)cap * 2);
+    f.blkcnt = off;  off = align256(off + (size_t)nblk * P->N * 4);
+    f.blkbase = off; off = align256(off + (size_t)nblk * P->N * 8);
+    f.tab = off;     off = align256(off + (size_t)2 * (qp::kMaxL + 1) * P->N * 16);
+    f.ctr = off;     off = align256(off + 4 * 8);  // n[0], n[1], overflow
+    f.kept = off;    off = align256(off + (size_t)(P->n_steps + 1) * 8);
+    f.total = off;
+    return f;
+}
+constexpr int kFilterBlocksPerSM = 4;
+}  // namespace
+
+qp_status qp_filter_query(const qp_plan *P, int64_t capacity, int64_t *bytes) {
+    if (!P || !bytes || capacity < 1) return err(QP_ERR_ARG, "arg: NULL plan / output or capacity < 1");
+    *bytes = (int64_t)filter_layout(P, capacity, 148 * kFilterBlocksPerSM * 2).total;  // room for up to 296 SMs
+    return QP_OK;
+}
+
+qp_status qp_filter_run(qp_plan *P, double theta, void *d_buf, int64_t buf_bytes, void *d_work, void *stream,
+                        qp_c64 *rho_out, int64_t *kept_out) {
+    if (!P || !d_buf || !d_work || !rho_out) return err(QP_ERR_ARG, "arg: NULL plan, buffer or output");
+    if (!(theta >= 0.0) || !std::isfinite(theta)) return err(QP_ERR_ARG, "arg: theta must be finite and >= 0");
+    if (P->sh.on) return err(QP_ERR_ARG, "arg: path filtering runs unsharded");
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    QP_CUDA(cudaGetDevice(&dev));
+    QP_CUDA(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
+    const int nblk = P->sms * kFilterBlocksPerSM;
+    // largest capacity that fits the buffer
+    // 50 B per list entry (two keys, two values, one flag word) + fixed tables and 256-B alignment slack
+    const int64_t fixed = (int64_t)filter_layout(P, 1, nblk).total + 8 * 256;
+    int64_t cap = std::max<int64_t>(1, (buf_bytes - fixed) / 50);
+    while (cap > 1 && (int64_t)filter_layout(P, cap, nblk).total > buf_bytes) --cap;
+    const FilterLayout f = filter_layout(P, cap, nblk);
+    if ((int64_t)f.total > buf_bytes) return err(QP_ERR_CAPACITY, "capacity: filter buffer of %lld B too small", (long long)buf_bytes);
+    char *b = (char *)d_buf, *w = (char *)d_work;
+    const int N = P->N, L = P->L;
+    // tables: small (K', beta, growth psi rows) into the workspace, slide partner psi rows into the buffer
+    QP_CUDA(cudaMemcpyAsync(w + P->off_small, P->small.data(), P->small.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+    std::vector<double2> tab((size_t)2 * (qp::kMaxL + 1) * N, make_double2(0.0, 0.0));
+    for (int lag = 1; lag <= L; ++lag)
+        for (int sg = 0; sg < N; ++sg) {
+            tab[(size_t)(0 * (qp::kMaxL + 1) + lag) * N + sg] = d2(psi(*P, sg, P->eta[lag]));
+            tab[(size_t)(1 * (qp::kMaxL + 1) + lag) * N + sg] = d2(psi(*P, sg, P->E[lag]));
+        }
+    QP_CUDA(cudaMemcpyAsync(b + f.tab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+    QP_CUDA(cudaMemsetAsync(w + P->off_cnt, 0, 256, s));
+    QP_CUDA(cudaMemsetAsync(b + f.ctr, 0, 4 * 8, s));
+    QP_CUDA(cudaMemsetAsync(b + f.kept, 0, (size_t)(P->n_steps + 1) * 8, s));
+    // A_0: its nonzero entries (exact zeros contribute nothing), keys sigma_0
+    std::vector<long long> k0;
+    std::vector<double2> v0;
+    for (int sg = 0; sg < N; ++sg)
+        if (P->A0[sg] != cd(0.0, 0.0)) { k0.push_back(sg); v0.push_back(d2(P->A0[sg])); }
+    const long long n0 = (long long)k0.size();
+    if (n0 > cap) return err(QP_ERR_CAPACITY, "capacity: filter buffer too small");
+    if (n0) {
+        QP_CUDA(cudaMemcpyAsync(b + f.key[0], k0.data(), n0 * 8, cudaMemcpyHostToDevice, s));
+        QP_CUDA(cudaMemcpyAsync(b + f.val[0], v0.data(), n0 * 16, cudaMemcpyHostToDevice, s));
+    }
+    QP_CUDA(cudaMemcpyAsync(b + f.ctr, &n0, 8, cudaMemcpyHostToDevice, s));
+    QP_CUDA(cudaMemcpyAsync(b + f.kept, &n0, 8, cudaMemcpyHostToDevice, s));
+    QP_CUDA(cudaStreamSynchronize(s));  // the host staging vectors above go out of scope
+    const int64_t slot0 = P->slot_of(0);
+    if (slot0 >= 0) {
+        std::vector<double2> r0(N);
+        for (int i = 0; i < N; ++i) r0[i] = d2(P->rho0[i]);
+        QP_CUDA(cudaMemcpyAsync(w + P->off_rho + slot0 * N * sizeof(double2), r0.data(), N * sizeof(double2), cudaMemcpyHostToDevice, s));
+        QP_CUDA(cudaStreamSynchronize(s));
+    }
+    long long *ctr = (long long *)(b + f.ctr);
+    for (int64_t k = 1; k <= P->n_steps; ++k) {
+        const int h = (int)((k - 1) & 1);
+        qp::OfpfArgs a{};
+        a.key_in = (const long long *)(b + f.key[h]);
+        a.val_in = (const double2 *)(b + f.val[h]);
+        a.key_out = (long long *)(b + f.key[h ^ 1]);
+        a.val_out = (double2 *)(b + f.val[h ^ 1]);
+        a.n_in = ctr + h;
+        a.n_out = ctr + (h ^ 1);
+        a.flags = (unsigned short *)(b + f.flags);
+        a.blkcnt = (int *)(b + f.blkcnt);
+        a.blkbase = (long long *)(b + f.blkbase);
+        a.kept = (long long *)(b + f.kept) + k;
+        a.overflow = (int *)(ctr + 2);
+        a.cap = cap;
+        a.small = (const double2 *)(w + P->off_small);
+        a.tab = (const double2 *)(b + f.tab);
+        a.partials = (double2 *)(w + P->off_part);
+        a.counter = (unsigned *)(w + P->off_cnt);
+        const int64_t slot = P->slot_of(k);
+        a.rho = slot >= 0 ? (double2 *)(w + P->off_rho) + slot * N : nullptr;
+        a.th2 = theta * theta;
+        a.top = ipow(N, L - 1);
+        a.grow_w = k < L ? ipow(N, (int)k) : 0;
+        a.k = (int)std::min<int64_t>(k, L);
+        a.L = L;
+        a.slide = k >= L ? 1 : 0;
+        a.var = (k == L) ? 1 : 0;
+        for (int d = 0; d < P->D; ++d) a.delta[d] = P->delta[d];
+        const cudaError_t e = qp::launch_ofpf_step(P->M, P->lattice, a, nblk, s);
+        if (e != cudaSuccess) return err(QP_ERR_CUDA, "cuda: filtered step %lld: %s", (long long)k, cudaGetErrorString(e));
+    }
+    long long hctr[3];
+    QP_CUDA(cudaMemcpyAsync(hctr, ctr, 3 * 8, cudaMemcpyDeviceToHost, s));
+    std::vector<long long> kept((size_t)P->n_steps + 1);
+    QP_CUDA(cudaMemcpyAsync(kept.data(), b + f.kept, kept.size() * 8, cudaMemcpyDeviceToHost, s));
+    QP_CUDA(cudaStreamSynchronize(s));
+    if (((int *)&hctr[2])[0]) {
+        int64_t kk = 0;
+        for (size_t i = 0; i < kept.size(); ++i) if (kept[i] > cap) { kk = (int64_t)i; break; }
+        return err(QP_ERR_CAPACITY, "capacity: the filtered ARDM exceeded %lld entries at step %lld", (long long)cap, (long long)kk);
+    }
+    if (kept_out) for (size_t i = 0; i < kept.size(); ++i) kept_out[i] = kept[i];
+    return qp_read_rho(P, d_work, rho_out, s);
+}
+
 qp_status qp_shard_combine(const qp_plan *P, const void *d_parts, void *d_work, qp_c64 *rho_out, void *stream) {
     if (!P || !d_parts || !d_work || !rho_out) return err(QP_ERR_ARG, "arg: NULL plan, buffer or output");
     if (!P->sh.on) return err(QP_ERR_ARG, "arg: plan is not sharded");

@@ -154,6 +154,33 @@ int fused4_occupancy(bool sym);
 int fused4_layout_type(const int (&lpos)[11], const int (&spos)[11], int q1swap, int q2swap, int swz);
 cudaError_t launch_fused4(bool sym, const FusedArgs &a, bool ro, int grid, cudaStream_t s);
 
+// Path-filtered step (ofpf.cu): one growth or slide step on the compacted list.
+struct OfpfArgs {
+    const long long *key_in;
+    const double2 *val_in;
+    long long *key_out;
+    double2 *val_out;
+    const long long *n_in;   // device: entries of the input list
+    long long *n_out;        // device: entries of the output list (written by the scan)
+    unsigned short *flags;   // [cap]: keep flags of the N outputs of the group headed by entry i
+    int *blkcnt;             // [nblk][N]
+    long long *blkbase;      // [nblk][N]
+    long long *kept;         // device: kept[k]
+    int *overflow;           // device: set when the output exceeds cap
+    long long cap;
+    const double2 *small;    // SmallLayout (K', beta, growth psi rows)
+    const double2 *tab;      // [2][kMaxL + 1][N]: psi(sigma'; eta_lag) / psi(sigma'; E_lag) (slide partners)
+    double2 *partials;
+    double2 *rho;            // readout of step k, or nullptr
+    unsigned *counter;
+    double th2;              // theta^2
+    long long top;           // N^(L-1)
+    long long grow_w;        // growth: N^k
+    int k, L, slide, var;
+    double delta[kMaxD];
+};
+cudaError_t launch_ofpf_step(int M, bool lattice, const OfpfArgs &a, int nblk, cudaStream_t s);
+
 // Batched sweeps (batch.cu): B independent problems, one CTA each, every step in one launch.
 // Table image (double2 entries) at `tab`: psi_eta[L+1][N], psi_E[L+1][N], psi_TI[L+1][N] (lag j = 1..L;
 // psi(sigma', e) = -(e s+(sigma') - conj(e) s-(sigma'))), psi_self[2][N] (self interior G(1), self end

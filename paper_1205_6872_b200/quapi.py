@@ -103,7 +103,8 @@ class qp_batch_sizes(ctypes.Structure):
 EXPORTS = ("qp_plan_create", "qp_plan_query", "qp_plan_eta", "qp_plan_propagator", "qp_init", "qp_steps",
            "qp_read_rho", "qp_run", "qp_last_error", "qp_plan_destroy", "qp_version",
            "qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_steps",
-           "qp_shard_pack", "qp_shard_unpack", "qp_shard_combine", "qp_rho_offset", "qp_plan_check", "qp_batch_create", "qp_batch_query", "qp_batch_run",
+           "qp_shard_pack", "qp_shard_unpack", "qp_shard_combine", "qp_rho_offset", "qp_plan_check",
+           "qp_filter_query", "qp_filter_run", "qp_batch_create", "qp_batch_query", "qp_batch_run",
            "qp_batch_destroy", "qp_eta_device")
 
 _lib = None
@@ -144,6 +145,11 @@ def lib() -> ctypes.CDLL:
         L.qp_rho_offset.argtypes = [vp]
         L.qp_rho_offset.restype = ctypes.c_int64
         L.qp_plan_check.argtypes = [vp]
+        L.qp_filter_query.argtypes = [vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+        L.qp_filter_run.argtypes = [vp, ctypes.c_double, vp, ctypes.c_int64, vp, vp, ctypes.POINTER(qp_c64),
+                                    ctypes.POINTER(ctypes.c_int64)]
+        L.qp_filter_query.restype = ctypes.c_int
+        L.qp_filter_run.restype = ctypes.c_int
         for f in ("qp_shard_configure", "qp_shard_query", "qp_shard_counts", "qp_shard_steps",
                   "qp_shard_pack", "qp_shard_unpack", "qp_shard_combine", "qp_plan_check"):
             getattr(L, f).restype = ctypes.c_int
@@ -376,6 +382,29 @@ class Plan:
     def shard_unpack(self, recv, xbuf, stream=None):
         _check(lib().qp_shard_unpack(self._h, ctypes.c_void_p(recv.data_ptr()), ctypes.c_void_p(xbuf.data_ptr()),
                                      ctypes.c_void_p(self._stream_ptr(stream))))
+
+    # ---- path filtering: compacted ARDM of the entries with |A| >= theta
+    def filter_bytes(self, capacity: int) -> int:
+        nb = ctypes.c_int64(0)
+        _check(lib().qp_filter_query(self._h, int(capacity), ctypes.byref(nb)))
+        return nb.value
+
+    def filter_run(self, theta: float, capacity: Optional[int] = None, device="cuda", stream=None):
+        """Filtered run: returns (rho [n_out, M, M], kept [n_steps + 1]: list entries after each step).
+        ``capacity``: list entries the buffer holds (default N^L, the dense worst case)."""
+        import torch
+        cap = int(capacity) if capacity is not None else self.sizes.ardm_entries
+        nbytes = self.filter_bytes(cap)
+        buf = torch.empty((nbytes + 7) // 8, dtype=torch.float64, device=device)
+        work = torch.empty((self.sizes.work_bytes + 7) // 8, dtype=torch.float64, device=device)
+        n = len(self.out_steps)
+        rho = (qp_c64 * max(1, n * self.w.N))()
+        kept = np.zeros(self.w.n_steps + 1, dtype=np.int64)
+        _check(lib().qp_filter_run(self._h, float(theta), ctypes.c_void_p(buf.data_ptr()), int(buf.numel() * 8),
+                                   ctypes.c_void_p(work.data_ptr()), ctypes.c_void_p(self._stream_ptr(stream)), rho,
+                                   kept.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        self.filter_buffer_bytes = int(buf.numel() * 8)
+        return _to_numpy(rho, (n, self.w.M, self.w.M))[:n], kept
 
     def rho_block(self, work):
         """Device view (float64, 2 * n_out * N) of the plan's rho outputs inside the workspace."""
