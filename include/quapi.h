@@ -88,8 +88,8 @@ typedef struct {
                                 (no check when no device is visible); < 0 => no check           */
     const qp_c64 *eta_in;    /* QP_J_ETA_TABLE only: [3*dkmax+2] eta classes, qp_plan_eta order   */
     int32_t fuse_steps;      /* cap on the time steps fused into one pass over the ARDM, 0..4;
-                                0 => the library's choice (4 for M = 2 with L >= 6, else 3; 1 for
-                                M = 3, 4).  Results
+                                0 => the library's choice (4 for M = 2 with L >= 6, else 3; 2 for
+                                M = 3; 1 for M = 4).  Results
                                 agree to rounding for every choice.                              */
     uint32_t flags;          /* QP_FLAG_* below; 0 for the default plan                          */
 } qp_problem;

@@ -103,6 +103,16 @@ __device__ __forceinline__ int fib_digit(int s, int r, int i) {  // digit i (i !
     return 0;
 }
 
+// ---- cp.async (LDGSTS) 16-byte copies global -> shared
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NPEND> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(NPEND) : "memory");
+}
+
 // ---- TMA (cp.async.bulk / cp.async.bulk.tensor) + mbarrier + 256-bit streaming access (sm_100a PTX)
 __device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {

@@ -567,6 +567,7 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
 // order (block partials) is deterministic.
 static int slide_path(int S, const qp::FusedArgs &a) { return S == 3 ? (a.use_tma ? 2 : (a.lane_map & 1)) : 0; }
 static int slide_occupancy(const qp_plan &P, int S, int path) {
+    if (P.M == 3 && S == 2) return qp::fused2s_occupancy(P.lattice);
     if (P.M == 2 && S == 4) return qp::fused4_occupancy(P.sym);
     if (P.M == 2 && S == 3) return qp::fused3_occupancy(P.sym, path & 1, path == 2);
     return qp::fused_r_occupancy(P.M, P.lattice, P.sym, S);
@@ -578,6 +579,15 @@ static int launch_grid(qp_plan *P, int S, const qp::FusedArgs &a) {
     return std::max(1, std::min<int>({a.n_tiles, P->sms * o, qp::kPartialsMax}));
 }
 static cudaError_t launch_slide(const qp_plan &P, int S, const qp::FusedArgs &a, bool ro, int grid, cudaStream_t s) {
+    if (P.M == 3 && S == 2) {
+        qp::Beta2s b{};
+        const qp::SmallLayout lay{P.N, P.D, P.L};
+        for (int st = 0; st < 2; ++st)
+            for (int kap = 0; kap < 2; ++kap)
+                for (int d = 0; d < P.D; ++d)
+                    for (int v = 0; v < P.N; ++v) b.b[st][kap][d][v] = P.small[lay.beta(a.var[st], kap) + d * P.N + v];
+        return qp::launch_fused2s(P.lattice, a, b, ro, grid, s);
+    }
     if (P.M == 2 && S == 4) return qp::launch_fused4(P.sym, a, ro, grid, s);
     if (P.M == 2 && S == 3) return qp::launch_fused3(P.sym, a, ro, grid, s);
     return qp::launch_fused_r(P.M, P.lattice, P.sym, S, a, ro, grid, s);
@@ -803,8 +813,8 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     const int nout = (int)outer.size();
     // tile digits: the kernel's preferred v, lowered (not below its minimum) so that small problems
     // still have >= ~2 tiles per SM of a 148-SM B200 to spread over the persistent grid
-    const bool f3 = (M == 2 && S == 3), f4 = (M == 2 && S == 4);
-    int v = std::min(f4 ? 4 : (f3 ? qp::kFused3TileDigits : qp::fused_r_tile_digits(M, S)), nout);
+    const bool f3 = (M == 2 && S == 3), f4 = (M == 2 && S == 4), f2s = (M == 3 && S == 2);
+    int v = std::min(f4 ? 4 : (f3 ? qp::kFused3TileDigits : (f2s ? 3 : qp::fused_r_tile_digits(M, S))), nout);
     const int vmin = std::min(f4 ? 2 : (f3 ? qp::kFused3TileDigitsMin : (N >= 9 ? 2 : 3)), nout);
     while (v > vmin && std::pow((double)N, nout - v) < 2.0 * 148) --v;
     const int w = std::max(1, P.group_w);
@@ -1014,7 +1024,7 @@ void build_tables(qp_plan &P, int fuse_cap) {
     // M = 2: four fused steps per pass (k_fused4, TMA load and store) when the outer slots hold at
     // least two digits (L >= 6), else three (k_fused3)
     const int s2 = (L >= 6 && !(P.flags & QP_FLAG_NO_TMA)) ? 4 : 3;
-    P.Smax = std::max(1, std::min(M == 2 ? s2 : 1, L - 1));
+    P.Smax = std::max(1, std::min(M == 2 ? s2 : (M == 3 ? 2 : 1), L - 1));
     if (fuse_cap > 0) P.Smax = std::min(P.Smax, fuse_cap);
     P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
     {  // the L * Smax launch sets are independent (read-only plan, own tables): build them on host threads
@@ -1309,7 +1319,8 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
         qp::FusedArgs a = ls.args;
         a.use_tma = ls.tma_a != -1;
         P->grid[P->Smax] = launch_grid(P, P->Smax, a);
-        P->block = (P->M == 2 && P->Smax == 4) ? qp::fused4_block()
+        P->block = (P->M == 3 && P->Smax == 2) ? qp::fused2s_block()
+                   : (P->M == 2 && P->Smax == 4) ? qp::fused4_block()
                    : (P->M == 2 && P->Smax == 3) ? qp::fused3_block(a.lane_map, a.use_tma) : qp::fused_r_block(P->M, P->Smax);
     }
     P->next_k = 1;

@@ -146,6 +146,15 @@ int fused3_block(int lane_map, bool tma);
 int fused3_round_fibres(int lane_map, bool tma);  // outer fibres per round (8 per warp)
 int fused3_occupancy(bool sym, int lane_map, bool tma);
 cudaError_t launch_fused3(bool sym, const FusedArgs &a, bool ro, int grid, cudaStream_t s);
+// k_fused2s (slide2.cu): M = 3, S = 2, shared-memory-staged units of 32 outer fibres
+int fused2s_block();
+int fused2s_occupancy(bool lattice);
+// class weights beta of both sub-steps, passed by value (kernel parameter space: the moment loop takes
+// them as constant-bank operands): [s][kap][d][old], copied from SmallLayout::beta(var[s], kap)
+struct Beta2s {
+    double2 b[2][2][kMaxM * (kMaxM - 1) < 6 ? kMaxM * (kMaxM - 1) : 6][9];
+};
+cudaError_t launch_fused2s(bool lattice, const FusedArgs &a, const Beta2s &b, bool ro, int grid, cudaStream_t s);
 // k_fused4 (slide4.cu): M = 2, S = 4, TMA load + store of 8-fibre rounds, warp-specialised
 int fused4_block();
 int fused4_round_fibres();

@@ -175,7 +175,7 @@ def test_fusion_depths(fuse, M, L, n, generic):
     for lat in (True, False) if M > 2 else (True,):
         w = W.random_problem(300 + 10 * M + L, M, L, n, kind=W.J_DEBYE, lattice_s=lat)
         rg, plan, _ = gpu_run(w, fuse_steps=fuse, flags=flags)
-        assert plan.sizes.fuse_steps == (min(fuse, L - 1, 4 if L >= 6 else 3) if M == 2 else 1)
+        assert plan.sizes.fuse_steps == min(fuse, L - 1, (4 if L >= 6 else 3) if M == 2 else (2 if M == 3 else 1))
         check(rg, O.run(P(w)))
 
 
