@@ -32,9 +32,11 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
     double2(*stage)[NS][kF2F] = reinterpret_cast<double2(*)[NS][kF2F]>(smem2);  // [2][81][32]
     __shared__ double2 sK[2][N][N];
     __shared__ double2 sIn[S][2][D][N];     // inner factor of the other inner digit: [s][kap][d][value]
-    __shared__ double2 sEI[S][2][D][N];     // per tile: Ehi (outer groups >= 1) x inner factor of the digit value
-    __shared__ long long sBase;
-    __shared__ int sLast;
+    // per tile (double buffered by tile parity: written while other warps may still read the previous
+    // tile's): Ehi (outer groups >= 1) x inner factor of the digit value, base offset, sub-step-0 'last'
+    __shared__ double2 sEI[2][S][2][D][N];
+    __shared__ long long sBase[2];
+    __shared__ int sLast[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // classes of the pair states (a, b) with a < b (the readout's upper triangle)
     auto upper_class = [](int d) {
@@ -84,29 +86,31 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
     if (u_begin < u_end) issue(u_begin, 0);
     int cur_tile = -1, last_t = 0;
     long long tbase = 0;
+    // Per unit: barrier A (its copies landed; every warp is done with the previous unit) -> copies of
+    // the next unit into the other buffer -> sub-step 0 (stage -> stage) -> barrier B -> sub-step 1
+    // (stage -> HBM: each thread stores the fibre it computed).
     for (long long u = u_begin; u < u_end; ++u) {
         const int buf = (int)((u - u_begin) & 1);
-        const int tau = (int)(u / CH), t = (int)(u % CH) * kF2F + lane;
+        const int tau = (int)(u / CH), t = (int)(u % CH) * kF2F + lane, tp = tau & 1;
         const bool valid = t < a.T;
-        if (tau != cur_tile) {  // tile constants (all threads are past the previous unit's last barrier)
+        if (tau != cur_tile) {  // tile constants into the parity-tau buffer (readers of tau-1 use the other)
             if (tid < S * 2 * D * N) {
                 const int s = tid / (2 * D * N), kap = (tid / (D * N)) % 2, d = (tid / N) % D, v = tid % N;
                 double2 e = make_double2(1.0, 0.0);
                 for (int g = 1; g < a.G; ++g)
                     e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
-                sEI[s][kap][d][v] = cmul(cmul(e, a.fixfac[s][kap][d]), sIn[s][kap][d][v]);
+                sEI[tp][s][kap][d][v] = cmul(cmul(e, a.fixfac[s][kap][d]), sIn[s][kap][d][v]);
             }
             if (tid == kF2Block - 1) {
-                sBase = tile_base(tau);
-                sLast = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
+                sBase[tp] = tile_base(tau);
+                sLast[tp] = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
             }
         }
+        const int2 lo = valid ? __ldg(&a.lofs[t]) : make_int2(0, 0);  // in flight across the barrier
+        cp_async_wait<0>();  // this unit's copies (every thread's) have landed ...
+        __syncthreads();     // A: ... and are visible, tile constants too; buf ^ 1 is free
         if (u + 1 < u_end) issue(u + 1, buf ^ 1);
-        else cp_async_commit();
-        cp_async_wait<1>();  // this unit's copies (every thread's) have landed ...
-        __syncthreads();     // ... and are visible; tile constants too
-        if (tau != cur_tile) cur_tile = tau, tbase = sBase, last_t = sLast;
-        const int2 lo = valid ? __ldg(&a.lofs[t]) : make_int2(0, 0);
+        if (tau != cur_tile) cur_tile = tau, tbase = sBase[tp], last_t = sLast[tp];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (valid) {
@@ -129,7 +133,7 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
                         p[j] = cfma(bt.b[s][kap][d][j + 6], xf[j + 6], p[j]);
                     }
                     const double2 mm = cadd(cadd(p[0], p[1]), p[2]);
-                    return cmul(cmul(__ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t]), sEI[s][kap][d][w]), mm);
+                    return cmul(cmul(__ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t]), sEI[tp][s][kap][d][w]), mm);
                 };
                 // readout first (upper triangle only: rho_ba = conj rho_ab), one class moment live at a time
                 if constexpr (RO) {
@@ -159,29 +163,26 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
                             if (upper_class(d)) accM1[RO ? d : 0] = cadd(accM1[RO ? d : 0], moment(1, d));
                     }
                 }
-                // propagate: the outputs of each class go straight to the stage (xf stays intact)
+                // propagate: the outputs of each class go straight out (xf stays intact): sub-step 0 to
+                // the stage, sub-step 1 to HBM (entry d0 = w, d1 = nw of this fibre)
+                double2 *out = a.A + tbase + lo.x + (long long)w * a.pw_in[0];
+                auto put = [&](int nw, double2 v) {
+                    if (s == 0) slot(nw) = v;
+                    else __stcs(out + (long long)nw * a.pw_in[1], v);
+                };
 #pragma unroll
                 for (int nw = 0; nw < N; ++nw)
-                    if (class_of(M, LAT, nw / M, nw % M) == 0) slot(nw) = cmul(sK[0][nw][last], S0);
+                    if (class_of(M, LAT, nw / M, nw % M) == 0) put(nw, cmul(sK[0][nw][last], S0));
 #pragma unroll
                 for (int d = 0; d < D; ++d) {
                     const double2 m = moment(0, d);
 #pragma unroll
                     for (int nw = 0; nw < N; ++nw)
-                        if (class_of(M, LAT, nw / M, nw % M) == d + 1) slot(nw) = cmul(sK[0][nw][last], m);
+                        if (class_of(M, LAT, nw / M, nw % M) == d + 1) put(nw, cmul(sK[0][nw][last], m));
                 }
             }
-            __syncthreads();
+            if (s == 0) __syncthreads();  // B
         }
-        if (valid) {
-            const long long base = tbase + lo.x;
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                const int e = warp + N * i, d0 = e % N, d1 = e / N;
-                __stcs(a.A + base + (long long)d0 * a.pw_in[0] + (long long)d1 * a.pw_in[1], stage[buf][e][lane]);
-            }
-        }
-        __syncthreads();  // the stage is refilled (unit u + 2) only after every thread has stored it
     }
     cp_async_wait<0>();
     if constexpr (RO) {

@@ -103,14 +103,21 @@ def test_mode_equivalence_and_determinism():
 
 
 def test_step_segments_equal_whole_run():
+    """Segment boundaries on fusion-group boundaries (k - L multiple of the fusion depth) give the
+    whole run bit for bit; a boundary inside a group splits it into shallower launches, which agree
+    to rounding."""
     w = W.CONFIGS[4].with_(L=4, n_steps=19)
     whole, _, _ = gpu_run(w)
-    plan = Q.Plan(w)
-    ardm, work = plan.alloc()
-    plan.init(ardm, work)
-    for k0, k1 in [(1, 3), (3, 4), (4, 11), (11, 20)]:
-        plan.steps(k0, k1, ardm, work)
-    assert np.array_equal(plan.read_rho(work), whole)
+    for segs, exact in [([(1, 3), (3, 4), (4, 12), (12, 20)], True), ([(1, 3), (3, 4), (4, 11), (11, 20)], False)]:
+        plan = Q.Plan(w)
+        ardm, work = plan.alloc()
+        plan.init(ardm, work)
+        for k0, k1 in segs:
+            plan.steps(k0, k1, ardm, work)
+        if exact:
+            assert np.array_equal(plan.read_rho(work), whole)
+        else:
+            assert np.abs(plan.read_rho(work) - whole).max() < 1e-13
     with pytest.raises(Q.QuapiError, match="order"):
         plan.steps(5, 6, ardm, work)
 
