@@ -22,18 +22,15 @@ __device__ __forceinline__ double2 cexp_(double2 z) {
 
 __host__ __device__ constexpr int cpow(int b, int e) { return e == 0 ? 1 : b * cpow(b, e - 1); }
 
-// Fixed-order CTA reduction of N complex per-thread values into partials[blockIdx][N]; the last
-// CTA to finish sums the partials over CTAs in fixed order into rho[N] (deterministic: the grid
-// and the tile -> CTA assignment are fixed by the plan).  accumulate: rho[n] += sum.
+// Fixed-order CTA reduction of N complex per-thread values into partials[blockIdx][N] (shuffle tree
+// per warp, then the warps in order).
+// dst: this CTA's row (partials + blockIdx.x * N), or rho itself when the grid is one CTA.
 template <int N, int BLOCK>
-__device__ __forceinline__ void reduce_finalize(double2 (&acc)[N], double2 *partials, double2 *rho,
-                                                unsigned *counter, bool accumulate = false) {
+__device__ __forceinline__ void reduce_block_to(double2 (&acc)[N], double2 *dst) {
     constexpr int W = BLOCK / 32;
     __shared__ double2 red[W][N];
-    __shared__ double2 fin[W];
-    __shared__ int is_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __syncthreads();  // red/fin may be reused by consecutive calls
+    __syncthreads();  // red may be reused by consecutive calls
 #pragma unroll
     for (int n = 0; n < N; ++n) {
 #pragma unroll
@@ -47,31 +44,69 @@ __device__ __forceinline__ void reduce_finalize(double2 (&acc)[N], double2 *part
     if (threadIdx.x < N) {
         double2 s = red[0][threadIdx.x];
         for (int w = 1; w < W; ++w) s = cadd(s, red[w][threadIdx.x]);
-        __stcg(&partials[(size_t)blockIdx.x * N + threadIdx.x], s);
+        __stcg(&dst[threadIdx.x], s);
     }
+}
+
+// One CTA sums partials[0..nblk)[N] in fixed order into rho[N] (accumulate: rho[n] += sum).  Thread t
+// takes the blocks b = t, t + BLOCK, ... with all N loads of a block (and of 4 blocks) in flight, then
+// the per-thread sums go through the CTA tree of reduce_block_to's shape.
+template <int N, int BLOCK>
+__device__ __forceinline__ void reduce_partials_sum(const double2 *partials, int nblk, double2 *rho, bool accumulate) {
+    constexpr int W = BLOCK / 32;
+    __shared__ double2 red2[W][N];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double2 s[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) s[n] = make_double2(0.0, 0.0);
+    int b = threadIdx.x;
+    for (; b + 3 * BLOCK < nblk; b += 4 * BLOCK) {
+        double2 v[4][N];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int n = 0; n < N; ++n) v[i][n] = __ldcg(&partials[(size_t)(b + i * BLOCK) * N + n]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int n = 0; n < N; ++n) s[n] = cadd(s[n], v[i][n]);
+    }
+    for (; b < nblk; b += BLOCK)
+#pragma unroll
+        for (int n = 0; n < N; ++n) s[n] = cadd(s[n], __ldcg(&partials[(size_t)b * N + n]));
+    __syncthreads();  // red2 may be reused by consecutive calls
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s[n].x += __shfl_xor_sync(0xffffffffu, s[n].x, o);
+            s[n].y += __shfl_xor_sync(0xffffffffu, s[n].y, o);
+        }
+        if (lane == 0) red2[warp][n] = s[n];
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double2 t = red2[0][threadIdx.x];
+        for (int w = 1; w < W; ++w) t = cadd(t, red2[w][threadIdx.x]);
+        rho[threadIdx.x] = accumulate ? cadd(rho[threadIdx.x], t) : t;
+    }
+}
+
+// Fixed-order reduction of N complex per-thread values over the grid: block partials, then the last
+// CTA to finish sums them (deterministic: the grid and the tile -> CTA assignment are fixed by the
+// plan).  accumulate: rho[n] += sum.
+template <int N, int BLOCK>
+__device__ __forceinline__ void reduce_finalize(double2 (&acc)[N], double2 *partials, double2 *rho,
+                                                unsigned *counter, bool accumulate = false) {
+    __shared__ int is_last;
+    reduce_block_to<N, BLOCK>(acc, partials + (size_t)blockIdx.x * N);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    for (int n = 0; n < N; ++n) {
-        double2 s = make_double2(0.0, 0.0);
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += BLOCK) s = cadd(s, __ldcg(&partials[(size_t)b * N + n]));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-            s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-        }
-        if (lane == 0) fin[warp] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double2 t = fin[0];
-            for (int w = 1; w < W; ++w) t = cadd(t, fin[w]);
-            rho[n] = accumulate ? cadd(rho[n], t) : t;
-        }
-        __syncthreads();
-    }
+    reduce_partials_sum<N, BLOCK>(partials, (int)gridDim.x, rho, accumulate);
     if (threadIdx.x == 0) *counter = 0u;
 }
 

@@ -22,7 +22,8 @@ SO_PATH = os.path.join(_HERE, "lib", "libquapi.so")
 
 QP_OK, QP_ERR_ARG, QP_ERR_CONFIG, QP_ERR_CAPACITY, QP_ERR_QUADRATURE, QP_ERR_CUDA, QP_ERR_COMM = 0, 1, 2, 3, 4, 6, 7
 QP_J_CALLBACK, QP_J_G_TABLE, QP_J_ETA_TABLE = 4, 5, 6
-QP_FLAG_NO_TMA, QP_FLAG_GENERIC_MOMENTS = 1, 2  # qp_problem.flags
+QP_FLAG_NO_TMA, QP_FLAG_GENERIC_MOMENTS, QP_FLAG_NO_PERSIST = 1, 2, 4  # qp_problem.flags
+QP_PERSIST_MAX_BYTES = 64 << 20
 
 _JFUNC = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
 
@@ -70,7 +71,7 @@ class qp_sizes(ctypes.Structure):
         ("bytes_per_step", ctypes.c_int64), ("lattice", ctypes.c_int32), ("n_classes", ctypes.c_int32),
         ("grid", ctypes.c_int32), ("block", ctypes.c_int32), ("tile_fibres", ctypes.c_int32),
         ("setup_seconds", ctypes.c_double), ("init_h2d_bytes", ctypes.c_int64), ("fuse_steps", ctypes.c_int32),
-        ("setup_ms", ctypes.c_double * 3),
+        ("setup_ms", ctypes.c_double * 3), ("persistent", ctypes.c_int32),
     ]
 
 
@@ -213,6 +214,7 @@ class Sizes:
     init_h2d_bytes: int
     fuse_steps: int
     setup_ms: tuple  # host setup phases (ms): validate + U, eta quadrature, factor tables
+    persistent: int  # 1: the slide steps of a steps() call run in one cooperative launch
 
 
 def _problem(w: W.Workload, keep: list, out_steps=None, J=None, J_cutoff: float = 0.0, G_in=None,
@@ -287,7 +289,7 @@ class Plan:
         o = qp_sizes()
         _check(lib().qp_plan_query(self._h, ctypes.byref(o)))
         v = [getattr(o, f) for f, _ in qp_sizes._fields_]
-        v[-1] = tuple(v[-1])
+        v[-2] = tuple(v[-2])
         return Sizes(*v)
 
     def eta(self) -> dict:

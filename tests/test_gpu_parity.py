@@ -27,7 +27,12 @@ def _cuda():
     B.build()
 
 
-def gpu_run(w, out_steps=None, **kw):
+def gpu_run(w, out_steps=None, persist=False, **kw):
+    """The per-group launch path by default (QP_FLAG_NO_PERSIST: these tests exercise the fused slide
+    kernels at small sizes); persist=True lets the library pick the persistent path
+    (tests/test_gpu_persist.py)."""
+    if not persist:
+        kw["flags"] = kw.get("flags", 0) | Q.QP_FLAG_NO_PERSIST
     plan = Q.Plan(w, out_steps=out_steps, **kw)
     ardm, work = plan.alloc()
     rho = plan.run(ardm, work)
@@ -109,7 +114,7 @@ def test_step_segments_equal_whole_run():
     w = W.CONFIGS[4].with_(L=4, n_steps=19)
     whole, _, _ = gpu_run(w)
     for segs, exact in [([(1, 3), (3, 4), (4, 12), (12, 20)], True), ([(1, 3), (3, 4), (4, 11), (11, 20)], False)]:
-        plan = Q.Plan(w)
+        plan = Q.Plan(w, flags=Q.QP_FLAG_NO_PERSIST)
         ardm, work = plan.alloc()
         plan.init(ardm, work)
         for k0, k1 in segs:
@@ -190,7 +195,7 @@ def test_fusion_grouping_independent_of_segments():
     """Fusion groups are aligned on k - L, so splitting qp_steps at group boundaries is bit-identical."""
     w = W.CONFIGS[2].with_(L=6, n_steps=31)
     whole, _, _ = gpu_run(w)
-    plan = Q.Plan(w)
+    plan = Q.Plan(w, flags=Q.QP_FLAG_NO_PERSIST)
     ardm, work = plan.alloc()
     plan.init(ardm, work)
     f = plan.sizes.fuse_steps
