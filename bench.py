@@ -97,6 +97,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def kernel_name(sz) -> str:
+    """The slide kernel the plan runs (include/quapi.h qp_sizes: fuse_steps, persistent)."""
+    if sz.persistent:
+        return "k_small: every slide step of the call in one single-CTA launch, ARDM + tables in shared memory"
+    if sz.M == 3 and sz.fuse_steps == 2:
+        return "k_fused2s: 2 time steps per HBM pass, 32-fibre units staged in shared memory (cp.async)"
+    return {4: "k_fused4: 4 time steps per HBM pass, TMA load + TMA store of 8-fibre rounds "
+               "(2-stage ring, producer warp), persistent grid",
+            3: "k_fused3: 3 time steps per HBM pass, per-warp TMA-staged rounds"}.get(
+        sz.fuse_steps, f"k_fused_r: {sz.fuse_steps} time step(s) per HBM pass")
+
+
 def cpu_baseline(cfg: int, max_slide: int = 3):
     """The oracle as it stands on the host cores, on a bounded sample of the workload:
     init + growth + `max_slide` slide steps with readout; value = slide steps / slide seconds."""
@@ -252,10 +264,7 @@ def main():
                               if sz.ardm_bytes > 2 * 126e6 else
                               f"L2-resident ARDM ({sz.ardm_bytes / 1e6:.1f} MB): not flushed, not a roofline case"),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "kernel": ({4: "k_fused4: 4 time steps per HBM pass, TMA load + TMA store of 8-fibre rounds "
-                                      "(2-stage ring, producer warp), persistent grid",
-                                   3: "k_fused3: 3 time steps per HBM pass, per-warp TMA-staged rounds"}
-                                  .get(sz.fuse_steps, f"k_fused_r: {sz.fuse_steps} time step(s) per HBM pass")),
+                       "kernel": kernel_name(sz),
                        "steps_per_launch": K / max(1, launches)},
             "achieved_gbs": achieved,
             "step_equivalent_gbs": step_equiv,

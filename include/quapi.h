@@ -89,7 +89,7 @@ typedef struct {
     const qp_c64 *eta_in;    /* QP_J_ETA_TABLE only: [3*dkmax+2] eta classes, qp_plan_eta order   */
     int32_t fuse_steps;      /* cap on the time steps fused into one pass over the ARDM, 0..4;
                                 0 => the library's choice (4 for M = 2 with L >= 6, else 3; 2 for
-                                M = 3; 1 for M = 4; persistent plans: 2 for M = 2, else 1).  Results
+                                M = 3; 1 for M = 4; persistent plans: 1).  Results
                                 agree to rounding for every choice.                              */
     uint32_t flags;          /* QP_FLAG_* below; 0 for the default plan                          */
 } qp_problem;
@@ -100,13 +100,14 @@ typedef struct {
                                instead of the per-warp TMA-staged rounds;
    QP_FLAG_GENERIC_MOMENTS  -- M = 2, s = (+s, -s): the generic per-class moments instead of the
                                symmetric four-sum moments;
-   QP_FLAG_NO_PERSIST       -- no persistent path: a small ARDM (<= QP_PERSIST_MAX_BYTES, L2-
-                               resident) otherwise runs all slide steps of a qp_steps call in one
-                               cooperative launch with fusion depth <= 2 (M = 2) or 1. */
+   QP_FLAG_NO_PERSIST       -- no persistent path: a small ARDM (<= QP_PERSIST_MAX_BYTES) otherwise
+                               runs all slide steps of a qp_steps call in one single-CTA launch
+                               with the ARDM and the tables in shared memory, one step at a time
+                               (DESIGN.md §5). */
 #define QP_FLAG_NO_TMA 1u
 #define QP_FLAG_GENERIC_MOMENTS 2u
 #define QP_FLAG_NO_PERSIST 4u
-#define QP_PERSIST_MAX_BYTES (64ll << 20)
+#define QP_PERSIST_MAX_BYTES (64ll << 10)
 
 typedef struct qp_plan qp_plan;
 
@@ -127,9 +128,10 @@ typedef struct {
     int64_t init_h2d_bytes;  /* bytes qp_init copies host->device (tables, A_0, rho(0))         */
     int32_t fuse_steps;      /* time steps fused into one pass over the ARDM (slide kernel)      */
     double setup_ms[3];      /* host setup phases: validate + U, eta quadrature, factor tables    */
-    int32_t persistent;      /* slide steps of a qp_steps call in one launch: 1 cooperative grid
-                                (L2-resident ARDM), 2 (after qp_init) one CTA holding the ARDM and
-                                the tables in shared memory; 0 one launch per fusion group        */
+    int32_t persistent;      /* 1: the slide steps of a qp_steps call run in one single-CTA launch
+                                (ARDM <= QP_PERSIST_MAX_BYTES; confirmed at qp_init against the
+                                device's shared memory, else 0: one launch per step); 0: one
+                                launch per fusion group                                          */
 } qp_sizes;
 
 /* Host only (no GPU needed): validate (a1), U = e^{-iH dt} and the pair propagator K (a2),

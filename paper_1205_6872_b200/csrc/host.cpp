@@ -374,8 +374,7 @@ struct qp_plan {
     // persistent path (small ARDM): launch-set arguments and per-step readout slots in the workspace
     bool persist = false;
     size_t off_psets = 0, off_pslot = 0;
-    int pgrid = 0;
-    size_t small_dyn = 0;              // > 0: single-CTA shared-memory path (k_small_r), its dynamic smem
+    size_t small_dyn = 0;              // > 0 after qp_init: k_small runs the slide steps, its dynamic smem
     std::vector<LaunchSet> sets;       // index p0 * Smax + (S - 1)
     size_t off_small = 0, off_part = 0, off_rho = 0, off_cnt = 0, tables_end = 0, work_bytes = 0;
     int64_t ardm_entries = 0;
@@ -1034,10 +1033,11 @@ void build_tables(qp_plan &P, int fuse_cap) {
     // least two digits (L >= 6), else three (k_fused3)
     const int s2 = (L >= 6 && !(P.flags & QP_FLAG_NO_TMA)) ? 4 : 3;
     P.Smax = std::max(1, std::min(M == 2 ? s2 : (M == 3 ? 2 : 1), L - 1));
-    // persistent path: an L2-resident ARDM runs each qp_steps call in one cooperative launch of the
-    // register-fused kernel body (fusion depth <= 2), launch overhead instead of bandwidth being the cost
+    // persistent path (persist.cu): a small ARDM runs each qp_steps call in one single-CTA launch with
+    // everything in shared memory, one step at a time -- there the launch, not the bandwidth, is the
+    // cost of a step
     P.persist = !(P.flags & QP_FLAG_NO_PERSIST) && 16.0 * std::pow((double)N, (double)L) <= (double)QP_PERSIST_MAX_BYTES;
-    if (P.persist) P.Smax = std::min(P.Smax, qp::persist_max_S(M));
+    if (P.persist) P.Smax = 1;
     if (fuse_cap > 0) P.Smax = std::min(P.Smax, fuse_cap);
     P.sets.assign((size_t)L * P.Smax, qp_plan::LaunchSet{});
     {  // the L * Smax launch sets are independent (read-only plan, own tables): build them on host threads
@@ -1228,7 +1228,7 @@ qp_status qp_plan_query(const qp_plan *P, qp_sizes *o) {
     o->block = P->block;
     o->tile_fibres = P->sets.empty() ? 0 : P->sets[(size_t)P->Smax - 1].args.T;
     o->fuse_steps = P->Smax;
-    o->persistent = P->persist ? (P->small_dyn ? 2 : 1) : 0;
+    o->persistent = (P->persist && (!P->inited || P->small_dyn)) ? 1 : 0;
     o->setup_seconds = P->setup_seconds;
     for (int i = 0; i < 3; ++i) o->setup_ms[i] = P->setup_ms[i];
     o->init_h2d_bytes = (int64_t)(P->tables_end + 2 * P->N * sizeof(double2));
@@ -1333,15 +1333,13 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
         qp::FusedArgs a = ls.args;
         a.use_tma = ls.tma_a != -1;
         P->grid[P->Smax] = launch_grid(P, P->Smax, a);
-        P->block = P->persist ? qp::persist_block(P->M)
+        P->block = P->persist ? qp::kPersistBlock
                    : (P->M == 3 && P->Smax == 2) ? qp::fused2s_block()
                    : (P->M == 2 && P->Smax == 4) ? qp::fused4_block()
                    : (P->M == 2 && P->Smax == 3) ? qp::fused3_block(a.lane_map, a.use_tma) : qp::fused_r_block(P->M, P->Smax);
     }
     if (P->persist) {  // launch-set arguments (table pointers into this workspace) + readout slot per step
         std::vector<qp::FusedArgs> sets(P->sets.size());
-        const int W = qp::persist_block(P->M) / 32;
-        int64_t units = 1;
         for (size_t i = 0; i < P->sets.size(); ++i) {
             const qp_plan::LaunchSet &ls = P->sets[i];
             qp::FusedArgs a = ls.args;
@@ -1355,24 +1353,19 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
             a.counter = (unsigned *)(w + P->off_cnt);
             a.rho_accumulate = 0;
             sets[i] = a;
-            units = std::max<int64_t>(units, (int64_t)a.n_tiles * ((a.T + 31) / 32));
         }
         std::vector<int> slot((size_t)P->n_steps + 1);
         for (int64_t k = 0; k <= P->n_steps; ++k) slot[(size_t)k] = (int)P->slot_of(k);
         QP_CUDA(cudaMemcpyAsync(w + P->off_psets, sets.data(), sets.size() * sizeof(qp::FusedArgs), cudaMemcpyHostToDevice, s));
         QP_CUDA(cudaMemcpyAsync(w + P->off_pslot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-        // grid: co-resident (cooperative launch), no more CTAs than the largest set has warp units
-        const int occ = std::max(1, qp::persist_occupancy(P->M, P->lattice, P->sym));
-        P->pgrid = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)P->sms * occ, (units + W - 1) / W, (int64_t)qp::kPartialsMax}));
-        P->grid[P->Smax] = P->pgrid;
         // one CTA when the ARDM, every table and the launch-set arguments fit its shared memory
-        const size_t dyn = qp::small_acc_bytes(P->M) + P->tables_end + 16 * (size_t)P->ardm_entries +
-                           P->sets.size() * sizeof(qp::FusedArgs);
+        const size_t dyn = P->tables_end + 16 * (size_t)P->ardm_entries + P->sets.size() * sizeof(qp::FusedArgs);
         int dev = 0, optin = 0;
         QP_CUDA(cudaGetDevice(&dev));
         QP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         P->small_dyn = (dyn + (size_t)qp::small_static_smem(P->M, P->lattice, P->sym) <= (size_t)optin) ? dyn : 0;
         if (P->small_dyn) P->grid[P->Smax] = 1;
+        else P->block = qp::fused_r_block(P->M, 1);  // does not fit this device: one k_fused_r launch per step
     }
     P->next_k = 1;
     P->sh.seg = 0;
@@ -1410,13 +1403,14 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             for (int d = 0; d < P->D; ++d) g.delta[d] = P->delta[d];
             const int grid = (int)std::min<int64_t>({(g.n_in + 255) / 256, (int64_t)P->sms * 8, (int64_t)qp::kPartialsMax});
             e = qp::launch_grow(P->M, P->lattice, g, std::max(1, grid), s);
-        } else if (P->persist) {  // every remaining slide step of this call: one cooperative launch
+        } else if (P->small_dyn) {  // every remaining slide step of this call: one single-CTA launch
             qp::PersistArgs pa{};
             pa.sets = (const qp::FusedArgs *)(w + P->off_psets);
+            pa.set_stride = P->Smax;
+            pa.small = small;
             pa.A = A;
             pa.slot = (const int *)(w + P->off_pslot);
             pa.rho_base = (double2 *)(w + P->off_rho);
-            pa.partials = part;
             const qp::SmallLayout lay{P->N, P->D, P->L};
             for (int var = 0; var < 2; ++var)
                 for (int kap = 0; kap < 2 && P->sym; ++kap) {  // FusedArgs::sym per beta variant
@@ -1430,14 +1424,11 @@ qp_status qp_steps(qp_plan *P, int64_t k_begin, int64_t k_end, void *d_ardm, voi
             pa.k_begin = k;
             pa.k_end = k_end;
             pa.L = P->L;
-            pa.Smax = P->Smax;
             pa.wbase = w;
             pa.tables_bytes = (long long)P->tables_end;
             pa.ardm_entries = P->ardm_entries;
-            pa.acc_bytes = (long long)qp::small_acc_bytes(P->M);
             pa.nsets = (int)P->sets.size();
-            e = P->small_dyn ? qp::launch_small(P->M, P->lattice, P->sym, pa, P->small_dyn, s)
-                             : qp::launch_persist(P->M, P->lattice, P->sym, pa, P->pgrid, s);
+            e = qp::launch_small(P->M, P->lattice, P->sym, pa, P->small_dyn, s);
             adv = k_end - k;
         } else {
             // fusion groups are aligned on absolute k (k - L multiple of Smax), so the floating-point

@@ -147,28 +147,23 @@ int fused3_round_fibres(int lane_map, bool tma);  // outer fibres per round (8 p
 int fused3_occupancy(bool sym, int lane_map, bool tma);
 cudaError_t launch_fused3(bool sym, const FusedArgs &a, bool ro, int grid, cudaStream_t s);
 // k_fused2s (slide2.cu): M = 3, S = 2, shared-memory-staged units of 32 outer fibres
-// k_persist_r (slide_r.cu): the slide steps of one qp_steps call on a small ARDM in one cooperative
-// launch (fusion groups of depth <= persist_max_S(M), grid-wide barrier between groups)
+// k_small (persist.cu): all slide steps of one qp_steps call on a small ARDM in ONE launch of one
+// CTA, the ARDM and every factor table staged in its shared memory, one step at a time.
 struct PersistArgs {
-    const FusedArgs *sets;   // device copy of the plan's launch-set arguments, index p0 * Smax + (S - 1)
+    const FusedArgs *sets;   // device copy of the plan's launch-set arguments, index p0 * set_stride
+    int set_stride;          // plan Smax (the S = 1 set of start slot p0 is sets[p0 * set_stride])
     double2 *A;              // ARDM
     const int *slot;         // [n_steps + 1]: readout slot of step k, -1 none
     double2 *rho_base;       // readout array [n_out][N]
-    double2 *partials;       // [2 parities][2 steps][kPartialsMax][N] block partials of the readout
+    const double2 *small;    // SmallLayout block (K', beta)
     double sym[2][2][4];     // symmetric-moment constants per beta variant (FusedArgs::sym)
     long long k_begin, k_end;
-    int L, Smax;
-    // k_small_r: the workspace tables [0, tables_bytes) and the ARDM are staged in shared memory
-    const void *wbase;       // d_work
-    long long tables_bytes, ardm_entries, acc_bytes;
+    int L;
+    const void *wbase;       // d_work: the tables [0, tables_bytes) are staged in shared memory
+    long long tables_bytes, ardm_entries;
     int nsets;
 };
-int persist_max_S(int M);
-int persist_block(int M);
-int persist_occupancy(int M, bool lattice, bool sym);
-cudaError_t launch_persist(int M, bool lattice, bool sym, const PersistArgs &pa, int grid, cudaStream_t s);
-// k_small_r (slide_r.cu): the same, one CTA, the ARDM and every table in shared memory
-size_t small_acc_bytes(int M);
+constexpr int kPersistBlock = 256;
 int small_static_smem(int M, bool lattice, bool sym);
 cudaError_t launch_small(int M, bool lattice, bool sym, const PersistArgs &pa, size_t dyn, cudaStream_t s);
 

@@ -25,35 +25,12 @@
 // (warp-synchronous, no CTA barrier in the main loop) and sweeps the tile in chunks of 32 outer
 // fibres, lane = outer fibre.  Readout accumulators live in shared memory; the CTA reduction at the
 // end is in fixed order (deterministic).
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 
 namespace qp {
 
-// One fused launch's work (every CTA of the grid runs it): the body of k_fused_r and of the
-// persistent k_persist_r (one call per fusion group).
-// Readout modes of fused_r_body: the grid-wide finalize (last CTA sums the block partials), the block
-// partials only (the persistent kernel sums them after its grid barrier), or straight into rho (grid
-// of one CTA).
-enum RoMode { kRoFinalize = 0, kRoDefer = 1, kRoDirect = 2 };
-// loads / stores of the table and ARDM pointers: global-memory cache hints, or plain generic accesses
-// when SMEM (k_small_r: every table and the ARDM live in shared memory)
-template <bool SMEM, typename T> __device__ __forceinline__ T ld_tab(const T *p) {
-    if constexpr (SMEM) return *p;
-    else return __ldg(p);
-}
-template <bool SMEM> __device__ __forceinline__ double2 ld_ardm(const double2 *p) {
-    if constexpr (SMEM) return *p;
-    else return __ldcs(p);
-}
-template <bool SMEM> __device__ __forceinline__ void st_ardm(double2 *p, double2 v) {
-    if constexpr (SMEM) *p = v;
-    else __stcs(p, v);
-}
-
-template <int M, bool LAT, bool SYM, int S, int BLOCK, bool RO, int RMODE = kRoFinalize, bool SMEM = false>
-__device__ __forceinline__ void fused_r_body(const FusedArgs &a) {
+template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool RO>
+__global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__ FusedArgs a) {
     constexpr int N = M * M;
     constexpr int D = n_classes(M, LAT);
     constexpr int Q = cpow(N, S - 1);    // fibres per super-fibre and sub-step
@@ -121,12 +98,12 @@ __device__ __forceinline__ void fused_r_body(const FusedArgs &a) {
                 const int s = lane / (NK * D), kap = (lane / D) % NK, d = lane % D;
                 double2 e = make_double2(1.0, 0.0);
                 for (int g = 1; g < a.G; ++g)
-                    e = cmul(e, ld_tab<SMEM>(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
+                    e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + d) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
                 sEhi[warp][s][kap][d] = cmul(e, a.fixfac[s][kap][d]);
             }
             if (lane == 31) {
                 long long b = 0;
-                for (int g = 1; g < a.G; ++g) b += ld_tab<SMEM>(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
+                for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
                 sBase[warp] = b;
                 sLast[warp] = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
             }
@@ -143,7 +120,7 @@ __device__ __forceinline__ void fused_r_body(const FusedArgs &a) {
             last_t = sLast[warp];
         }
         if (t >= a.T) continue;
-        const int2 lo = ld_tab<SMEM>(&a.lofs[t]);
+        const int2 lo = __ldg(&a.lofs[t]);
         const long long base = tbase + lo.x;
         double2 x[NS];
 #pragma unroll
@@ -151,7 +128,7 @@ __device__ __forceinline__ void fused_r_body(const FusedArgs &a) {
             long long o = base;
 #pragma unroll
             for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
-            x[e] = ld_ardm<SMEM>(a.A + o);
+            x[e] = __ldcs(a.A + o);
         }
         const int last0 = lo.y >= 0 ? lo.y : last_t;
 #pragma unroll
@@ -162,7 +139,7 @@ __device__ __forceinline__ void fused_r_body(const FusedArgs &a) {
             for (int kap = 0; kap < NK; ++kap)
 #pragma unroll
                 for (int d = 0; d < D; ++d)
-                    E0[kap][d] = (kap == 0 || ro) ? ld_tab<SMEM>(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t])
+                    E0[kap][d] = (kap == 0 || ro) ? __ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t])
                                                   : make_double2(0.0, 0.0);
             double2 acc[RO ? N : 1];
 #pragma unroll
@@ -244,7 +221,7 @@ __device__ __forceinline__ void fused_r_body(const FusedArgs &a) {
             long long o = base;
 #pragma unroll
             for (int i = 0; i < S; ++i) o += (long long)((e / cpow(N, i)) % N) * a.pw_in[i];
-            st_ardm<SMEM>(a.A + o, x[e]);
+            __stcs(a.A + o, x[e]);
         }
     }
     if constexpr (RO) {
@@ -254,69 +231,9 @@ __device__ __forceinline__ void fused_r_body(const FusedArgs &a) {
                 double2 tt[N];
 #pragma unroll
                 for (int n = 0; n < N; ++n) tt[n] = accS[RO ? s : 0][RO ? n : 0][RO ? threadIdx.x : 0];
-                if constexpr (RMODE == kRoDefer)
-                    reduce_block_to<N, BLOCK>(tt, a.partials + ((size_t)s * kPartialsMax + blockIdx.x) * N);
-                else if constexpr (RMODE == kRoDirect)
-                    reduce_block_to<N, BLOCK>(tt, a.rho[s]);
-                else
-                    reduce_finalize<N, BLOCK>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
-                                              a.rho_accumulate != 0);
+                reduce_finalize<N, BLOCK>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
+                                          a.rho_accumulate != 0);
             }
-    }
-}
-
-template <int M, bool LAT, bool SYM, int S, int BLOCK, int MINB, bool RO>
-__global__ void __launch_bounds__(BLOCK, MINB) k_fused_r(const __grid_constant__ FusedArgs a) {
-    fused_r_body<M, LAT, SYM, S, BLOCK, RO>(a);
-}
-
-// ---------------------------------------------------------------------------------- persistent
-// k_persist_r: the slide steps k_begin..k_end-1 of a small (L2-resident) ARDM in ONE cooperative
-// launch.  Per fusion group (aligned on k - L, depth S <= PA.Smax <= 2): the group's launch-set
-// arguments are copied from the device table into shared memory, the per-step fields (rho
-// destination, beta variant, symmetric-moment constants) are set from k, every CTA runs
-// fused_r_body, and a grid-wide barrier orders the group's in-place update before the next group.
-// The readout stops at the block partials (double buffered by group parity); after the barrier CTA 0
-// sums them into rho while the others start the next group.  The launch count per qp_steps call
-// drops from one per group to one.
-template <int M, bool LAT, bool SYM, int BLOCK, int MINB>
-__global__ void __launch_bounds__(BLOCK, MINB) k_persist_r(const __grid_constant__ PersistArgs pa) {
-    __shared__ FusedArgs sa;
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    constexpr int N = M * M;
-    int par = 0;
-    for (long long k = pa.k_begin; k < pa.k_end; par ^= 1) {
-        const long long grp_end = pa.L + ((k - pa.L) / pa.Smax + 1) * pa.Smax;
-        const int S = (int)(grp_end < pa.k_end ? grp_end - k : pa.k_end - k);
-        const int p0 = (int)(k % pa.L);
-        {
-            const int4 *src = reinterpret_cast<const int4 *>(pa.sets + (size_t)p0 * pa.Smax + (S - 1));
-            int4 *dst = reinterpret_cast<int4 *>(&sa);
-            for (int i = threadIdx.x; i < (int)(sizeof(FusedArgs) / 16); i += BLOCK) dst[i] = src[i];
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            sa.A = pa.A;
-            sa.partials = pa.partials + (size_t)2 * par * kPartialsMax * N;
-            for (int st = 0; st < S; ++st) {
-                const int slot = pa.slot[k + st];
-                const int var = (k + st == pa.L) ? 1 : 0;
-                sa.rho[st] = slot >= 0 ? pa.rho_base + (size_t)slot * (M * M) : nullptr;
-                sa.var[st] = var;
-                for (int kap = 0; kap < 2; ++kap)
-                    for (int j = 0; j < 4; ++j) sa.sym[st][kap][j] = pa.sym[var][kap][j];
-            }
-        }
-        __syncthreads();
-        if (M == 2 && S == 2) fused_r_body<M, LAT, SYM, (M == 2 ? 2 : 1), BLOCK, true, kRoDefer>(sa);
-        else fused_r_body<M, LAT, SYM, 1, BLOCK, true, kRoDefer>(sa);
-        grid.sync();
-        if (blockIdx.x == 0)
-            for (int st = 0; st < S; ++st)
-                if (sa.rho[st] != nullptr)
-                    reduce_partials_sum<N, BLOCK>(sa.partials + (size_t)st * kPartialsMax * N, (int)gridDim.x, sa.rho[st], false);
-        k += S;
     }
 }
 
@@ -328,110 +245,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_persist_r(const __grid_constant
     X(3, 1, 256, 3, 2)     \
     X(4, 1, 64, 2, 4)
 
-// k_small_r: the same group loop for an ARDM small enough to live in ONE CTA's shared memory together
-// with every factor table of the plan: the tables ([0, tables_bytes) of the workspace) and the ARDM
-// are copied in once, the launch-set arguments are re-pointed at the shared copies, the groups run
-// with CTA barriers only (readout straight into rho), and the ARDM is copied back at the end.
-// Dynamic shared memory: [body readout accumulators][tables][ARDM][launch-set arguments].
-template <int M, bool LAT, bool SYM, int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 1) k_small_r(const __grid_constant__ PersistArgs pa) {
-    constexpr int N = M * M;
-    extern __shared__ __align__(16) double2 dyn_smem[];
-    __shared__ FusedArgs sa;
-    unsigned char *base = reinterpret_cast<unsigned char *>(dyn_smem);
-    unsigned char *tab = base + pa.acc_bytes;
-    double2 *sA = reinterpret_cast<double2 *>(tab + pa.tables_bytes);
-    FusedArgs *sets = reinterpret_cast<FusedArgs *>(reinterpret_cast<unsigned char *>(sA) + pa.ardm_entries * 16);
-    {
-        const int4 *src = reinterpret_cast<const int4 *>(pa.wbase);
-        int4 *dst = reinterpret_cast<int4 *>(tab);
-        for (long long i = threadIdx.x; i < pa.tables_bytes / 16; i += BLOCK) dst[i] = src[i];
-        const int4 *srcA = reinterpret_cast<const int4 *>(pa.A);
-        int4 *dstA = reinterpret_cast<int4 *>(sA);
-        for (long long i = threadIdx.x; i < pa.ardm_entries; i += BLOCK) dstA[i] = srcA[i];
-        const int4 *srcS = reinterpret_cast<const int4 *>(pa.sets);
-        int4 *dstS = reinterpret_cast<int4 *>(sets);
-        for (long long i = threadIdx.x; i < (long long)pa.nsets * (long long)(sizeof(FusedArgs) / 16); i += BLOCK) dstS[i] = srcS[i];
-    }
-    __syncthreads();
-    auto rebase = [&](const void *p) -> unsigned char * {
-        return tab + (reinterpret_cast<const unsigned char *>(p) - reinterpret_cast<const unsigned char *>(pa.wbase));
-    };
-    for (int i = threadIdx.x; i < pa.nsets; i += BLOCK) {
-        FusedArgs &f = sets[i];
-        f.A = sA;
-        f.small = reinterpret_cast<const double2 *>(rebase(f.small));
-        f.inner = reinterpret_cast<const double2 *>(rebase(f.inner));
-        f.Etab = reinterpret_cast<const double2 *>(rebase(f.Etab));
-        f.goff = reinterpret_cast<const long long *>(rebase(f.goff));
-        f.lofs = reinterpret_cast<const int2 *>(rebase(f.lofs));
-    }
-    __syncthreads();
-    for (long long k = pa.k_begin; k < pa.k_end;) {
-        const long long grp_end = pa.L + ((k - pa.L) / pa.Smax + 1) * pa.Smax;
-        const int S = (int)(grp_end < pa.k_end ? grp_end - k : pa.k_end - k);
-        const int p0 = (int)(k % pa.L);
-        {
-            const int4 *src = reinterpret_cast<const int4 *>(sets + (size_t)p0 * pa.Smax + (S - 1));
-            int4 *dst = reinterpret_cast<int4 *>(&sa);
-            for (int i = threadIdx.x; i < (int)(sizeof(FusedArgs) / 16); i += BLOCK) dst[i] = src[i];
-        }
-        __syncthreads();
-        if (threadIdx.x == 0)
-            for (int st = 0; st < S; ++st) {
-                const int slot = pa.slot[k + st];
-                const int var = (k + st == pa.L) ? 1 : 0;
-                sa.rho[st] = slot >= 0 ? pa.rho_base + (size_t)slot * N : nullptr;
-                sa.var[st] = var;
-                for (int kap = 0; kap < 2; ++kap)
-                    for (int j = 0; j < 4; ++j) sa.sym[st][kap][j] = pa.sym[var][kap][j];
-            }
-        __syncthreads();
-        if (M == 2 && S == 2) fused_r_body<M, LAT, SYM, (M == 2 ? 2 : 1), BLOCK, true, kRoDirect, true>(sa);
-        else fused_r_body<M, LAT, SYM, 1, BLOCK, true, kRoDirect, true>(sa);
-        __syncthreads();
-        k += S;
-    }
-    {
-        const int4 *srcA = reinterpret_cast<const int4 *>(sA);
-        int4 *dstA = reinterpret_cast<int4 *>(pa.A);
-        for (long long i = threadIdx.x; i < pa.ardm_entries; i += BLOCK) dstA[i] = srcA[i];
-    }
-}
-
 namespace {
-template <int M, bool LAT, bool SYM, int BLOCK>
-cudaError_t small_t(const PersistArgs &pa, size_t dyn, cudaStream_t s) {
-    auto f = k_small_r<M, LAT, SYM, BLOCK>;
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    f<<<1, BLOCK, dyn, s>>>(pa);
-    return cudaGetLastError();
-}
-template <int M, bool LAT, bool SYM, int BLOCK>
-int small_static_t() {
-    cudaFuncAttributes at{};
-    if (cudaFuncGetAttributes(&at, k_small_r<M, LAT, SYM, BLOCK>) != cudaSuccess) return 1 << 30;
-    return (int)at.sharedSizeBytes;
-}
-
-template <int M, bool LAT, bool SYM, int BLOCK, int MINB>
-cudaError_t persist_t(const PersistArgs &pa, int grid, cudaStream_t s) {
-    const size_t dyn = (size_t)(M == 2 ? 2 : 1) * M * M * BLOCK * 16;  // readout accumulators of the deepest body
-    auto f = k_persist_r<M, LAT, SYM, BLOCK, MINB>;
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    void *args[] = {(void *)&pa};
-    return cudaLaunchCooperativeKernel((const void *)f, dim3(grid), dim3(BLOCK), args, dyn, s);
-}
-template <int M, bool LAT, bool SYM, int BLOCK, int MINB>
-int persist_occ_t() {
-    const size_t dyn = (size_t)(M == 2 ? 2 : 1) * M * M * BLOCK * 16;
-    auto f = k_persist_r<M, LAT, SYM, BLOCK, MINB>;
-    int o = 0;
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, BLOCK, dyn);
-    return o;
-}
-
 template <int M, int S, int BLOCK>
 constexpr size_t fused_r_dyn_smem(bool ro) {
     return (ro ? (size_t)S * M * M * BLOCK : 0) * 16;
@@ -491,44 +305,6 @@ cudaError_t launch_fused_r(int M, bool lattice, bool sym, int S, const FusedArgs
     QP_FUSED_R_CFGS(X)
 #undef X
     return cudaErrorInvalidValue;
-}
-
-// persistent kernel: per M the block / min-blocks of k_fused_r at S = 1 (M = 2: 128 threads so that the
-// static shared memory of both bodies, S = 1 and 2, fits)
-int persist_max_S(int M) { return M == 2 ? 2 : 1; }
-cudaError_t launch_persist(int M, bool lattice, bool sym, const PersistArgs &pa, int grid, cudaStream_t s) {
-    switch (M) {
-    case 2: return sym ? persist_t<2, false, true, 128, 4>(pa, grid, s) : persist_t<2, false, false, 128, 4>(pa, grid, s);
-    case 3: return lattice ? persist_t<3, true, false, 256, 2>(pa, grid, s) : persist_t<3, false, false, 256, 2>(pa, grid, s);
-    case 4: return lattice ? persist_t<4, true, false, 64, 4>(pa, grid, s) : persist_t<4, false, false, 64, 4>(pa, grid, s);
-    }
-    return cudaErrorInvalidValue;
-}
-int persist_occupancy(int M, bool lattice, bool sym) {
-    switch (M) {
-    case 2: return sym ? persist_occ_t<2, false, true, 128, 4>() : persist_occ_t<2, false, false, 128, 4>();
-    case 3: return lattice ? persist_occ_t<3, true, false, 256, 2>() : persist_occ_t<3, false, false, 256, 2>();
-    case 4: return lattice ? persist_occ_t<4, true, false, 64, 4>() : persist_occ_t<4, false, false, 64, 4>();
-    }
-    return 0;
-}
-int persist_block(int M) { return M == 4 ? 64 : (M == 2 ? 128 : 256); }
-size_t small_acc_bytes(int M) { return (size_t)persist_max_S(M) * M * M * persist_block(M) * 16; }
-cudaError_t launch_small(int M, bool lattice, bool sym, const PersistArgs &pa, size_t dyn, cudaStream_t s) {
-    switch (M) {
-    case 2: return sym ? small_t<2, false, true, 128>(pa, dyn, s) : small_t<2, false, false, 128>(pa, dyn, s);
-    case 3: return lattice ? small_t<3, true, false, 256>(pa, dyn, s) : small_t<3, false, false, 256>(pa, dyn, s);
-    case 4: return lattice ? small_t<4, true, false, 64>(pa, dyn, s) : small_t<4, false, false, 64>(pa, dyn, s);
-    }
-    return cudaErrorInvalidValue;
-}
-int small_static_smem(int M, bool lattice, bool sym) {
-    switch (M) {
-    case 2: return sym ? small_static_t<2, false, true, 128>() : small_static_t<2, false, false, 128>();
-    case 3: return lattice ? small_static_t<3, true, false, 256>() : small_static_t<3, false, false, 256>();
-    case 4: return lattice ? small_static_t<4, true, false, 64>() : small_static_t<4, false, false, 64>();
-    }
-    return 1 << 30;
 }
 
 int fused_r_occupancy(int M, bool lattice, bool sym, int S) {

@@ -23,7 +23,7 @@ SO_PATH = os.path.join(_HERE, "lib", "libquapi.so")
 QP_OK, QP_ERR_ARG, QP_ERR_CONFIG, QP_ERR_CAPACITY, QP_ERR_QUADRATURE, QP_ERR_CUDA, QP_ERR_COMM = 0, 1, 2, 3, 4, 6, 7
 QP_J_CALLBACK, QP_J_G_TABLE, QP_J_ETA_TABLE = 4, 5, 6
 QP_FLAG_NO_TMA, QP_FLAG_GENERIC_MOMENTS, QP_FLAG_NO_PERSIST = 1, 2, 4  # qp_problem.flags
-QP_PERSIST_MAX_BYTES = 64 << 20
+QP_PERSIST_MAX_BYTES = 64 << 10
 
 _JFUNC = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
 
@@ -214,7 +214,7 @@ class Sizes:
     init_h2d_bytes: int
     fuse_steps: int
     setup_ms: tuple  # host setup phases (ms): validate + U, eta quadrature, factor tables
-    persistent: int  # 1: the slide steps of a steps() call run in one cooperative launch
+    persistent: int  # 1: the slide steps of a steps() call run in one single-CTA launch
 
 
 def _problem(w: W.Workload, keep: list, out_steps=None, J=None, J_cutoff: float = 0.0, G_in=None,

@@ -92,15 +92,15 @@ def test_sizes_and_pmc():
 
 
 def test_persistent_path_selection():
-    """The persistent path is chosen for ARDMs up to QP_PERSIST_MAX_BYTES (fusion depth capped at 2 for
-    M = 2, 1 for M = 3, 4) and never above it or under QP_FLAG_NO_PERSIST."""
-    for L, M in [(5, 2), (10, 2), (11, 2), (12, 2), (5, 3), (8, 3), (9, 3), (3, 4), (6, 4), (7, 4)]:
+    """The persistent path (one step at a time) is chosen for ARDMs up to QP_PERSIST_MAX_BYTES and never
+    above it or under QP_FLAG_NO_PERSIST."""
+    for L, M in [(5, 2), (6, 2), (7, 2), (10, 2), (12, 2), (3, 3), (4, 3), (8, 3), (2, 4), (3, 4), (4, 4)]:
         w = W.random_problem(3, M, L, L + 4)
         s = Q.Plan(w, out_steps=[0]).sizes
         small = s.ardm_bytes <= Q.QP_PERSIST_MAX_BYTES
         assert s.persistent == int(small), (L, M)
         if small:
-            assert s.fuse_steps == min(L - 1, 2 if M == 2 else 1)
+            assert s.fuse_steps == 1
         s2 = Q.Plan(w, out_steps=[0], flags=Q.QP_FLAG_NO_PERSIST).sizes
         assert s2.persistent == 0
         assert s2.fuse_steps == min(L - 1, ((4 if L >= 6 else 3) if M == 2 else (2 if M == 3 else 1)))
