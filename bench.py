@@ -125,7 +125,7 @@ def cpu_baseline(cfg: int, max_slide: int = 3):
     _, tm = O.run(p, out_steps=np.arange(n + 1), nthreads=cores, timings=True)
     wall = time.perf_counter() - t0
     v = tm["n_slide"] / tm["slide_s"] if tm["slide_s"] > 0 else None
-    return {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
+    return {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle", "timed_steps": int(tm["n_slide"]),
             "sample": (f"{w.name}: init + {w.L - 1} growth + {tm['n_slide']} slide steps with readout "
                        f"(allPoints), {cores} OpenMP threads; slide {tm['slide_s']:.2f} s of {wall:.1f} s wall")}
 
@@ -138,7 +138,7 @@ def run_reference(args):
     from paper_1205_6872_b200 import workloads as W
     w = W.CONFIGS[args.cfg]
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "steps/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": args.gpus, "steps": cb["timed_steps"], "requested_steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / cb["value"] if cb["value"] else None, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "ardm_entries": w.ardm_entries},
@@ -160,6 +160,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo stages the all-to-all through host memory; tests only)")
+    ap.add_argument("--reps", type=int, default=3,
+                    help="timed repetitions of K steps each; value = the median repetition (single GPU)")
     ap.add_argument("--mode", default="shard", choices=["shard", "replica"],
                     help="N > 1: shard one ARDM over the ranks (strong scaling, NCCL all-to-all re-shard) "
                          "or run independent replicas (weak scaling)")
@@ -187,8 +189,10 @@ def main():
     base = W.CONFIGS[args.cfg]
     if world > 1 and args.mode == "shard":
         return bench_sharded(args, base, world, rank, local)
-    K, Wm, L = args.steps, max(args.warmup, 3), base.L
-    n_total = L - 1 + Wm + K  # growth steps, then W warm-up and K timed slide steps
+    K, Wm, L, R = args.steps, max(args.warmup, 3), base.L, max(1, args.reps)
+    fuse = Q.Plan(base.with_(n_steps=L + 4), out_steps=[0], fuse_steps=args.fuse_steps).sizes.fuse_steps
+    Wm = -(-Wm // fuse) * fuse  # warm-up rounded up to whole fusion groups: the timed steps start a group
+    n_total = L - 1 + Wm + R * K  # growth steps, then W warm-up and R x K timed slide steps
     w = base.with_(n_steps=n_total)
     plan = Q.Plan(w, fuse_steps=args.fuse_steps)  # allPoints readout: every step reduces rho(t_k)
     sz = plan.sizes
@@ -201,21 +205,40 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # R repetitions of K steps; inside each, events after every quarter (cuts on fusion-group bounds)
+    # give the time-vs-N_t line the paper shows ("the linear scaling" of the propagator)
+    q = max(1, K // 4)
+    cuts = [0, q, 2 * q, 3 * q, K] if (q % fuse == 0 and K >= 4) else [0, K]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in cuts] for _ in range(R)]
+    launches = 0
     with ClockSampler(local) as clk:
         time.sleep(0.3)  # let the sampler start
-        ev0.record(stream)
-        launches = plan.steps(L + Wm, L + Wm + K, ardm, work, stream)
-        ev1.record(stream)
+        for r in range(R):
+            k0 = L + Wm + r * K
+            evs[r][0].record(stream)
+            for i in range(1, len(cuts)):
+                launches += plan.steps(k0 + cuts[i - 1], k0 + cuts[i], ardm, work, stream)
+                evs[r][i].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    rep_ms = [evs[r][0].elapsed_time(evs[r][-1]) for r in range(R)]
+    ms = sorted(rep_ms)[R // 2]
+    launches //= R
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    nt_fit = None
+    if len(cuts) > 2:  # least squares t = a + b N_t over (cut, cumulative ms) of every repetition
+        xs = np.array([c for r in range(R) for c in cuts[1:]], dtype=float)
+        ys = np.array([evs[r][0].elapsed_time(evs[r][i]) for r in range(R) for i in range(1, len(cuts))])
+        b, a = np.polyfit(xs, ys, 1)
+        res = ys - (a + b * xs)
+        r2 = 1.0 - float(res @ res) / float(((ys - ys.mean()) ** 2).sum())
+        nt_fit = {"ms_per_step": float(b), "intercept_ms": float(a), "r2": r2, "points": int(len(xs)),
+                  "steps_at": cuts[1:], "note": "wall time linear in the number of time steps (P:455-466)"}
     rho = plan.read_rho(work, stream)
     tr_err = float(np.abs(np.einsum("kii->k", rho) - 1).max())
     del ardm, work
@@ -256,6 +279,8 @@ def main():
         line = {
             "metric": METRIC, "value": steps_per_s, "unit": "steps/s", "n_gpus": world, "steps": K,
             "warmup": Wm, "ms_per_step": ms_max / K, "higher_is_better": True,
+            "repetitions": {"count": R, "ms": rep_ms, "reported": "median"},
+            "n_t_fit": nt_fit,
             "scaling": "weak" if world > 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": base.name, "ardm_entries": sz.ardm_entries, "ardm_bytes": sz.ardm_bytes,
@@ -265,7 +290,8 @@ def main():
                               f"L2-resident ARDM ({sz.ardm_bytes / 1e6:.1f} MB): not flushed, not a roofline case"),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "kernel": kernel_name(sz),
-                       "steps_per_launch": K / max(1, launches)},
+                       "steps_per_launch": K / max(1, launches),
+                       "timed_steps_aligned_to_fusion_groups": K % fuse == 0, "fuse_steps": fuse},
             "achieved_gbs": achieved,
             "step_equivalent_gbs": step_equiv,
             "frac_of_unfused_roofline": step_equiv / peak,

@@ -1,25 +1,25 @@
 #!/bin/bash
-# End-of-round GPU session: sanitizers, bench line, launch list, ncu of the top kernel (summary + warp
-# stalls, the .ncu-rep stays on the box), per-slot launch times, sweep / eta benchmarks, GPU tests.
+# Round-end GPU profiling session (run from the repo root on a B200): bench lines of every config,
+# the launch list of the default bench, ncu --set full of the top kernels (summaries + warp stalls;
+# the .ncu-rep files stay on the box), per-slot launch times.  Sanitizers, the GPU test suite and
+# smoke() run separately (scripts/final_checks.sh).
 mkdir -p gpurun_out
-for tool in memcheck racecheck synccheck; do
-  echo "== $tool"; timeout 900 compute-sanitizer --tool $tool python scripts/sanitize_run.py 2>&1 | grep -E "sanitize run ok|SUMMARY|Error|error" | head -5
-done > gpurun_out/sanitize.txt 2>&1
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+for c in 1 2 0 4 5; do
+  timeout 900 python bench.py --cfg $c --no-cpu-baseline 2>> gpurun_out/bench_cfgs.err | tail -1
+done > gpurun_out/bench_cfgs.jsonl
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 60 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+    python bench.py --steps 60 --warmup 4 --reps 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 python scripts/launches_json.py gpurun_out/launches.csv gpurun_out/launches.json > /dev/null
-for sk in 1 4 0 9; do   # perp.py launch order: p0 = 0, 3, 6, 9, 12, 1, 4, 7, 10, 13, ...
-  ncu --set full --clock-control none --import-source on -k regex:k_fused3 -s $sk -c 1 -o /tmp/prof_s$sk -f \
-      python scripts/perp.py --reps 0 > /tmp/ncu_s$sk.log 2>&1
-  python scripts/ncu_summary.py /tmp/prof_s$sk.ncu-rep gpurun_out/prof_s$sk.json > /dev/null
-  python scripts/ncu_stalls.py /tmp/prof_s$sk.ncu-rep 8 > gpurun_out/stalls_s$sk.json
-done
-python scripts/perp.py > gpurun_out/perp.txt 2>&1
-{ timeout 600 python scripts/sweep_bench.py --L 5; timeout 600 python scripts/sweep_bench.py --L 7;
-  timeout 900 python scripts/sweep_bench.py --L 9 --no-cpu-baseline;
-  timeout 600 python scripts/sweep_bench.py --L 5 --temperature-sweep; } > gpurun_out/sweep.jsonl 2> gpurun_out/sweep.err
-timeout 300 python scripts/eta_bench.py > gpurun_out/eta_bench.jsonl 2> gpurun_out/eta_bench.err
-timeout 1800 python -m pytest tests/ -q -m gpu > gpurun_out/pytest_gpu.txt 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
-tail -2 gpurun_out/pytest_gpu.txt; cat gpurun_out/sanitize.txt; tail -1 gpurun_out/perp.txt; du -sh gpurun_out
+# k_fused4 on cfg3: two consecutive launches (two start slots) of the timed region
+ncu --set full --clock-control none --import-source on -k regex:k_fused4 -s 6 -c 2 -o /tmp/prof_f4 -f \
+    python bench.py --steps 40 --warmup 4 --reps 1 --no-cpu-baseline --no-e2e > /tmp/ncu_f4.log 2>&1
+python scripts/ncu_summary.py /tmp/prof_f4.ncu-rep gpurun_out/prof_f4.json > /dev/null
+python scripts/ncu_stalls.py /tmp/prof_f4.ncu-rep 8 > gpurun_out/stalls_f4.json
+# k_fused2s on cfg4
+ncu --set full --clock-control none --import-source on -k regex:k_fused2s -s 4 -c 1 -o /tmp/prof_f2s -f \
+    python bench.py --cfg 4 --steps 20 --warmup 4 --reps 1 --no-cpu-baseline --no-e2e > /tmp/ncu_f2s.log 2>&1
+python scripts/ncu_summary.py /tmp/prof_f2s.ncu-rep gpurun_out/prof_f2s.json > /dev/null
+python scripts/ncu_stalls.py /tmp/prof_f2s.ncu-rep 8 > gpurun_out/stalls_f2s.json
+timeout 600 python scripts/perp.py > gpurun_out/perp.txt 2>&1
+tail -c 400 gpurun_out/bench.json; echo; cut -c1-200 gpurun_out/bench_cfgs.jsonl; tail -2 gpurun_out/perp.txt; du -sh gpurun_out

@@ -17,14 +17,26 @@ def run(w, **kw):
     assert np.isfinite(r).all()
 
 
-# k_fused_r (S = 1, 2; M = 2, 3, 4; lattice and general s) and k_grow
+NP = Q.QP_FLAG_NO_PERSIST  # the per-group launch kernels (small problems otherwise take k_small)
+# k_fused_r (S = 1, 2; M = 2, 3, 4; lattice and general s), k_fused2s (M = 3, S = 2) and k_grow
 for fuse in (1, 2):
     for w in (W.CONFIGS[1].with_(n_steps=14), W.random_problem(3, 3, 4, 9), W.random_problem(4, 4, 3, 7),
               W.random_problem(5, 2, 7, 15, lattice_s=False), W.random_problem(6, 3, 4, 9, lattice_s=False)):
-        run(w, fuse_steps=fuse)
+        run(w, fuse_steps=fuse, flags=NP)
 # k_fused3: TMA-staged rounds (all four views at L = 8), plain loads (lane maps 0 and 1), generic moments
 for flags in (0, Q.QP_FLAG_NO_TMA, Q.QP_FLAG_GENERIC_MOMENTS):
-    run(W.random_problem(7, 2, 8, 20), flags=flags)
+    run(W.random_problem(7, 2, 8, 20), fuse_steps=3, flags=flags | NP)
+# k_fused4: TMA load + store rounds, every start slot at L = 8 and L = 9, symmetric and generic moments
+for flags in (0, Q.QP_FLAG_GENERIC_MOMENTS):
+    for L in (8, 9):
+        run(W.random_problem(7, 2, L, 2 * L + 6), flags=flags)
+# k_small: one CTA, ARDM and tables in shared memory (M = 2, 3, 4)
+for w in (W.CONFIGS[1].with_(n_steps=14), W.random_problem(3, 3, 3, 9), W.random_problem(4, 4, 2, 7),
+          W.random_problem(5, 2, 6, 15, lattice_s=False)):
+    run(w)
+# OFPF path filtering (k_ofpf_count / scan / scatter)
+rf, kept = Q.Plan(W.random_problem(11, 2, 6, 18)).filter_run(1e-3)
+assert np.isfinite(rf).all()
 # device eta setup (k_eta: 8-CTA clusters, DSMEM reduction) and a plan built from it
 eta = Q.eta_device([(1, 0.1, 7.5, 0.2), (2, 0.1, 7.5, 0.0), (3, 0.08, 2.2, 0.3), (0, 0.0, 1.0, 0.0)], 0.25, 6)
 assert np.isfinite(eta).all()
