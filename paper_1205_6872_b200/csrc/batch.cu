@@ -7,13 +7,51 @@
 // bit-identical).  The per-problem ARDM (16 N^L bytes) stays L2-resident for the sweep sizes of
 // interest; steps are separated by CTA barriers only (no kernel launch per step).
 //
-// Same mathematics as kernels.cu: for a fibre along the contracted slot p,
+// Same mathematics as the single-problem kernels: for a fibre along the contracted
+// slot p,
 //   out[new] = K'(new, last) exp(Ds(new) Psi(mid)) sum_old exp(Ds(new) psi_L(old)) a[old]
-// with the Eq. 9 exponents evaluated directly from the per-lag psi tables (Psi = sum over the kept
-// partners, one complex exp per Delta-s class), so no per-launch-set factor tables are needed.
+// with exp(delta_d Psi(mid)) a product over the L-1 kept partners.  Per slide step the CTA builds
+// digit-group tables in shared memory -- for groups of w consecutive kept slots (w digits of the
+// fibre index), the product of their per-lag factors for every digit combination -- so a fibre
+// multiplies ceil((L-1)/w) table entries per class instead of L-1 (the single-problem path's
+// Etab groups, built per step from the problem's own psi tables).
 #include "qp_internal.h"
 
 namespace qp {
+
+// Group width w (digits) of the slide factor tables: the widest w <= 4 with N^w <= 256 whose tables
+// (both kinds, D classes, all groups) stay within 48 KB and hold at most a quarter as many entries
+// as a step has fibres (the per-step table build stays small against the fibre loop); entries per
+// (kind, class): full groups of N^w plus the last group.
+__host__ __device__ inline int batch_bw(int M, int L, int D) {
+    const int N = M * M;
+    long long nf = 1;
+    for (int i = 0; i < L - 1; ++i) nf *= N;
+    for (int w = 4; w > 1; --w) {
+        long long nw = 1;
+        for (int i = 0; i < w; ++i) nw *= N;
+        if (nw > 256) continue;
+        long long tot = 0;
+        for (int r = L - 1; r > 0; r -= w) {
+            long long e = 1;
+            for (int i = 0; i < (r < w ? r : w); ++i) e *= N;
+            tot += e;
+        }
+        if (2LL * D * tot * 16 <= 48 * 1024 && 4 * tot <= nf) return w;
+    }
+    return 1;
+}
+__host__ __device__ inline long long batch_gtot(int M, int L, int w) {
+    const int N = M * M;
+    long long tot = 0;
+    for (int r = L - 1; r > 0; r -= w) {
+        long long e = 1;
+        for (int i = 0; i < (r < w ? r : w); ++i) e *= N;
+        tot += e;
+    }
+    return tot;
+}
+
 namespace {
 
 __device__ __forceinline__ double2 bmul(double2 a, double2 b) {
@@ -111,7 +149,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_batch(const __grid_constant__ B
                    *const pSelf = tabs + 3 * (L + 1) * N;
     double2 *const sT = tabs + ntab;
     const int nT = 2 * D * L * N;
-    double2 *const A = SMEM ? sT + nT : a.A + (size_t)b * a.NL;
+    // slide digit-group tables gT[kap][d][g * N^w + v] (rebuilt every slide step)
+    const int bw = batch_bw(M, L, D), G = (L - 1 + bw - 1) / bw;
+    const int gtot = (int)batch_gtot(M, L, bw);
+    unsigned Nw = 1;
+    for (int i = 0; i < bw; ++i) Nw *= N;
+    double2 *const gT = sT + nT;
+    double2 *const A = SMEM ? gT + 2 * D * gtot : a.A + (size_t)b * a.NL;
     __shared__ double2 sH0[M][M], sH1[M][M], sU[M][M];
     __shared__ double2 sKp[2][N][N];     // K'(new, last) for propagate (0) / terminal (1) self classes
     // exp(delta_d psi_L(old)) of the lag-L partner [variant][kap][d][old]: variant 0 (k > L) propagate
@@ -202,29 +246,47 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_batch(const __grid_constant__ B
                     A[x + v * nin] = bmul(bmul(sKp[0][v][last], fp), ax);
                 }
             }
-        } else {  // slide on slot p = k mod L: exp(delta_d Psi) as products of the sT digit factors
-            const int p = (int)(k % L), qlast = (p - 1 + L) % L;
+        } else {  // slide on slot p = k mod L: exp(delta_d Psi) as products of digit-group table entries
+            const int p = (int)(k % L);
             unsigned Pp_ = 1;
             for (int t = 0; t < p; ++t) Pp_ *= N;
+            // the fibre index fi enumerates the kept slots q != p in increasing order (rank r = q or
+            // q - 1); the previous point sigma_{k-1} sits in slot p - 1 (rank p - 1), or L - 1 (rank L - 2)
+            unsigned Pl = 1;
+            for (int t = 0; t < (p >= 1 ? p - 1 : L - 2); ++t) Pl *= N;
+            for (int i = threadIdx.x; i < (ro ? 2 : 1) * D * gtot; i += BLOCK) {
+                const int kd = i / gtot, e = i % gtot, g = e / (int)Nw, kap = kd / D, d = kd % D;
+                unsigned v = (unsigned)(e - g * (int)Nw);
+                double2 pr = make_double2(1.0, 0.0);
+                for (int j = 0; j < bw && g * bw + j < L - 1; ++j, v /= N) {
+                    const int rk = g * bw + j, q = rk < p ? rk : rk + 1;
+                    pr = bmul(pr, sT[((kap * D + d) * L + (p - q + L) % L) * N + (int)(v % N)]);  // lag 1..L-1
+                }
+                gT[i] = pr;
+            }
+            __syncthreads();
             const unsigned nf = (unsigned)(a.NL / N);  // N^(L-1) < 2^32 for batch problems
             for (unsigned fi = threadIdx.x; fi < nf; fi += BLOCK) {
                 const unsigned xb = (fi % Pp_) + (fi / Pp_) * Pp_ * N;
+                const int last = (int)((fi / Pl) % N);
                 double2 Ep[DMX], Et[DMX];
-#pragma unroll
-                for (int d = 0; d < DMX; ++d) Ep[d] = Et[d] = make_double2(1.0, 0.0);
-                int last = 0;
-                unsigned r = xb;
-                for (int q = 0; q < L; ++q) {
-                    const int dq = (int)(r % N);
-                    r /= N;
-                    if (q == qlast) last = dq;
-                    if (q == p) continue;
-                    const double2 *t0 = sT + ((p - q + L) % L) * N + dq;  // lag 1..L-1
+                {
+                    const unsigned v0 = G > 1 ? fi % Nw : fi;
 #pragma unroll
                     for (int d = 0; d < DMX; ++d)
                         if (d < D) {
-                            Ep[d] = bmul(Ep[d], t0[d * L * N]);
-                            if (ro) Et[d] = bmul(Et[d], t0[(D + d) * L * N]);
+                            Ep[d] = gT[d * gtot + v0];
+                            Et[d] = ro ? gT[(D + d) * gtot + v0] : make_double2(0.0, 0.0);
+                        }
+                }
+                unsigned rem = fi / Nw;
+                for (int g = 1; g < G; ++g, rem /= Nw) {
+                    const int o = g * (int)Nw + (int)(g < G - 1 ? rem % Nw : rem);
+#pragma unroll
+                    for (int d = 0; d < DMX; ++d)
+                        if (d < D) {
+                            Ep[d] = bmul(Ep[d], gT[d * gtot + o]);
+                            if (ro) Et[d] = bmul(Et[d], gT[(D + d) * gtot + o]);
                         }
                 }
                 double2 xo[N];
@@ -336,7 +398,8 @@ cudaError_t batch_t(const BatchArgs &a, int B, cudaStream_t s) {
 }  // namespace
 
 size_t batch_dyn_smem(int M, int L, int D) {
-    return ((size_t)(3 * (L + 1) + 2) * M * M + (size_t)2 * D * L * M * M) * sizeof(double2);
+    return ((size_t)(3 * (L + 1) + 2) * M * M + (size_t)2 * D * L * M * M + (size_t)2 * D * batch_gtot(M, L, batch_bw(M, L, D))) *
+           sizeof(double2);
 }
 
 cudaError_t launch_psi_tables(int M, const double (&s)[kMaxM], const double2 *eta, double2 *ptab, int B, int L, cudaStream_t st) {

@@ -71,10 +71,21 @@ def main():
             "rho11_final_min_max": [float(rho[:, -1, 1, 1].real.min()), float(rho[:, -1, 1, 1].real.max())],
             "max_abs_trace_err": float(np.abs(np.einsum("bkii->bk", rho) - 1).max())}
     # roofline of k_batch (one step per pass over each problem's ARDM): FP64 flops per element update
-    # counted from the slide step with readout (M = 2, D = 2; per fibre of N = 4 entries: digit-factor
-    # products 24 (L-1), S0 6, beta moments 128, class factors 24, outputs 24, readout 32), bytes 32 per
-    # element update when the ARDM streams through HBM (B N^L 16 B > L2), else none (L2 / smem resident)
-    flops = (24 * (L - 1) + 214) / N
+    # counted from the slide step with readout (M = 2, D = 2; per fibre of N = 4 entries: digit-group
+    # factor products 24 (G - 1) for G groups of w digits plus the per-step table build
+    # 24 (w - 1) tot / N^(L-1), S0 6, beta moments 128, class factors 24, outputs 24, readout 32;
+    # w and G as batch.cu batch_bw), bytes 32 per element update when the ARDM streams through HBM
+    # (B N^L 16 B > L2), else none (L2 / smem resident)
+    nf = N ** (L - 1)
+    bw = 1
+    for w_ in (4, 3, 2):
+        tot_ = sum(N ** min(w_, r) for r in range(L - 1, 0, -w_))
+        if 2 * 2 * tot_ * 16 <= 48 * 1024 and 4 * tot_ <= nf:
+            bw = w_
+            break
+    G = -(-(L - 1) // bw)
+    tot = sum(N ** min(bw, r) for r in range(L - 1, 0, -bw))
+    flops = (24 * (G - 1) + 24 * (bw - 1) * tot / nf + 214) / N
     tflops = ps * N ** L * flops / 1e12
     fp64_peak = 35.1  # measured DFMA rate, scripts/membench.cu (profiles/README.md); no FP64 in MEASURED_PEAKS
     ardm = 16 * a.B * N ** L
@@ -84,7 +95,7 @@ def main():
         gbs = ps * N ** L * 32 / 1e9
         hbm = {"achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"]}
     alu = {"achieved": tflops, "peak": fp64_peak, "unit": "TFLOP/s", "frac": tflops / fp64_peak,
-           "flops_per_element_update": flops}
+           "flops_per_element_update": flops, "digit_groups": G, "group_width": bw}
     if hbm and hbm["frac"] > alu["frac"]:
         line["roofline"] = {"bound": "hbm", **hbm, "alu": alu}
     else:
