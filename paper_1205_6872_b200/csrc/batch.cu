@@ -156,7 +156,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_batch(const __grid_constant__ B
     for (int i = 0; i < bw; ++i) Nw *= N;
     double2 *const gT = sT + nT;
     double2 *const A = SMEM ? gT + 2 * D * gtot : a.A + (size_t)b * a.NL;
-    __shared__ double2 sH0[M][M], sH1[M][M], sU[M][M];
+    // the steps' propagators, computed for a chunk of CH steps at once (one step per thread) instead of
+    // by one thread inside every step
+    constexpr int CH = 8192 / (M * M * 16);
+    __shared__ double2 sH0[M][M], sH1[M][M], sU[CH][M][M];
     __shared__ double2 sKp[2][N][N];     // K'(new, last) for propagate (0) / terminal (1) self classes
     // exp(delta_d psi_L(old)) of the lag-L partner [variant][kap][d][old]: variant 0 (k > L) propagate
     // eta_L / terminal E_L; variant 1 (k == L, partner sigma_0) propagate E_L / terminal TI_L
@@ -188,23 +191,39 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_batch(const __grid_constant__ B
         if (a.out_idx[0] >= 0) a.rho[((size_t)b * a.n_out + a.out_idx[0]) * N + n] = r0[n];
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool drive = a.f != nullptr;
+    // divisions by powers of N: shifts and masks when N is a power of two (M = 2, 4)
+    constexpr bool POW2 = (N & (N - 1)) == 0;
+    auto udiv = [&](unsigned x, unsigned pw) -> unsigned {
+        if constexpr (POW2) return x >> (31 - __clz(pw));
+        else return x / pw;
+    };
+    auto umod = [&](unsigned x, unsigned pw) -> unsigned {
+        if constexpr (POW2) return x & (pw - 1);
+        else return x % pw;
+    };
     for (long long k = 1; k <= a.n_steps; ++k) {
         const bool ro = a.out_idx[k] >= 0;
-        if (threadIdx.x == 0 && (k == 1 || a.f != nullptr)) {  // the step's propagator
-            const double fk = a.f ? a.f[(size_t)b * a.n_steps + (k - 1)] : 0.0;
-            double2 H[M][M], U[M][M];
-            for (int i = 0; i < M; ++i)
-                for (int j = 0; j < M; ++j) H[i][j] = make_double2(sH0[i][j].x + fk * sH1[i][j].x, sH0[i][j].y + fk * sH1[i][j].y);
-            expm_herm<M>(H, a.dt, U);
-            for (int i = 0; i < M; ++i)
-                for (int j = 0; j < M; ++j) sU[i][j] = U[i][j];
+        if ((k - 1) % CH == 0 && (k == 1 || drive)) {  // propagators of steps k .. k + CH - 1
+            const long long kk = k + threadIdx.x;
+            if (threadIdx.x < CH && kk <= a.n_steps && (drive || threadIdx.x == 0)) {
+                const double fk = drive ? a.f[(size_t)b * a.n_steps + (kk - 1)] : 0.0;
+                double2 H[M][M], U[M][M];
+                for (int i = 0; i < M; ++i)
+                    for (int j = 0; j < M; ++j)
+                        H[i][j] = make_double2(sH0[i][j].x + fk * sH1[i][j].x, sH0[i][j].y + fk * sH1[i][j].y);
+                expm_herm<M>(H, a.dt, U);
+                for (int i = 0; i < M; ++i)
+                    for (int j = 0; j < M; ++j) sU[threadIdx.x][i][j] = U[i][j];
+            }
         }
         __syncthreads();  // sU ready; previous step's writes visible
-        if (k == 1 || a.f != nullptr) {
+        if (k == 1 || drive) {
+            const double2(&U)[M][M] = sU[drive ? (int)((k - 1) % CH) : 0];
             for (int i = threadIdx.x; i < 2 * N * N; i += BLOCK) {
                 const int kap = i / (N * N), nw = (i / N) % N, last = i % N;
                 // K(new, last) = U[a, a'] conj(U[b, b']) (Eq. 8), times the self factor of the new point
-                const double2 ua = sU[nw / M][last / M], ub = sU[nw % M][last % M];
+                const double2 ua = U[nw / M][last / M], ub = U[nw % M][last % M];
                 sKp[kap][nw][last] = bmul(bmul(ua, make_double2(ub.x, -ub.y)), sSelf[kap][nw]);
             }
             __syncthreads();
@@ -267,11 +286,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_batch(const __grid_constant__ B
             __syncthreads();
             const unsigned nf = (unsigned)(a.NL / N);  // N^(L-1) < 2^32 for batch problems
             for (unsigned fi = threadIdx.x; fi < nf; fi += BLOCK) {
-                const unsigned xb = (fi % Pp_) + (fi / Pp_) * Pp_ * N;
-                const int last = (int)((fi / Pl) % N);
+                const unsigned xb = udiv(fi, Pp_) * Pp_ * N + umod(fi, Pp_);
+                const int last = (int)umod(udiv(fi, Pl), (unsigned)N);
                 double2 Ep[DMX], Et[DMX];
                 {
-                    const unsigned v0 = G > 1 ? fi % Nw : fi;
+                    const unsigned v0 = G > 1 ? umod(fi, Nw) : fi;
 #pragma unroll
                     for (int d = 0; d < DMX; ++d)
                         if (d < D) {
@@ -279,9 +298,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_batch(const __grid_constant__ B
                             Et[d] = ro ? gT[(D + d) * gtot + v0] : make_double2(0.0, 0.0);
                         }
                 }
-                unsigned rem = fi / Nw;
-                for (int g = 1; g < G; ++g, rem /= Nw) {
-                    const int o = g * (int)Nw + (int)(g < G - 1 ? rem % Nw : rem);
+                unsigned rem = udiv(fi, Nw);
+                for (int g = 1; g < G; ++g, rem = udiv(rem, Nw)) {
+                    const int o = g * (int)Nw + (int)(g < G - 1 ? umod(rem, Nw) : rem);
 #pragma unroll
                     for (int d = 0; d < DMX; ++d)
                         if (d < D) {
