@@ -104,7 +104,7 @@ def kernel_name(sz) -> str:
     if sz.M == 3 and sz.fuse_steps == 2:
         return "k_fused2s: 2 time steps per HBM pass, 32-fibre units staged in shared memory (cp.async)"
     return {4: "k_fused4: 4 time steps per HBM pass, TMA load + TMA store of 8-fibre rounds "
-               "(2-stage ring, producer warp), persistent grid",
+               "(6-stage ring, load and store warps, 8 consumer warps, readout sums in TMEM), one CTA per SM",
             3: "k_fused3: 3 time steps per HBM pass, per-warp TMA-staged rounds"}.get(
         sz.fuse_steps, f"k_fused_r: {sz.fuse_steps} time step(s) per HBM pass")
 

@@ -944,7 +944,7 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
     ls.f4 = false;
     if (f4) {
         // k_fused4: one E0 block per 8-fibre round of a tile: factors [s][kap][c][f] + the 8 lofs (int2)
-        if (f4_layout(P, ls, pos, inner, outer) && T % 8 == 0) {
+        if (f4_layout(P, ls, pos, inner, outer) && T % 8 == 0 && T >= 16) {  // >= 2 rounds per tile (slide4.cu ring depth)
             ls.f4 = true;
             const int F = 8, R = T / F, Q = S * 2 * D;
             const size_t blk = (size_t)Q * F + F / 2;

@@ -9,14 +9,15 @@
 //   phase 2 (sub-steps 2, 3: fibres along d2, d3): lane q2 holds fixed (d0, d1), Y[d3][d2];
 // between the phases the 16 lanes transpose through shared memory (__syncwarp only).
 //
-// Warp specialisation: a CTA is 4 consumer warps (8 outer fibres per round, 2 per warp, one per
-// half-warp) and 1 producer warp.  The producer streams rounds through a 2-deep ring of 32 KB
-// shared-memory stages with TMA: a 5-D cp.async.bulk.tensor box of the round's 8 x 256 entries
-// (load tensor map) plus one bulk copy of the round's outer factors, completing on full[b]; the
-// consumers read the stage, run the four sub-steps in registers, write the results back into the
-// stage in the store map's layout, fence the async proxy and arrive on done[b]; the producer then
-// writes the stage back with one cp.async.bulk.tensor store (store tensor map) and, once the store
-// has read the stage, refills it with round r + 2.  The load and store maps order the box dimensions
+// Warp specialisation: one CTA per SM of 8 consumer warps in two groups of 4 and 1 producer warp.
+// A round is 8 outer fibres (2 per consumer warp, one per half-warp); the groups take alternate
+// rounds.  The producer streams rounds through a ring of kF4NS 32 KB shared-memory stages with TMA:
+// a 5-D cp.async.bulk.tensor box of the round's 8 x 256 entries (load tensor map) plus one bulk copy
+// of the round's outer factors, completing on full[b]; the group's consumers read the stage, run the
+// four sub-steps in registers, write the results back into the stage in the store map's layout,
+// fence the async proxy and arrive on done[b]; the producer writes each finished stage back with one
+// cp.async.bulk.tensor store (store tensor map) as soon as it is done and, once the store has read
+// the stage, refills it with the round kF4NS ahead.  The load and store maps order the box dimensions
 // (host.cpp: f4_layout) so that the phase-1 reads and the phase-2 writes are free of bank conflicts
 // under the 128-B swizzle; the transpose uses its own conflict-free placement inside the stage.
 //
@@ -24,16 +25,24 @@
 //   K'(nw, last) x inner factor of the lane-varying inner digit   (KU, CTA-wide, built once)
 //   x inner factors of the lane-fixed inner digits x outer digit groups >= 1   (LF, per tile)
 //   x outer group-0 factor of the fibre                                   (E0, per round)
-// Readout: rho_00, rho_11 and rho_01 per step (rho_10 = conj rho_01: rho(t) is Hermitian, SURVEY
-// 8(c) C.4), per-thread shared-memory accumulators, fixed-order reduction at the end.
+// Readout: Re rho_00, Re rho_11 and rho_01 per step (rho_10 = conj rho_01 and a real diagonal: rho(t)
+// is Hermitian), per-thread shared-memory accumulators, fixed-order reduction at the end.
 #include "common.cuh"
 
 namespace qp {
 
 namespace {
 
-constexpr int kF4Consumers = 4;                    // consumer warps
-constexpr int kF4Block = 32 * (kF4Consumers + 1);  // + 1 producer warp
+#ifndef QP_F4_GROUPS
+#define QP_F4_GROUPS 2
+#endif
+#ifndef QP_F4_NS
+#define QP_F4_NS 6
+#endif
+constexpr int kF4Groups = QP_F4_GROUPS;             // consumer groups of 4 warps (alternate rounds)
+constexpr int kF4Consumers = 4 * kF4Groups;         // consumer warps
+constexpr int kF4Block = 32 * (kF4Consumers + 2);  // + a store warp and a load warp
+constexpr int kF4NS = QP_F4_NS;                     // stages in the ring
 constexpr int kF4F = 8;                            // outer fibres per round
 constexpr int kF4Stage = kF4F * 256;               // entries per stage (32 KB)
 constexpr int kF4E0B = 4 * 2 * 2 * kF4F + kF4F / 2;  // E0 block: factors [s][kap][c][f] + 8 int2 (offset, 'last' digit)
@@ -49,11 +58,32 @@ __device__ __forceinline__ void tma_store_5dc(const void *tmap, const void *src,
                  ::"l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_addr(src)) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
 }
+// Tensor memory (TMEM) as per-thread accumulator storage: the readout sums of a consumer thread live in
+// its TMEM lane (32x32b shape: warp w reaches lanes 32 (w % 4) .. + 31), 8 x 32-bit columns per sub-step.
+__device__ __forceinline__ void tmem_ld8(unsigned ta, double (&v)[4]) {
+    unsigned r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta) : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+__device__ __forceinline__ void tmem_st8(unsigned ta, const double (&v)[4]) {
+    unsigned r[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[2 * i] = (unsigned)__double2loint(v[i]), r[2 * i + 1] = (unsigned)__double2hiint(v[i]);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                 ::"r"(ta), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // 128-B swizzle of a stage offset in 16-B units (stage 1024-B aligned): chunk bits 0-2 ^= bits 3-5
 __device__ __forceinline__ int swz(int o, int on) { return on ? o ^ ((o >> 3) & 7) : o; }
 
@@ -81,17 +111,17 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     constexpr bool LAT = false;
     constexpr int NK = RO ? 2 : 1;
     extern __shared__ __align__(1024) double2 smem4[];
-    double2 *const stage = smem4;                                    // [2][kF4Stage]
-    double2 *const sE0 = smem4 + 2 * kF4Stage;                       // [2][kF4E0B]
-    double2 *const sLF = sE0 + 2 * kF4E0B;                           // [2][S][NK][D][16]
+    double2 *const stage = smem4;                                    // [kF4NS][kF4Stage]
+    double2 *const sE0 = smem4 + kF4NS * kF4Stage;                   // [kF4NS][kF4E0B]
+    double2 *const sLF = sE0 + kF4NS * kF4E0B;                       // [2][S][NK][D][16]
     double2 *const sKU = sLF + 2 * S * 2 * D * 16;                   // [S][NK][4 vd][N nw][N last]
-    double2 *const accS = sKU + S * 2 * 4 * N * N;                   // [S][3][128] (RO)
     __shared__ double2 sBeta[S][2][D][N];
-    __shared__ __align__(8) unsigned long long bar_full[2], bar_done[2], bar_lf[2];
+    __shared__ unsigned tmem_base;
+    __shared__ __align__(8) unsigned long long bar_full[kF4NS], bar_done[kF4NS], bar_empty[kF4NS], bar_lf[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const SmallLayout lay{N, D, 0};
 
-    // ---- CTA-wide setup: KU (tile independent), beta, readout accumulators, barriers
+    // ---- CTA-wide setup: KU (tile independent), beta, barriers
     for (int i = tid; i < S * NK * 4 * N * N; i += kF4Block) {
         const int last = i % N, nw = (i / N) % N, vd = (i / (N * N)) % 4, kap = (i / (N * N * 4)) % NK, s = i / (N * N * 4 * NK);
         // lane-varying inner digit of sub-step s: s = 0 -> d1, 1 -> d0, 2 -> d3, 3 -> d2
@@ -105,85 +135,105 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
         const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
         (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
     }
-    if constexpr (RO)
-        for (int i = tid; i < S * 3 * 128; i += kF4Block) accS[i] = make_double2(0.0, 0.0);
     if (tid == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kF4NS; ++b) {
             mbar_init(&bar_full[b], 1);
-            mbar_init(&bar_done[b], kF4Consumers);
-            mbar_init(&bar_lf[b], 1);
+            mbar_init(&bar_done[b], 4);
+            mbar_init(&bar_empty[b], 1);
         }
+        for (int b = 0; b < 2; ++b) mbar_init(&bar_lf[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
+    // readout accumulators in TMEM: 32 columns per consumer thread (warps w, w + 4 share lanes: columns
+    // 32 (w / 4) .. + 31), allocated by warp 0, zeroed by their threads
+    if constexpr (RO) {
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
+                         "n"(32 * kF4Groups) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 32u * (unsigned)(warp >> 2);
+    if constexpr (RO)
+        if (warp < kF4Consumers) {
+            const double z[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int s = 0; s < S; ++s) tmem_st8(tacc + 8 * s, z);
+            tmem_wait_st();
+        }
+
     const int per = a.n_tiles / (int)gridDim.x, rem = a.n_tiles % (int)gridDim.x;
     const int t_begin = (int)blockIdx.x * per + min((int)blockIdx.x, rem);
     const int t_end = t_begin + per + ((int)blockIdx.x < rem ? 1 : 0);
-    const int rounds = a.T / kF4F;
+    const int rounds = a.T / kF4F;                 // >= 2 (host: T >= 16)
+    const int R = (t_end - t_begin) * rounds;      // this CTA's rounds, in order
+    // ring depth: the load warp refills the stage of round j with round j + NS once j has been stored and
+    // builds a tile's LF table (buffer tile & 1) only then, so every round of the tile two back is done
+    // when NS <= rounds + 1
+    const int NS = min(kF4NS, rounds + 1);
 
     if (warp == kF4Consumers) {
-        // =========================================================== producer warp
-        int r = 0;
-        for (int tau = t_begin; tau < t_end; ++tau) {
-            for (int rd = 0; rd < rounds; ++rd, ++r) {
-                const int b = r & 1;
-                if (r >= 2) {  // round r - 2 (same stage) done by the consumers: write it back
-                    if (lane == 0) {
-                        mbar_wait(&bar_done[b], ((r - 2) >> 1) & 1);
-                        const int rp = rd >= 2 ? rd - 2 : rd - 2 + rounds, taup = rd >= 2 ? tau : tau - 1;
-                        const Coords k = f4_coords(a, (long long)taup * a.T + (long long)rp * kF4F, 1);
-                        tma_store_5dc(&a.tmapS, stage + b * kF4Stage, k.c[0], k.c[1], k.c[2], k.c[3], k.c[4]);
-                        bulk_commit();
-                    }
-                    __syncwarp();  // the other lanes may rewrite LF only after lane 0 has seen round r - 2 done
-                }
-                if (rd == 0) {
-                    // this tile's LF[s][kap][c][q] = (outer groups >= 1 x shard digits) x inner factors of the
-                    // lane-fixed digits of lane mapping q (buffer tau & 1; its tile tau - 2 finished before
-                    // round r - 2 completed, which the wait above has seen)
-                    const int lb = (tau - t_begin) & 1;
-                    for (int i = lane; i < S * NK * D * 16; i += 32) {
-                        const int q = i % 16, c = (i / 16) % D, kap = (i / (16 * D)) % NK, s = i / (16 * D * NK);
-                        double2 e = a.fixfac[s][kap][c];
-                        for (int g = 1; g < a.G; ++g)
-                            e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + c) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
-                        int da, db, ia, ib;  // the two lane-fixed digits (ia, ib) and their values for lane q
-                        if (s < 2) {
-                            ia = 2, ib = 3;
-                            if (a.f4_q1swap) db = q & 3, da = q >> 2; else da = q & 3, db = q >> 2;
-                        } else {
-                            ia = 0, ib = 1;
-                            if (a.f4_q2swap) db = q & 3, da = q >> 2; else da = q & 3, db = q >> 2;
-                        }
-                        e = cmul(e, __ldg(&a.inner[((((size_t)s * S + ia) * 2 + kap) * D + c) * N + da]));
-                        e = cmul(e, __ldg(&a.inner[((((size_t)s * S + ib) * 2 + kap) * D + c) * N + db]));
-                        sLF[(size_t)lb * S * 2 * D * 16 + i] = e;
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bar_lf[lb]);
-                }
-                if (lane == 0) {
-                    if (r >= 2) bulk_wait_read0();  // the store of round r - 2 has read the stage
-                    fence_proxy_async();
-                    mbar_expect_tx(&bar_full[b], kF4Stage * 16 + kF4E0B * 16);
-                    const Coords k = f4_coords(a, (long long)tau * a.T + (long long)rd * kF4F, 0);
-                    tma_load_5dc(stage + b * kF4Stage, &a.tmap, &bar_full[b], k.c[0], k.c[1], k.c[2], k.c[3], k.c[4]);
-                    bulk_g2s(sE0 + b * kF4E0B, a.E0r + (size_t)rd * kF4E0B, kF4E0B * 16, &bar_full[b]);
-                }
-            }
-        }
-        // drain: the last two rounds
+        // =========================================================== store warp
+        // round j: wait for its group (done), store the stage; once the store of round j - 1 has read
+        // its stage (bulk wait_group.read 1: the store of j may still be reading), release that stage
         if (lane == 0) {
-            for (int rr = (r >= 2 ? r - 2 : 0); rr < r; ++rr) {
-                const int b = rr & 1;
-                mbar_wait(&bar_done[b], (rr >> 1) & 1);
-                const int rd = rr % rounds, tau = t_begin + rr / rounds;
+            for (int j = 0; j < R; ++j) {
+                const int b = j % NS, tau = t_begin + j / rounds, rd = j % rounds;
+                mbar_wait(&bar_done[b], (j / NS) & 1);
                 const Coords k = f4_coords(a, (long long)tau * a.T + (long long)rd * kF4F, 1);
                 tma_store_5dc(&a.tmapS, stage + b * kF4Stage, k.c[0], k.c[1], k.c[2], k.c[3], k.c[4]);
                 bulk_commit();
+                if (j >= 1) {
+                    bulk_wait_read1();
+                    mbar_arrive(&bar_empty[(j - 1) % NS]);
+                }
             }
             bulk_wait0();
+        }
+    } else if (warp == kF4Consumers + 1) {
+        // =========================================================== load warp
+        // round r into stage r % NS once the stage's previous round (r - NS) has been stored and read
+        for (int r = 0; r < R; ++r) {
+            const int tau = t_begin + r / rounds, rd = r % rounds, b = r % NS;
+            if (r >= NS) mbar_wait(&bar_empty[b], ((r / NS) - 1) & 1);
+            if (rd == 0) {
+                // this tile's LF[s][kap][c][q] = (outer groups >= 1 x shard digits) x inner factors of the
+                // lane-fixed digits of lane mapping q (buffer tau & 1: every round of tile tau - 2 has been
+                // stored, as NS <= rounds + 1)
+                const int lb = (tau - t_begin) & 1;
+                for (int i = lane; i < S * NK * D * 16; i += 32) {
+                    const int q = i % 16, c = (i / 16) % D, kap = (i / (16 * D)) % NK, s = i / (16 * D * NK);
+                    double2 e = a.fixfac[s][kap][c];
+                    for (int g = 1; g < a.G; ++g)
+                        e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + c) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
+                    int da, db, ia, ib;  // the two lane-fixed digits (ia, ib) and their values for lane q
+                    if (s < 2) {
+                        ia = 2, ib = 3;
+                        if (a.f4_q1swap) db = q & 3, da = q >> 2; else da = q & 3, db = q >> 2;
+                    } else {
+                        ia = 0, ib = 1;
+                        if (a.f4_q2swap) db = q & 3, da = q >> 2; else da = q & 3, db = q >> 2;
+                    }
+                    e = cmul(e, __ldg(&a.inner[((((size_t)s * S + ia) * 2 + kap) * D + c) * N + da]));
+                    e = cmul(e, __ldg(&a.inner[((((size_t)s * S + ib) * 2 + kap) * D + c) * N + db]));
+                    sLF[(size_t)lb * S * 2 * D * 16 + i] = e;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_lf[lb]);
+            }
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&bar_full[b], kF4Stage * 16 + kF4E0B * 16);
+                const Coords k = f4_coords(a, (long long)tau * a.T + (long long)rd * kF4F, 0);
+                tma_load_5dc(stage + b * kF4Stage, &a.tmap, &bar_full[b], k.c[0], k.c[1], k.c[2], k.c[3], k.c[4]);
+                bulk_g2s(sE0 + b * kF4E0B, a.E0r + (size_t)rd * kF4E0B, kF4E0B * 16, &bar_full[b]);
+            }
+            __syncwarp();
         }
     } else {
         // =========================================================== consumer warps
@@ -198,7 +248,8 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
         const int q1swap = LT ? 0 : a.f4_q1swap, q2swap = LT ? 0 : a.f4_q2swap;
         const int colreg = LT ? (LT == 1) : a.f4_colregion, swon = LT ? 1 : a.f4_swz;
         const int h = lane >> 4, q = lane & 15;
-        const int f = 2 * warp + h;  // fibre of this half-warp within the round
+        const int grp = warp >> 2;          // consumer group: rounds grp, grp + kF4Groups, ...
+        const int f = 2 * (warp & 3) + h;   // fibre of this half-warp within the round
         // phase-1 lane digits (d2, d3) and phase-2 lane digits (d0, d1)
         const int l2 = q1swap ? (q >> 2) : (q & 3), l3 = q1swap ? (q & 3) : (q >> 2);
         const int l0 = q2swap ? (q >> 2) : (q & 3), l1 = q2swap ? (q & 3) : (q >> 2);
@@ -216,12 +267,11 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
             // col-region: fibre f owns chunk f ^ (row & 7) (swizzled) or f (dense) of every row
             return colreg ? (p + 8 * rho) * 8 + (swon ? f ^ p : f) : (32 * f + rho) * 8 + p;
         };
-        double2 *const acc_t = accS + tid;  // [s][j][128] at acc_t[(s * 3 + j) * 128]
 
         // one fibre at sub-step s: xf = old values along the contracted digit -> new values.
         // vd = value of the lane-varying inner digit, last = previous time point's value.
         auto fibre = [&](double2 (&xf)[N], int s, int vd, int last, bool ro, const double2 (&E0e)[D], double2 &t01,
-                         double2 &a00, double2 &a11) {
+                         double &a00, double &a11) {
             double2 S0, m0[D], m10;
             if constexpr (SYM) {
                 const double2 uu = cadd(xf[0], xf[3]), w = csub(xf[0], xf[3]);
@@ -264,8 +314,8 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
             xf[2] = cmul(ku0[2 * N], P1);  // class 2 = (1, 0)
             if (ro) {
                 const double2 *ku1 = sKU + ((s * NK + (NK - 1)) * 4 + vd) * N * N + last;
-                a00 = cadd(a00, xf[0]);
-                a11 = cadd(a11, xf[3]);
+                a00 += xf[0].x;
+                a11 += xf[3].x;
                 t01 = cfma(ku1[1 * N], m10, t01);
             }
         };
@@ -273,22 +323,32 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
         auto e0eff = [&](const double2 *e0b, const double2 *lf, int s, int kap, int c) {
             return cmul(e0b[((s * 2 + kap) * D + c) * kF4F + f], lf[((s * NK + kap) * D + c) * 16 + q]);
         };
-        auto flush = [&](int s, double2 a00, double2 a11, double2 t01, const double2 &E0t) {
-            double2 *p = acc_t + (s * 3) * 128;
-            p[0] = cadd(p[0], a00);
-            p[128] = cadd(p[128], a11);
-            p[256] = cfma(E0t, t01, p[256]);
+        // readout: per consumer thread Re rho_00, Re rho_11, rho_01 (re, im) per sub-step in shared memory
+        // readout: Re rho_00, Re rho_11, rho_01 (re, im) of sub-step s in TMEM columns 8 s .. 8 s + 7
+        auto flush = [&](int s, double a00, double a11, double2 t01, const double2 &E0t) {
+            double p[4];
+            tmem_wait_st();  // this thread's previous store to the columns (a sub-step ago) has landed
+            tmem_ld8(tacc + 8 * s, p);
+            p[0] += a00;
+            p[1] += a11;
+            p[2] = fma(E0t.x, t01.x, fma(-E0t.y, t01.y, p[2]));
+            p[3] = fma(E0t.x, t01.y, fma(E0t.y, t01.x, p[3]));
+            tmem_st8(tacc + 8 * s, p);
         };
 
-        int r = 0;
-        for (int tau = t_begin; tau < t_end; ++tau) {
-            const int lb = (tau - t_begin) & 1;
-            mbar_wait(&bar_lf[lb], ((tau - t_begin) >> 1) & 1);
-            const double2 *lf = sLF + (size_t)lb * S * 2 * D * 16;
-            const int last_t = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
-            for (int rd = 0; rd < rounds; ++rd, ++r) {
-                const int b = r & 1;
-                mbar_wait(&bar_full[b], (r >> 1) & 1);
+        int cur = -1, last_t = 0;
+        const double2 *lf = sLF;
+        for (int r = grp; r < R; r += kF4Groups) {
+            const int tau = t_begin + r / rounds, b = r % NS;
+            if (tau != cur) {  // a new tile: its LF table (buffer tau & 1) and sub-step 0's 'last' digit
+                cur = tau;
+                const int lb = (tau - t_begin) & 1;
+                mbar_wait(&bar_lf[lb], ((tau - t_begin) >> 1) & 1);
+                lf = sLF + (size_t)lb * S * 2 * D * 16;
+                last_t = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
+            }
+            {
+                mbar_wait(&bar_full[b], (r / NS) & 1);
                 double2 *const st = stage + b * kF4Stage;
                 const double2 *const e0b = sE0 + b * kF4E0B;
                 const int lastf = reinterpret_cast<const int2 *>(e0b + 4 * 2 * 2 * kF4F)[f].y;
@@ -307,7 +367,8 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
 #pragma unroll
                     for (int c = 0; c < D; ++c) E0e[c] = e0eff(e0b, lf, s, 0, c);
                     if (ro) E0t = e0eff(e0b, lf, s, NK - 1, 0);
-                    double2 t01 = make_double2(0.0, 0.0), a00 = t01, a11 = t01;
+                    double2 t01 = make_double2(0.0, 0.0);
+                    double a00 = 0.0, a11 = 0.0;
                     if (s == 0) {
 #pragma unroll
                         for (int d1 = 0; d1 < N; ++d1) fibre(X[d1], 0, d1, last0, ro, E0e, t01, a00, a11);
@@ -344,7 +405,8 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
 #pragma unroll
                     for (int c = 0; c < D; ++c) E0e[c] = e0eff(e0b, lf, s, 0, c);
                     if (ro) E0t = e0eff(e0b, lf, s, NK - 1, 0);
-                    double2 t01 = make_double2(0.0, 0.0), a00 = t01, a11 = t01;
+                    double2 t01 = make_double2(0.0, 0.0);
+                    double a00 = 0.0, a11 = 0.0;
                     if (s == 2) {
 #pragma unroll
                         for (int d3 = 0; d3 < N; ++d3) fibre(Y[d3], 2, d3, l1, ro, E0e, t01, a00, a11);
@@ -374,30 +436,38 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
             }
         }
     }
+    __syncthreads();  // every warp (incl. the store warp's last bulk wait) is done
     if constexpr (RO) {
-        // fixed-order CTA reduction of the per-thread accumulators (producer threads contribute 0)
-        __syncthreads();
+        // fixed-order CTA reduction of the per-thread accumulators (the producer warps contribute 0)
 #pragma unroll
         for (int s = 0; s < S; ++s)
             if (a.rho[s] != nullptr) {
                 double2 tt[N];
-                if (tid < 128) {
-                    const double2 r00 = accS[(s * 3 + 0) * 128 + tid], r11 = accS[(s * 3 + 1) * 128 + tid],
-                                  r01 = accS[(s * 3 + 2) * 128 + tid];
-                    tt[0] = r00, tt[1] = r01, tt[2] = make_double2(r01.x, -r01.y), tt[3] = r11;
+                if (warp < kF4Consumers) {
+                    double p[4];
+                    tmem_wait_st();
+                    tmem_ld8(tacc + 8 * s, p);
+                    tt[0] = make_double2(p[0], 0.0), tt[1] = make_double2(p[2], p[3]);
+                    tt[2] = make_double2(p[2], -p[3]), tt[3] = make_double2(p[1], 0.0);
                 } else {
                     tt[0] = tt[1] = tt[2] = tt[3] = make_double2(0.0, 0.0);
                 }
                 reduce_finalize<N, kF4Block>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
                                              a.rho_accumulate != 0);
             }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (warp == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(32 * kF4Groups) : "memory");
+        }
     }
 }
 
 // ---------------------------------------------------------------------------------- dispatch
 namespace {
 constexpr size_t fused4_dyn() {
-    return (size_t)(2 * kF4Stage + 2 * kF4E0B + 2 * 4 * 2 * 2 * 16 + 4 * 2 * 4 * 16 + 4 * 3 * 128) * 16;
+    return (size_t)(kF4NS * kF4Stage + kF4NS * kF4E0B + 2 * 4 * 2 * 2 * 16 + 4 * 2 * 4 * 16) * 16;
 }
 template <bool SYM, bool RO, int LT>
 cudaError_t fused4_t(const FusedArgs &a, int grid, cudaStream_t s) {

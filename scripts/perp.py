@@ -18,7 +18,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=3)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--final-only", action="store_true", help="readout of the last step only (no fused readout)")
+ap.add_argument("--so", default=None, help="time another build of libquapi.so (A/B)")
 args = ap.parse_args()
+if args.so:
+    Q.SO_PATH = args.so
 w = W.CONFIGS[args.cfg]
 L = w.L
 n = L + 14 * 3 * (args.reps + 1)
@@ -49,3 +52,5 @@ for p0 in sorted(res):
     tot += ms
     print(f"p0={p0:2d} {ms:.3f} ms  {byts / ms / 1e6:.0f} GB/s")
 print(f"mean {tot / len(res):.3f} ms per launch, {S * len(res) / tot * 1e3:.1f} steps/s")
+rho = plan.read_rho(work)
+print(f"checksum rho[-1] = {rho[-1].real.sum():.15f} {abs(rho[-1][0, 1]):.15e}")
