@@ -110,6 +110,52 @@ __device__ __forceinline__ void reduce_finalize(double2 (&acc)[N], double2 *part
     if (threadIdx.x == 0) *counter = 0u;
 }
 
+// Fixed-order grid reduction of NV complex values per thread in ONE pass (several readouts of one
+// launch together): shuffle tree per warp, warps in order into partials[blockIdx][NV], one counter;
+// the last CTA to finish sums the block rows in block order (b = t, t + BLOCK, ... per thread, then the
+// same trees) and calls put(v, total) for v < NV.  red: shared scratch of (BLOCK / 32) * NV entries.
+template <int NV, int BLOCK, class Put>
+__device__ __forceinline__ void grid_sum_multi(double2 (&v)[NV], double2 *red, double2 *partials, unsigned *counter, Put put) {
+    constexpr int W = BLOCK / 32;
+    __shared__ int is_last_m;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto tree = [&]() {  // v -> red[warp][n] (lane 0), fixed shuffle order
+#pragma unroll
+        for (int n = 0; n < NV; ++n) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                v[n].x += __shfl_xor_sync(0xffffffffu, v[n].x, o);
+                v[n].y += __shfl_xor_sync(0xffffffffu, v[n].y, o);
+            }
+            if (lane == 0) red[warp * NV + n] = v[n];
+        }
+        __syncthreads();
+    };
+    auto warps_sum = [&](int t) {
+        double2 s = red[t];
+        for (int w = 1; w < W; ++w) s = cadd(s, red[w * NV + t]);
+        return s;
+    };
+    __syncthreads();  // red may alias memory the caller used
+    tree();
+    if (threadIdx.x < NV) __stcg(&partials[(size_t)blockIdx.x * NV + threadIdx.x], warps_sum(threadIdx.x));
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last_m = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!is_last_m) return;
+    __threadfence();
+#pragma unroll
+    for (int n = 0; n < NV; ++n) v[n] = make_double2(0.0, 0.0);
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += BLOCK)
+#pragma unroll
+        for (int n = 0; n < NV; ++n) v[n] = cadd(v[n], __ldcg(&partials[(size_t)b * NV + n]));
+    __syncthreads();  // red: every thread has read its block sums above
+    tree();
+    if (threadIdx.x < NV) put(threadIdx.x, warps_sum(threadIdx.x));
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
 // Super-fibre index helpers.  A super-fibre holds the N^S entries of the S inner digits of one
 // outer fibre, entry e = sum_i d_i N^i.  During sub-step s a "fibre" is the N entries along inner
 // digit s; r enumerates the other S-1 inner digits (ascending, digit s skipped).

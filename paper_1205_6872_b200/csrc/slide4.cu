@@ -27,7 +27,7 @@
 //   x outer group-0 factor of the fibre                                   (E0, per round)
 // Readout: Re rho_00, Re rho_11 and rho_01 per step (rho_10 = conj rho_01 and a real diagonal: rho(t)
 // is Hermitian), per-thread shared-memory accumulators, fixed-order reduction at the end.
-#include "common.cuh"
+#include "tmem.cuh"
 
 namespace qp {
 
@@ -63,27 +63,6 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 __device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
 }
-// Tensor memory (TMEM) as per-thread accumulator storage: the readout sums of a consumer thread live in
-// its TMEM lane (32x32b shape: warp w reaches lanes 32 (w % 4) .. + 31), 8 x 32-bit columns per sub-step.
-__device__ __forceinline__ void tmem_ld8(unsigned ta, double (&v)[4]) {
-    unsigned r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(ta) : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
-}
-__device__ __forceinline__ void tmem_st8(unsigned ta, const double (&v)[4]) {
-    unsigned r[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) r[2 * i] = (unsigned)__double2loint(v[i]), r[2 * i + 1] = (unsigned)__double2hiint(v[i]);
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
-                 ::"r"(ta), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
 // 128-B swizzle of a stage offset in 16-B units (stage 1024-B aligned): chunk bits 0-2 ^= bits 3-5
 __device__ __forceinline__ int swz(int o, int on) { return on ? o ^ ((o >> 3) & 7) : o; }
 
@@ -121,52 +100,6 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const SmallLayout lay{N, D, 0};
 
-    // ---- CTA-wide setup: KU (tile independent), beta, barriers
-    for (int i = tid; i < S * NK * 4 * N * N; i += kF4Block) {
-        const int last = i % N, nw = (i / N) % N, vd = (i / (N * N)) % 4, kap = (i / (N * N * 4)) % NK, s = i / (N * N * 4 * NK);
-        // lane-varying inner digit of sub-step s: s = 0 -> d1, 1 -> d0, 2 -> d3, 3 -> d2
-        const int iv = s == 0 ? 1 : (s == 1 ? 0 : (s == 2 ? 3 : 2));
-        const int c = class_of(M, LAT, nw / M, nw % M);
-        double2 e = a.small[lay.kp(kap) + nw * N + last];
-        if (c > 0) e = cmul(e, a.inner[((((size_t)s * S + iv) * 2 + kap) * D + (c - 1)) * N + vd]);
-        sKU[i] = e;
-    }
-    for (int i = tid; i < S * 2 * D * N; i += kF4Block) {
-        const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
-        (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
-    }
-    if (tid == 0) {
-        for (int b = 0; b < kF4NS; ++b) {
-            mbar_init(&bar_full[b], 1);
-            mbar_init(&bar_done[b], 4);
-            mbar_init(&bar_empty[b], 1);
-        }
-        for (int b = 0; b < 2; ++b) mbar_init(&bar_lf[b], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    // readout accumulators in TMEM: 32 columns per consumer thread (warps w, w + 4 share lanes: columns
-    // 32 (w / 4) .. + 31), allocated by warp 0, zeroed by their threads
-    if constexpr (RO) {
-        if (warp == 0) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
-                         "n"(32 * kF4Groups) : "memory");
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-    const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 32u * (unsigned)(warp >> 2);
-    if constexpr (RO)
-        if (warp < kF4Consumers) {
-            const double z[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int s = 0; s < S; ++s) tmem_st8(tacc + 8 * s, z);
-            tmem_wait_st();
-        }
-
     const int per = a.n_tiles / (int)gridDim.x, rem = a.n_tiles % (int)gridDim.x;
     const int t_begin = (int)blockIdx.x * per + min((int)blockIdx.x, rem);
     const int t_end = t_begin + per + ((int)blockIdx.x < rem ? 1 : 0);
@@ -176,6 +109,60 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     // builds a tile's LF table (buffer tile & 1) only then, so every round of the tile two back is done
     // when NS <= rounds + 1
     const int NS = min(kF4NS, rounds + 1);
+    constexpr int kLoadWarp = kF4Consumers + 1;
+    auto issue_load = [&](int r) {  // lane 0 of the load warp: round r into stage r % NS
+        const int tau = t_begin + r / rounds, rd = r % rounds, b = r % NS;
+        fence_proxy_async();
+        mbar_expect_tx(&bar_full[b], kF4Stage * 16 + kF4E0B * 16);
+        const Coords k = f4_coords(a, (long long)tau * a.T + (long long)rd * kF4F, 0);
+        tma_load_5dc(stage + b * kF4Stage, &a.tmap, &bar_full[b], k.c[0], k.c[1], k.c[2], k.c[3], k.c[4]);
+        bulk_g2s(sE0 + b * kF4E0B, a.E0r + (size_t)rd * kF4E0B, kF4E0B * 16, &bar_full[b]);
+    };
+
+    // ---- CTA-wide setup.  The load warp initialises the barriers and puts the first NS rounds in
+    // flight while the other warps build KU (tile independent) and beta; warp 0 allocates TMEM.
+    if (warp == kLoadWarp) {
+        if (lane == 0) {
+            for (int b = 0; b < kF4NS; ++b) {
+                mbar_init(&bar_full[b], 1);
+                mbar_init(&bar_done[b], 4);
+                mbar_init(&bar_empty[b], 1);
+            }
+            for (int b = 0; b < 2; ++b) mbar_init(&bar_lf[b], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (int r = 0; r < min(R, NS); ++r) issue_load(r);
+        }
+    } else {
+        constexpr int kSetup = kF4Block - 32;
+        for (int i = tid; i < S * NK * 4 * N * N; i += kSetup) {
+            const int last = i % N, nw = (i / N) % N, vd = (i / (N * N)) % 4, kap = (i / (N * N * 4)) % NK, s = i / (N * N * 4 * NK);
+            // lane-varying inner digit of sub-step s: s = 0 -> d1, 1 -> d0, 2 -> d3, 3 -> d2
+            const int iv = s == 0 ? 1 : (s == 1 ? 0 : (s == 2 ? 3 : 2));
+            const int c = class_of(M, LAT, nw / M, nw % M);
+            double2 e = a.small[lay.kp(kap) + nw * N + last];
+            if (c > 0) e = cmul(e, a.inner[((((size_t)s * S + iv) * 2 + kap) * D + (c - 1)) * N + vd]);
+            sKU[i] = e;
+        }
+        for (int i = tid; i < S * 2 * D * N; i += kSetup) {
+            const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
+            (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
+        }
+    }
+    // readout accumulators in TMEM: 32 columns per consumer thread (warps w, w + 4 share lanes: columns
+    // 32 (w / 4) .. + 31), allocated by warp 0, zeroed by their threads
+    if constexpr (RO)
+        if (warp == 0) tmem_alloc(&tmem_base, 32 * kF4Groups);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 32u * (unsigned)(warp >> 2);
+    if constexpr (RO)
+        if (warp < kF4Consumers) {
+            const double z[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int s = 0; s < S; ++s) tmem_st_d4(tacc + 8 * s, z);
+            tmem_wait_st();
+        }
 
     if (warp == kF4Consumers) {
         // =========================================================== store warp
@@ -200,8 +187,11 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
         // round r into stage r % NS once the stage's previous round (r - NS) has been stored and read
         for (int r = 0; r < R; ++r) {
             const int tau = t_begin + r / rounds, rd = r % rounds, b = r % NS;
-            if (r >= NS) mbar_wait(&bar_empty[b], ((r / NS) - 1) & 1);
-            if (rd == 0) {
+            if (r >= NS) {  // (rounds < NS went out during the setup)
+                mbar_wait(&bar_empty[b], ((r / NS) - 1) & 1);
+                if (lane == 0) issue_load(r);
+            }
+            if (rd == 0) {  // (after the round's TMA load is in flight: consumers wait for both)
                 // this tile's LF[s][kap][c][q] = (outer groups >= 1 x shard digits) x inner factors of the
                 // lane-fixed digits of lane mapping q (buffer tau & 1: every round of tile tau - 2 has been
                 // stored, as NS <= rounds + 1)
@@ -225,13 +215,6 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bar_lf[lb]);
-            }
-            if (lane == 0) {
-                fence_proxy_async();
-                mbar_expect_tx(&bar_full[b], kF4Stage * 16 + kF4E0B * 16);
-                const Coords k = f4_coords(a, (long long)tau * a.T + (long long)rd * kF4F, 0);
-                tma_load_5dc(stage + b * kF4Stage, &a.tmap, &bar_full[b], k.c[0], k.c[1], k.c[2], k.c[3], k.c[4]);
-                bulk_g2s(sE0 + b * kF4E0B, a.E0r + (size_t)rd * kF4E0B, kF4E0B * 16, &bar_full[b]);
             }
             __syncwarp();
         }
@@ -328,12 +311,12 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
         auto flush = [&](int s, double a00, double a11, double2 t01, const double2 &E0t) {
             double p[4];
             tmem_wait_st();  // this thread's previous store to the columns (a sub-step ago) has landed
-            tmem_ld8(tacc + 8 * s, p);
+            tmem_ld_d4(tacc + 8 * s, p);
             p[0] += a00;
             p[1] += a11;
             p[2] = fma(E0t.x, t01.x, fma(-E0t.y, t01.y, p[2]));
             p[3] = fma(E0t.x, t01.y, fma(E0t.y, t01.x, p[3]));
-            tmem_st8(tacc + 8 * s, p);
+            tmem_st_d4(tacc + 8 * s, p);
         };
 
         int cur = -1, last_t = 0;
@@ -438,28 +421,30 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     }
     __syncthreads();  // every warp (incl. the store warp's last bulk wait) is done
     if constexpr (RO) {
-        // fixed-order CTA reduction of the per-thread accumulators (the producer warps contribute 0)
+        // one fixed-order grid reduction of the four steps' per-thread accumulators (the producer warps
+        // contribute 0); the stages are free now and hold the scratch
+        double2 tt[S * N];
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-            if (a.rho[s] != nullptr) {
-                double2 tt[N];
-                if (warp < kF4Consumers) {
-                    double p[4];
-                    tmem_wait_st();
-                    tmem_ld8(tacc + 8 * s, p);
-                    tt[0] = make_double2(p[0], 0.0), tt[1] = make_double2(p[2], p[3]);
-                    tt[2] = make_double2(p[2], -p[3]), tt[3] = make_double2(p[1], 0.0);
-                } else {
-                    tt[0] = tt[1] = tt[2] = tt[3] = make_double2(0.0, 0.0);
-                }
-                reduce_finalize<N, kF4Block>(tt, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
-                                             a.rho_accumulate != 0);
+        for (int s = 0; s < S; ++s) {
+            if (warp < kF4Consumers) {
+                double p[4];
+                tmem_wait_st();
+                tmem_ld_d4(tacc + 8 * s, p);
+                tt[s * N + 0] = make_double2(p[0], 0.0), tt[s * N + 1] = make_double2(p[2], p[3]);
+                tt[s * N + 2] = make_double2(p[2], -p[3]), tt[s * N + 3] = make_double2(p[1], 0.0);
+            } else {
+                tt[s * N + 0] = tt[s * N + 1] = tt[s * N + 2] = tt[s * N + 3] = make_double2(0.0, 0.0);
             }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        }
+        grid_sum_multi<S * N, kF4Block>(tt, stage, a.partials, a.counter, [&](int v, double2 x) {
+            double2 *r = a.rho[v / N];
+            if (r != nullptr) r[v % N] = a.rho_accumulate ? cadd(r[v % N], x) : x;
+        });
+        tmem_fence_before();
         __syncthreads();
         if (warp == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(32 * kF4Groups) : "memory");
+            tmem_fence_after();
+            tmem_dealloc(tmem_base, 32 * kF4Groups);
         }
     }
 }
