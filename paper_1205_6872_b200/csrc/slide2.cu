@@ -11,7 +11,7 @@
 //   sub-step 0   : thread (w, lane) takes the fibre along d0 with d1 = w -- the inner
 //                  combination is warp-uniform; last = the outer slot p0-1;
 //   sub-step 1   : thread (w, lane) takes the fibre along d1 with d0 = w; last = d0 = w.
-// Class factors per fibre: E0 (outer group 0, per fibre) x Ehi (outer groups >= 1, per tile) x the
+// Class factors per fibre: E0 (outer group 0, per fibre; copied into shared memory with the unit) x Ehi (outer groups >= 1, per tile) x the
 // inner factor of the other inner digit; K' from a CTA-wide table.  Readout accumulators in
 // registers, fixed-order CTA reduction at the end (deterministic).
 #include "common.cuh"
@@ -30,6 +30,8 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
     const SmallLayout lay{N, D, 0};
     extern __shared__ __align__(16) double2 smem2[];
     double2(*stage)[NS][kF2F] = reinterpret_cast<double2(*)[NS][kF2F]>(smem2);  // [2][81][32]
+    // the unit's outer group-0 factors E0[s][kap][d][fibre], copied with the unit: [2][S][2][D][32]
+    double2(*sE0u)[S][2][D][kF2F] = reinterpret_cast<double2(*)[S][2][D][kF2F]>(smem2 + 2 * NS * kF2F);
     __shared__ double2 sK[2][N][N];
     __shared__ double2 sIn[S][2][D][N];     // inner factor of the other inner digit: [s][kap][d][value]
     // per tile (double buffered by tile parity: written while other warps may still read the previous
@@ -71,7 +73,13 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
     };
     // cp.async the unit's entries into stage[buf]: thread (w, lane) copies rows e = w + 9 i of fibre `lane`
     auto issue = [&](long long u, int buf) {
-        const int tau = (int)(u / CH), t = (int)(u % CH) * kF2F + lane;
+        const int tau = (int)(u / CH), t0 = (int)(u % CH) * kF2F, t = t0 + lane;
+        // E0[s][kap][d][fibre t] = Etab[s][kap][group 0][d][t]: rows of kF2F consecutive entries
+        for (int i = tid; i < S * 2 * D * kF2F; i += kF2Block) {
+            const int f = i % kF2F, row = i / kF2F;  // row = (s * 2 + kap) * D + d
+            if (t0 + f < a.T)
+                cp_async16(&(&sE0u[buf][0][0][0][0])[i], a.Etab + ((size_t)(row / D) * a.G * D + row % D) * a.X + t0 + f);
+        }
         if (t < a.T) {
             const long long base = tile_base(tau) + __ldg(&a.lofs[t]).x;
 #pragma unroll
@@ -115,25 +123,32 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
         for (int s = 0; s < S; ++s) {
             if (valid) {
                 const int w = warp;  // s = 0: d1 = w, fibre along d0;  s = 1: d0 = w, fibre along d1
-                double2 xf[N];
                 auto slot = [&](int v) -> double2 & { return stage[buf][s == 0 ? v + N * w : w + N * v][lane]; };
-#pragma unroll
-                for (int v = 0; v < N; ++v) xf[v] = slot(v);
                 const int last = s == 0 ? (lo.y >= 0 ? lo.y : last_t) : w;
-                // three independent partial chains per sum (latency: the CTA holds few warps)
-                const double2 S0 = cadd(cadd(cadd(xf[0], xf[1]), cadd(xf[2], xf[3])), cadd(cadd(xf[4], xf[5]), cadd(cadd(xf[6], xf[7]), xf[8])));
+                // the plain sum and every class moment in one pass over the fibre's old values (one entry
+                // live at a time: the register budget of 2 CTAs per SM holds no 9-entry fibre next to the
+                // readout accumulators); D + NUC independent chains
+                double2 S0 = make_double2(0.0, 0.0), mp[D], mr[RO ? D : 1];
+#pragma unroll
+                for (int d = 0; d < D; ++d) mp[d] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int d = 0; d < (RO ? D : 1); ++d) mr[d] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int v = 0; v < N; ++v) {
+                    const double2 x = slot(v);
+                    S0 = cadd(S0, x);
+#pragma unroll
+                    for (int d = 0; d < D; ++d) mp[d] = cfma(bt.b[s][0][d][v], x, mp[d]);
+                    if constexpr (RO)
+#pragma unroll
+                        for (int d = 0; d < D; ++d)
+                            if (upper_class(d)) mr[d] = cfma(bt.b[s][1][d][v], x, mr[d]);
+                }
                 // class moment of class d, weights kap (0: propagation, 1: readout), times its class
                 // factor E0 (outer group 0, this fibre) x EI (tile groups x inner digit w)
                 auto moment = [&](int kap, int d) {
-                    double2 p[3];
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        p[j] = cmul(bt.b[s][kap][d][j], xf[j]);
-                        p[j] = cfma(bt.b[s][kap][d][j + 3], xf[j + 3], p[j]);
-                        p[j] = cfma(bt.b[s][kap][d][j + 6], xf[j + 6], p[j]);
-                    }
-                    const double2 mm = cadd(cadd(p[0], p[1]), p[2]);
-                    return cmul(cmul(__ldg(&a.Etab[(((size_t)s * 2 + kap) * a.G * D + d) * a.X + t]), sEI[tp][s][kap][d][w]), mm);
+                    const double2 mm = kap == 0 ? mp[d] : mr[RO ? d : 0];
+                    return cmul(cmul(sE0u[buf][s][kap][d][lane], sEI[tp][s][kap][d][w]), mm);
                 };
                 // readout first (upper triangle only: rho_ba = conj rho_ab), one class moment live at a time
                 if constexpr (RO) {
@@ -163,8 +178,8 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
                             if (upper_class(d)) accM1[RO ? d : 0] = cadd(accM1[RO ? d : 0], moment(1, d));
                     }
                 }
-                // propagate: the outputs of each class go straight out (xf stays intact): sub-step 0 to
-                // the stage, sub-step 1 to HBM (entry d0 = w, d1 = nw of this fibre)
+                // propagate: the outputs of each class go straight out: sub-step 0 back into the fibre's
+                // stage slots (all read above), sub-step 1 to HBM (entry d0 = w, d1 = nw of this fibre)
                 double2 *out = a.A + tbase + lo.x + (long long)w * a.pw_in[0];
                 auto put = [&](int nw, double2 v) {
                     if (s == 0) slot(nw) = v;
@@ -208,18 +223,19 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
 }
 
 namespace {
-constexpr size_t fused2s_dyn() { return (size_t)2 * kF2N * kF2N * kF2F * 16; }
+template <bool LAT>
+constexpr size_t fused2s_dyn() { return (size_t)2 * (kF2N * kF2N + 2 * 2 * n_classes(3, LAT)) * kF2F * 16; }
 template <bool LAT, bool RO>
 cudaError_t fused2s_t(const FusedArgs &a, const Beta2s &b, int grid, cudaStream_t s) {
-    cudaFuncSetAttribute(k_fused2s<LAT, RO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused2s_dyn());
-    k_fused2s<LAT, RO><<<grid, kF2Block, fused2s_dyn(), s>>>(a, b);
+    cudaFuncSetAttribute(k_fused2s<LAT, RO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused2s_dyn<LAT>());
+    k_fused2s<LAT, RO><<<grid, kF2Block, fused2s_dyn<LAT>(), s>>>(a, b);
     return cudaGetLastError();
 }
 template <bool LAT, bool RO>
 int fused2s_occ_t() {
     int o = 0;
-    cudaFuncSetAttribute(k_fused2s<LAT, RO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused2s_dyn());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused2s<LAT, RO>, kF2Block, fused2s_dyn());
+    cudaFuncSetAttribute(k_fused2s<LAT, RO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused2s_dyn<LAT>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused2s<LAT, RO>, kF2Block, fused2s_dyn<LAT>());
     return o;
 }
 }  // namespace
