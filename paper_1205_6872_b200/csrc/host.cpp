@@ -782,6 +782,9 @@ static qp_status set_tma(const qp_plan &P, const qp_plan::LaunchSet &ls, qp::Fus
         a.f4_layout = qp::fused4_layout_type(a.f4_lpos, a.f4_spos, a.f4_q1swap, a.f4_q2swap, a.f4_swz);
         for (int m = 0; m < 2; ++m) a.f4_cdimA[m] = ls.f4map[m].cdimA, a.f4_cdimB[m] = ls.f4map[m].cdimB;
         a.tma_nA = ls.f4_nA;
+        a.tma_nA_log2 = -1;
+        for (int b = 0; b < 62; ++b)
+            if ((1LL << b) == a.tma_nA) a.tma_nA_log2 = b;
         a.tma_c0m = ls.f4_c0m;
         a.E0r = (const double2 *)(w + ls.off_E0r);
         return QP_OK;
@@ -792,6 +795,9 @@ static qp_status set_tma(const qp_plan &P, const qp_plan::LaunchSet &ls, qp::Fus
         // TMA box coordinates of unit G (first outer fibre): c0 = tma_c0m (G mod tma_nA), c1 = G / tma_nA
         // (view A: run A as doubles; view B: rows of two fibres; views C, D: one fibre per row group)
         a.tma_nA = ls.tma_a > 0 ? ipow(P.N, ls.tma_a) : (ls.tma_a == 0 ? 2 : 1);
+        a.tma_nA_log2 = -1;
+        for (int b = 0; b < 62; ++b)
+            if ((1LL << b) == a.tma_nA) a.tma_nA_log2 = b;
         a.tma_c0m = ls.tma_a > 0 ? 2 : 0;
         a.tma_view = ls.tma_a > 0 ? 0 : (ls.tma_a == 0 ? 1 : (ls.tma_a == -2 ? 2 : 3));
         a.E0r = (const double2 *)(w + ls.off_E0r);

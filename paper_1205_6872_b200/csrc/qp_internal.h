@@ -69,6 +69,7 @@ struct FusedArgs {
     int tma_view;            // k_fused3 stage view: 0 = A, 1 = B, 2 = C, 3 = D (slide3.cu, host.cpp encode_f3_tmap)
     long long tma_nA;        // outer fibres in run A (slots 0 .. p0-1) of the TMA view (view B: 2, views C/D: 1)
     int tma_c0m;             // TMA coordinate 0 = tma_c0m x (G mod tma_nA) doubles, coordinate 1 = G / tma_nA
+    int tma_nA_log2;         // log2(tma_nA) when tma_nA is a power of two (always for M = 2), else -1
     alignas(64) CUtensorMap tmap;   // k_fused3 / k_fused4 load map
     alignas(64) CUtensorMap tmapS;  // k_fused4 store map
     // k_fused4 stage layouts (slide4.cu, host.cpp f4_layout): smem bit position (16-B units) of each

@@ -188,7 +188,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_fused3(const __grid_constant__ 
         const long long G = (long long)tau * a.T + (long long)rw * FS;
         fence_proxy_async();
         mbar_expect_tx(sFull, FS * 64 * 16 + E0B * 16);
-        tma_load_5d(stg, &a.tmap, sFull, (int)(a.tma_c0m * (G % a.tma_nA)), (int)(G / a.tma_nA));
+        const int sh = a.tma_nA_log2;  // power-of-two run length (M = 2): shifts, no 64-bit division
+        const long long q = sh >= 0 ? (G >> sh) : G / a.tma_nA, rm = sh >= 0 ? (G & (a.tma_nA - 1)) : G - q * a.tma_nA;
+        tma_load_5d(stg, &a.tmap, sFull, (int)(a.tma_c0m * rm), (int)q);
         bulk_g2s(sE0w + buf * E0B, a.E0r + (size_t)rw * E0B, E0B * 16, sFull);
     };
     unsigned phase = 0, cur = 0;

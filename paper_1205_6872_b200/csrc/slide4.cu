@@ -74,10 +74,12 @@ __device__ __forceinline__ Coords f4_coords(const FusedArgs &a, long long G, int
     Coords k{{0, 0, 0, 0, 0}};
     const int dA = a.f4_cdimA[which], dB = a.f4_cdimB[which];
     const long long nA = a.tma_nA;
+    const int sh = a.tma_nA_log2;  // power-of-two run length (M = 2): shifts, no 64-bit division
+    const long long q = sh >= 0 ? (G >> sh) : G / nA, rm = sh >= 0 ? (G & (nA - 1)) : G - q * nA;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-        if (i == dA) k.c[i] = (int)(a.tma_c0m * (G % nA));
-        if (i == dB) k.c[i] = (int)(G / nA);
+        if (i == dA) k.c[i] = (int)(a.tma_c0m * rm);
+        if (i == dB) k.c[i] = (int)q;
     }
     return k;
 }
