@@ -97,6 +97,7 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     double2 *const sLF = sE0 + kF4NS * kF4E0B;                       // [2][S][NK][D][16]
     double2 *const sKU = sLF + 2 * S * 2 * D * 16;                   // [S][NK][4 vd][N nw][N last]
     __shared__ double2 sBeta[S][2][D][N];
+    __shared__ double2 sQ[S * 2 * D * 16];  // [S][NK][D][16] (tile-independent part of LF)
     __shared__ unsigned tmem_base;
     __shared__ __align__(8) unsigned long long bar_full[kF4NS], bar_done[kF4NS], bar_empty[kF4NS], bar_lf[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -112,8 +113,7 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     // when NS <= rounds + 1
     const int NS = min(kF4NS, rounds + 1);
     constexpr int kLoadWarp = kF4Consumers + 1;
-    auto issue_load = [&](int r) {  // lane 0 of the load warp: round r into stage r % NS
-        const int tau = t_begin + r / rounds, rd = r % rounds, b = r % NS;
+    auto issue_load = [&](int b, int tau, int rd) {  // lane 0 of the load warp: round (tau, rd) into stage b
         fence_proxy_async();
         mbar_expect_tx(&bar_full[b], kF4Stage * 16 + kF4E0B * 16);
         const Coords k = f4_coords(a, (long long)tau * a.T + (long long)rd * kF4F, 0);
@@ -132,7 +132,7 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
             }
             for (int b = 0; b < 2; ++b) mbar_init(&bar_lf[b], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            for (int r = 0; r < min(R, NS); ++r) issue_load(r);
+            for (int r = 0; r < min(R, NS); ++r) issue_load(r, t_begin + r / rounds, r % rounds);
         }
     } else {
         constexpr int kSetup = kF4Block - 32;
@@ -148,6 +148,23 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
         for (int i = tid; i < S * 2 * D * N; i += kSetup) {
             const int s_ = i / (2 * D * N), kap = (i / (D * N)) % 2, r_ = i % (D * N);
             (&sBeta[0][0][0][0])[i] = a.small[lay.beta(a.var[s_], kap) + r_];
+        }
+        // sQ[s][kap][c][q] = shard-digit factor x inner factors of the two lane-fixed digits of lane
+        // mapping q (tile independent; a tile's LF multiplies in its outer groups >= 1)
+        for (int i = tid; i < S * NK * D * 16; i += kSetup) {
+            const int q = i % 16, c = (i / 16) % D, kap = (i / (16 * D)) % NK, s = i / (16 * D * NK);
+            int da, db, ia, ib;  // the two lane-fixed digits (ia, ib) and their values for lane q
+            if (s < 2) {
+                ia = 2, ib = 3;
+                if (a.f4_q1swap) db = q & 3, da = q >> 2; else da = q & 3, db = q >> 2;
+            } else {
+                ia = 0, ib = 1;
+                if (a.f4_q2swap) db = q & 3, da = q >> 2; else da = q & 3, db = q >> 2;
+            }
+            double2 e = a.fixfac[s][kap][c];
+            e = cmul(e, a.inner[((((size_t)s * S + ia) * 2 + kap) * D + c) * N + da]);
+            e = cmul(e, a.inner[((((size_t)s * S + ib) * 2 + kap) * D + c) * N + db]);
+            sQ[i] = e;
         }
     }
     // readout accumulators in TMEM: 32 columns per consumer thread (warps w, w + 4 share lanes: columns
@@ -169,56 +186,57 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     if (warp == kF4Consumers) {
         // =========================================================== store warp
         // round j: wait for its group (done), store the stage; once the store of round j - 1 has read
-        // its stage (bulk wait_group.read 1: the store of j may still be reading), release that stage
+        // its stage (bulk wait_group.read 1: the store of j may still be reading), release that stage.
+        // Stage index / phase / tile position advance incrementally (no divisions in the chain).
         if (lane == 0) {
+            int b = 0, ph = 0, bp = 0, tau = t_begin, rd = 0;
             for (int j = 0; j < R; ++j) {
-                const int b = j % NS, tau = t_begin + j / rounds, rd = j % rounds;
-                mbar_wait(&bar_done[b], (j / NS) & 1);
+                mbar_wait(&bar_done[b], ph);
                 const Coords k = f4_coords(a, (long long)tau * a.T + (long long)rd * kF4F, 1);
                 tma_store_5dc(&a.tmapS, stage + b * kF4Stage, k.c[0], k.c[1], k.c[2], k.c[3], k.c[4]);
                 bulk_commit();
                 if (j >= 1) {
                     bulk_wait_read1();
-                    mbar_arrive(&bar_empty[(j - 1) % NS]);
+                    mbar_arrive(&bar_empty[bp]);
                 }
+                bp = b;
+                if (++b == NS) b = 0, ph ^= 1;
+                if (++rd == rounds) rd = 0, ++tau;
             }
             bulk_wait0();
         }
     } else if (warp == kF4Consumers + 1) {
         // =========================================================== load warp
-        // round r into stage r % NS once the stage's previous round (r - NS) has been stored and read
+        // round r into stage r % NS once the stage's previous round (r - NS) has been stored and read.
+        // A tile's LF = Ehi(tile)[s][kap][c] x sQ[s][kap][c][q]: lanes 0..15 form the 16 outer-group
+        // products (independent loads), every lane then 8 entries from the CTA's sQ table.
+        int b = 0, ph = 1, tau = t_begin, rd = 0;
         for (int r = 0; r < R; ++r) {
-            const int tau = t_begin + r / rounds, rd = r % rounds, b = r % NS;
             if (r >= NS) {  // (rounds < NS went out during the setup)
-                mbar_wait(&bar_empty[b], ((r / NS) - 1) & 1);
-                if (lane == 0) issue_load(r);
+                mbar_wait(&bar_empty[b], ph);
+                if (lane == 0) issue_load(b, tau, rd);
             }
             if (rd == 0) {  // (after the round's TMA load is in flight: consumers wait for both)
-                // this tile's LF[s][kap][c][q] = (outer groups >= 1 x shard digits) x inner factors of the
-                // lane-fixed digits of lane mapping q (buffer tau & 1: every round of tile tau - 2 has been
-                // stored, as NS <= rounds + 1)
+                // this tile's LF (buffer tau & 1: every round of tile tau - 2 has been stored, as NS <= rounds + 1)
                 const int lb = (tau - t_begin) & 1;
-                for (int i = lane; i < S * NK * D * 16; i += 32) {
-                    const int q = i % 16, c = (i / 16) % D, kap = (i / (16 * D)) % NK, s = i / (16 * D * NK);
-                    double2 e = a.fixfac[s][kap][c];
+                double2 e = make_double2(1.0, 0.0);
+                if (lane < S * NK * D) {
+                    const int c = lane % D, kap = (lane / D) % NK, s = lane / (D * NK);
                     for (int g = 1; g < a.G; ++g)
                         e = cmul(e, __ldg(&a.Etab[((((size_t)s * 2 + kap) * a.G + g) * D + c) * a.X + (tau / a.gdiv[g]) % a.gmod[g]]));
-                    int da, db, ia, ib;  // the two lane-fixed digits (ia, ib) and their values for lane q
-                    if (s < 2) {
-                        ia = 2, ib = 3;
-                        if (a.f4_q1swap) db = q & 3, da = q >> 2; else da = q & 3, db = q >> 2;
-                    } else {
-                        ia = 0, ib = 1;
-                        if (a.f4_q2swap) db = q & 3, da = q >> 2; else da = q & 3, db = q >> 2;
-                    }
-                    e = cmul(e, __ldg(&a.inner[((((size_t)s * S + ia) * 2 + kap) * D + c) * N + da]));
-                    e = cmul(e, __ldg(&a.inner[((((size_t)s * S + ib) * 2 + kap) * D + c) * N + db]));
-                    sLF[(size_t)lb * S * 2 * D * 16 + i] = e;
+                }
+#pragma unroll
+                for (int i0 = 0; i0 < S * NK * D * 16; i0 += 32) {
+                    const int i = i0 + lane, src = i / 16;
+                    const double2 eh = make_double2(__shfl_sync(0xffffffffu, e.x, src), __shfl_sync(0xffffffffu, e.y, src));
+                    sLF[(size_t)lb * S * 2 * D * 16 + i] = cmul(eh, sQ[i]);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bar_lf[lb]);
             }
             __syncwarp();
+            if (++b == NS) b = 0, ph ^= 1;
+            if (++rd == rounds) rd = 0, ++tau;
         }
     } else {
         // =========================================================== consumer warps
