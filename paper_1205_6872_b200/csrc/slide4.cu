@@ -341,8 +341,9 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
 
         int cur = -1, last_t = 0;
         const double2 *lf = sLF;
+        // round r = grp, grp + kF4Groups, ...: stage b, its phase ph and tile tau advance incrementally
+        int b = grp % NS, ph = (grp / NS) & 1, tau = t_begin + grp / rounds, rd = grp % rounds;
         for (int r = grp; r < R; r += kF4Groups) {
-            const int tau = t_begin + r / rounds, b = r % NS;
             if (tau != cur) {  // a new tile: its LF table (buffer tau & 1) and sub-step 0's 'last' digit
                 cur = tau;
                 const int lb = (tau - t_begin) & 1;
@@ -351,7 +352,7 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
                 last_t = a.fixed_last >= 0 ? a.fixed_last : (a.last_div > 0 ? (tau / a.last_div) % N : 0);
             }
             {
-                mbar_wait(&bar_full[b], (r / NS) & 1);
+                mbar_wait(&bar_full[b], ph);
                 double2 *const st = stage + b * kF4Stage;
                 const double2 *const e0b = sE0 + b * kF4E0B;
                 const int lastf = reinterpret_cast<const int2 *>(e0b + 4 * 2 * 2 * kF4F)[f].y;
@@ -437,6 +438,8 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bar_done[b]);
             }
+            if ((b += kF4Groups) >= NS) b -= NS, ph ^= 1;
+            if ((rd += kF4Groups) >= rounds) rd -= rounds, ++tau;
         }
     }
     __syncthreads();  // every warp (incl. the store warp's last bulk wait) is done
