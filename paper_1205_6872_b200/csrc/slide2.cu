@@ -71,9 +71,10 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
         for (int g = 1; g < a.G; ++g) b += __ldg(&a.goff[(size_t)g * a.X + (tau / a.gdiv[g]) % a.gmod[g]]);
         return b;
     };
-    // cp.async the unit's entries into stage[buf]: thread (w, lane) copies rows e = w + 9 i of fibre `lane`
-    auto issue = [&](long long u, int buf) {
-        const int tau = (int)(u / CH), t0 = (int)(u % CH) * kF2F, t = t0 + lane;
+    // cp.async the entries of unit (tau, chunk ch) into stage[buf]: thread (w, lane) copies rows
+    // e = w + 9 i of fibre `lane`; tbase = the tile's base offset, lofs_t = lofs[t] of the thread's fibre
+    auto issue = [&](int tau, int ch, int buf, long long tbase_u, int lofs_x) {
+        const int t0 = ch * kF2F, t = t0 + lane;
         // E0[s][kap][d][fibre t] = Etab[s][kap][group 0][d][t]: rows of kF2F consecutive entries
         for (int i = tid; i < S * 2 * D * kF2F; i += kF2Block) {
             const int f = i % kF2F, row = i / kF2F;  // row = (s * 2 + kap) * D + d
@@ -81,7 +82,7 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
                 cp_async16(&(&sE0u[buf][0][0][0][0])[i], a.Etab + ((size_t)(row / D) * a.G * D + row % D) * a.X + t0 + f);
         }
         if (t < a.T) {
-            const long long base = tile_base(tau) + __ldg(&a.lofs[t]).x;
+            const long long base = tbase_u + lofs_x;
 #pragma unroll
             for (int i = 0; i < N; ++i) {
                 const int e = warp + N * i, d0 = e % N, d1 = e / N;
@@ -90,8 +91,13 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
         }
         cp_async_commit();
     };
+    // unit u = tau * CH + ch: (tau, ch) of this unit and of the next advance incrementally; the issuing
+    // threads cache the base of the tile they last issued for and the next unit's lofs entry
+    int tau = (int)(u_begin / CH), ch = (int)(u_begin % CH);
+    int itau = tau;
+    long long ibase = tile_base(tau);
     __syncthreads();
-    if (u_begin < u_end) issue(u_begin, 0);
+    if (u_begin < u_end) issue(tau, ch, 0, ibase, ch * kF2F + lane < a.T ? __ldg(&a.lofs[ch * kF2F + lane]).x : 0);
     int cur_tile = -1, last_t = 0;
     long long tbase = 0;
     // Per unit: barrier A (its copies landed; every warp is done with the previous unit) -> copies of
@@ -99,8 +105,10 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
     // (stage -> HBM: each thread stores the fibre it computed).
     for (long long u = u_begin; u < u_end; ++u) {
         const int buf = (int)((u - u_begin) & 1);
-        const int tau = (int)(u / CH), t = (int)(u % CH) * kF2F + lane, tp = tau & 1;
+        const int t = ch * kF2F + lane, tp = tau & 1;
         const bool valid = t < a.T;
+        const int ntau = ch + 1 == CH ? tau + 1 : tau, nch = ch + 1 == CH ? 0 : ch + 1, nt = nch * kF2F + lane;
+        const int nlofs = (u + 1 < u_end && nt < a.T) ? __ldg(&a.lofs[nt]).x : 0;  // in flight across the barrier
         if (tau != cur_tile) {  // tile constants into the parity-tau buffer (readers of tau-1 use the other)
             if (tid < S * 2 * D * N) {
                 const int s = tid / (2 * D * N), kap = (tid / (D * N)) % 2, d = (tid / N) % D, v = tid % N;
@@ -117,7 +125,10 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
         const int2 lo = valid ? __ldg(&a.lofs[t]) : make_int2(0, 0);  // in flight across the barrier
         cp_async_wait<0>();  // this unit's copies (every thread's) have landed ...
         __syncthreads();     // A: ... and are visible, tile constants too; buf ^ 1 is free
-        if (u + 1 < u_end) issue(u + 1, buf ^ 1);
+        if (u + 1 < u_end) {
+            if (ntau != itau) itau = ntau, ibase = tile_base(ntau);  // once per tile
+            issue(ntau, nch, buf ^ 1, ibase, nlofs);
+        }
         if (tau != cur_tile) cur_tile = tau, tbase = sBase[tp], last_t = sLast[tp];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -198,6 +209,7 @@ __global__ void __maxnreg__(96) k_fused2s(const __grid_constant__ FusedArgs a, c
             }
             if (s == 0) __syncthreads();  // B
         }
+        tau = ntau, ch = nch;
     }
     cp_async_wait<0>();
     if constexpr (RO) {
