@@ -132,6 +132,9 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
             }
             for (int b = 0; b < 2; ++b) mbar_init(&bar_lf[b], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            // programmatic dependent launch: everything above overlapped the previous launch's tail;
+            // the ARDM it writes is read from here on
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             for (int r = 0; r < min(R, NS); ++r) issue_load(r, t_begin + r / rounds, r % rounds);
         }
     } else {
@@ -171,6 +174,7 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     // 32 (w / 4) .. + 31), allocated by warp 0, zeroed by their threads
     if constexpr (RO)
         if (warp == 0) tmem_alloc(&tmem_base, 32 * kF4Groups);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous launch's ARDM / readout writes visible
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
@@ -442,6 +446,8 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
             if ((rd += kF4Groups) >= rounds) rd -= rounds, ++tau;
         }
     }
+    // the next launch (programmatic dependent launch) may start its setup on SMs this grid frees
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();  // every warp (incl. the store warp's last bulk wait) is done
     if constexpr (RO) {
         // one fixed-order grid reduction of the four steps' per-thread accumulators (the producer warps
@@ -481,8 +487,19 @@ template <bool SYM, bool RO, int LT>
 cudaError_t fused4_t(const FusedArgs &a, int grid, cudaStream_t s) {
     const size_t dyn = fused4_dyn();
     cudaFuncSetAttribute(k_fused4<SYM, RO, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    k_fused4<SYM, RO, LT><<<grid, kF4Block, dyn, s>>>(a);
-    return cudaGetLastError();
+    // programmatic dependent launch: the CTA setup (tables, barriers, TMEM) of this launch overlaps the
+    // tail of the previous one; the kernel waits (griddepcontrol.wait) before it touches the ARDM
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kF4Block);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_fused4<SYM, RO, LT>, a);
 }
 template <bool SYM, bool RO>
 cudaError_t fused4_lt(const FusedArgs &a, int grid, cudaStream_t s) {
