@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 SO = os.path.join(LIBDIR, "libquapi.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("host.cpp", "slide4.cu", "slide3.cu", "slide2.cu", "slide_r.cu", "persist.cu", "grow.cu", "ofpf.cu", "batch.cu", "eta.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("host.cpp", "slide4.cu", "slide3.cu", "slide2.cu", "slide2t.cu", "slide_r.cu", "persist.cu", "grow.cu", "ofpf.cu", "batch.cu", "eta.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "qp_internal.h"), os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "tmem.cuh"), os.path.join(ROOT, "include", "quapi.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -330,6 +330,7 @@ struct qp_plan {
     int M = 0, N = 0, L = 0, D = 0;
     bool lattice = false;        // class map used by the kernels
     bool sym = false;            // M = 2 with s = (+s, -s): symmetric-moment kernel
+    bool sym3 = false;           // M = 3 with s = (c, 0, -c): k_fused2t (conjugate-pair moments)
     uint32_t flags = 0;          // qp_problem.flags (QP_FLAG_*)
     double dt = 0.0;
     int64_t n_steps = 0;
@@ -368,6 +369,8 @@ struct qp_plan {
         long long f4_nA = 1;
         int f4_c0m = 1;
         mutable CUtensorMap tmapS{};
+        // k_fused2t (M = 3 lattice, S = 2, unsharded): view kind (slide2t.cu), -1 none
+        int f2t = -1;
     };
     int group_w = 1;                   // digits per outer digit group (g >= 1) of the factor tables
     int Smax = 1;
@@ -432,6 +435,7 @@ void build_classes(qp_plan &P) {
     }
     P.lattice = lat;
     P.sym = (M == 2) && P.s[0] == -P.s[1] && P.s[0] != 0.0 && !(P.flags & QP_FLAG_GENERIC_MOMENTS);
+    P.sym3 = (M == 3) && P.s[1] == 0.0 && P.s[0] == -P.s[2] && P.s[0] != 0.0 && !(P.flags & QP_FLAG_GENERIC_MOMENTS);
     P.D = qp::n_classes(M, lat);
     P.delta.assign(P.D, 0.0);
     for (int a = 0; a < M; ++a)
@@ -569,9 +573,11 @@ static bool encode_f3_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doubl
 
 // Persistent grid of one fused launch: fixed per (plan, launch set, device type), so the readout
 // order (block partials) is deterministic.
-static int slide_path(int S, const qp::FusedArgs &a) { return S == 3 ? (a.use_tma ? 2 : (a.lane_map & 1)) : 0; }
+static int slide_path(int S, const qp::FusedArgs &a) {
+    return S == 3 ? (a.use_tma ? 2 : (a.lane_map & 1)) : (S == 2 && a.use_tma ? 2 : 0);
+}
 static int slide_occupancy(const qp_plan &P, int S, int path) {
-    if (P.M == 3 && S == 2) return qp::fused2s_occupancy(P.lattice);
+    if (P.M == 3 && S == 2) return path == 2 ? qp::fused2t_occupancy() : qp::fused2s_occupancy(P.lattice);
     if (P.M == 2 && S == 4) return qp::fused4_occupancy(P.sym);
     if (P.M == 2 && S == 3) return qp::fused3_occupancy(P.sym, path & 1, path == 2);
     return qp::fused_r_occupancy(P.M, P.lattice, P.sym, S);
@@ -590,6 +596,7 @@ static cudaError_t launch_slide(const qp_plan &P, int S, const qp::FusedArgs &a,
             for (int kap = 0; kap < 2; ++kap)
                 for (int d = 0; d < P.D; ++d)
                     for (int v = 0; v < P.N; ++v) b.b[st][kap][d][v] = P.small[lay.beta(a.var[st], kap) + d * P.N + v];
+        if (a.use_tma) return qp::launch_fused2t(a, b, ro, grid, s);
         return qp::launch_fused2s(P.lattice, a, b, ro, grid, s);
     }
     if (P.M == 2 && S == 4) return qp::launch_fused4(P.sym, a, ro, grid, s);
@@ -766,9 +773,57 @@ static bool encode_f4_tmaps(const qp_plan::LaunchSet &ls, double2 *A) {
     return true;
 }
 
+// k_fused2t's TMA view of the ARDM for launch set ls (slide2t.cu): a 5-D tensor of FP64 whose box is one
+// unit of 27 outer fibres x the 81 inner entries (d0 = slot p0, d1 = slot p0 + 1); the same map loads
+// and stores.  VK 0 (p0 = 0): [d0][d1][slots 2..L-1]; VK 1 (p0 = L-1): [d1 = slot 0][slots 1..L-2][d0];
+// VK 2 (2 <= p0 <= L-2): [slots 0..p0-1][d0][d1][slots p0+2..]; VK 3 (p0 = 1): the same with a box of
+// 9 x 3 fibres.
+static bool encode_f2t_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, double2 *A) {
+    if (ls.tma_A == A) return true;
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const int L = P.L, p0 = ls.p0;
+    const cuuint64_t big = 16ull * (cuuint64_t)ipow(9, L);
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5];
+    auto set = [&](std::initializer_list<cuuint64_t> d, std::initializer_list<cuuint64_t> st, std::initializer_list<cuuint32_t> b) {
+        std::copy(d.begin(), d.end(), gd), std::copy(st.begin(), st.end(), gs), std::copy(b.begin(), b.end(), bx);
+    };
+    switch (ls.f2t) {
+    case 0: set({18, 9, (cuuint64_t)ipow(9, L - 2), 1, 1}, {16 * 9, 16 * 81, big, big}, {18, 9, 27, 1, 1}); break;
+    case 1: set({18, (cuuint64_t)ipow(9, L - 2), 9, 1, 1}, {16 * 9, 16ull * (cuuint64_t)ipow(9, L - 1), big, big}, {18, 27, 9, 1, 1}); break;
+    case 2:
+        set({2ull * (cuuint64_t)ipow(9, p0), 9, 9, (cuuint64_t)ipow(9, L - 2 - p0), 1},
+            {16ull * (cuuint64_t)ipow(9, p0), 16ull * (cuuint64_t)ipow(9, p0 + 1), 16ull * (cuuint64_t)ipow(9, p0 + 2), big},
+            {54, 9, 9, 1, 1});
+        break;
+    default: set({18, 9, 9, (cuuint64_t)ipow(9, L - 3), 1}, {16 * 9, 16 * 81, 16 * 729, big}, {18, 9, 9, 3, 1}); break;
+    }
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (enc(&ls.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)A, gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    ls.tma_A = A;
+    return true;
+}
+
 // TMA fields of one launch of set ls on the ARDM (or local shard block) A; d_work w holds the tables.
 static qp_status set_tma(const qp_plan &P, const qp_plan::LaunchSet &ls, qp::FusedArgs &a, double2 *A, char *w) {
     a.use_tma = 0;
+    if (ls.f2t >= 0) {
+        if (!encode_f2t_tmap(P, ls, A)) return err(QP_ERR_CUDA, "cuda: cannot encode the k_fused2t tensor map (p0 = %d)", ls.p0);
+        a.use_tma = 1;
+        a.tmap = ls.tmap;
+        a.f4_layout = ls.f2t;
+        // unit G (first outer fibre) = cB nA + cA: run A (VK 2, 3) as doubles in box dimension 0, the rest in
+        // dimension cdimB; VK 0, 1: one coordinate G
+        a.tma_nA = ls.f2t == 2 ? ipow(P.N, ls.p0) : (ls.f2t == 3 ? P.N : 0);
+        a.tma_c0m = 2;
+        a.f4_cdimA[0] = ls.f2t >= 2 ? 0 : -1;
+        a.f4_cdimB[0] = ls.f2t == 0 ? 2 : (ls.f2t == 1 ? 1 : 3);
+        a.E0r = (const double2 *)(w + ls.off_E0r);
+        return QP_OK;
+    }
     if (ls.S == 4) {
         if (!ls.f4 || !encode_f4_tmaps(ls, A)) return err(QP_ERR_CUDA, "cuda: cannot encode the k_fused4 tensor maps (p0 = %d)", ls.p0);
         a.use_tma = 1;
@@ -965,6 +1020,23 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
             }
             ls.e0r_F = F;
         }
+    }
+    ls.f2t = -1;
+    if (f2s && P.sym3 && removed.empty() && !(P.flags & QP_FLAG_NO_TMA) && L >= 4 && T % 27 == 0 && T / 27 >= 3) {
+        // k_fused2t: one block per 27-fibre unit of a tile: factors [s][kap][d][f] + the 27 lofs (int2)
+        ls.f2t = p0 == 0 ? 0 : (p0 == L - 1 ? 1 : (p0 == 1 ? 3 : 2));
+        const int F = qp::fused2t_unit_fibres(), R = T / F, Q = S * 2 * D;
+        const size_t blk = (size_t)qp::fused2t_e0_block();
+        ls.E0r.assign((size_t)R * blk, make_double2(0.0, 0.0));
+        for (int rd = 0; rd < R; ++rd) {
+            double2 *b = ls.E0r.data() + rd * blk;
+            for (int q = 0; q < Q; ++q) {
+                const int st = q / (2 * D), kap = (q / D) % 2, d = q % D;
+                for (int f = 0; f < F; ++f) b[(size_t)q * F + f] = ls.Etab[((((size_t)st * 2 + kap) * G) * D + d) * X + rd * F + f];
+            }
+            std::memcpy(b + (size_t)Q * F, ls.lofs.data() + (size_t)rd * F, F * sizeof(int2));
+        }
+        ls.e0r_F = F;
     }
     for (int st = 0; st < qp::kMaxS; ++st)
         for (int kap = 0; kap < 2; ++kap)
@@ -1337,10 +1409,10 @@ qp_status qp_init(qp_plan *P, void *d_ardm, void *d_work, void *stream) {
     {
         const qp_plan::LaunchSet &ls = P->sets[(size_t)std::min(1, P->L - 1) * P->Smax + P->Smax - 1];
         qp::FusedArgs a = ls.args;
-        a.use_tma = ls.tma_a != -1;
+        a.use_tma = ls.tma_a != -1 || ls.f2t >= 0;
         P->grid[P->Smax] = launch_grid(P, P->Smax, a);
         P->block = P->persist ? qp::kPersistBlock
-                   : (P->M == 3 && P->Smax == 2) ? qp::fused2s_block()
+                   : (P->M == 3 && P->Smax == 2) ? (ls.f2t >= 0 ? qp::fused2t_block() : qp::fused2s_block())
                    : (P->M == 2 && P->Smax == 4) ? qp::fused4_block()
                    : (P->M == 2 && P->Smax == 3) ? qp::fused3_block(a.lane_map, a.use_tma) : qp::fused_r_block(P->M, P->Smax);
     }

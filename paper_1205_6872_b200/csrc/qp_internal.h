@@ -176,6 +176,13 @@ struct Beta2s {
     double2 b[2][2][kMaxM * (kMaxM - 1) < 6 ? kMaxM * (kMaxM - 1) : 6][9];
 };
 cudaError_t launch_fused2s(bool lattice, const FusedArgs &a, const Beta2s &b, bool ro, int grid, cudaStream_t s);
+// k_fused2t (slide2t.cu): M = 3 lattice, S = 2, unsharded launch sets: TMA-staged 27-fibre units,
+// warp-specialised (load / store / 2 x 9 consumer warps); a.f4_layout = view kind VK (0..3)
+int fused2t_block();
+int fused2t_unit_fibres();
+int fused2t_e0_block();  // double2 entries of one unit's block: factors [S][2][D][27] + 27 int2 ('last')
+int fused2t_occupancy();
+cudaError_t launch_fused2t(const FusedArgs &a, const Beta2s &b, bool ro, int grid, cudaStream_t s);
 // k_fused4 (slide4.cu): M = 2, S = 4, TMA load + store of 8-fibre rounds, warp-specialised
 int fused4_block();
 int fused4_round_fibres();

@@ -232,3 +232,21 @@ def test_fused4_every_start_slot(L, generic):
     rg, plan, _ = gpu_run(w, flags=flags)
     assert plan.sizes.fuse_steps == 4
     check(rg, O.run(P(w)))
+
+
+@pytest.mark.parametrize("kind", [W.J_OHMIC_EXP, W.J_DEBYE])
+@pytest.mark.parametrize("L", [4, 5, 6, 7])
+def test_fused2t_every_start_slot(L, kind):
+    """k_fused2t (M = 3, s = (1, 0, -1): two steps per pass, TMA load + store of 27-fibre units,
+    conjugate-pair class moments) against the oracle; odd L visit every start slot, so all four TMA
+    views occur (p0 = 0, p0 = 1, 2 <= p0 <= L-2, p0 = L-1).  The same run through k_fused2s
+    (QP_FLAG_NO_TMA: cp.async staging, nine complex products per moment) agrees to rounding."""
+    n = 3 * L + 3
+    w = W.random_problem(900 + L, 3, L, n, kind=kind)
+    assert tuple(w.s) == (1.0, 0.0, -1.0)
+    rg, plan, _ = gpu_run(w)
+    assert plan.sizes.fuse_steps == 2 and plan.sizes.block == 640  # the k_fused2t launch configuration
+    check(rg, O.run(P(w)))
+    rs, plan_s, _ = gpu_run(w, flags=Q.QP_FLAG_NO_TMA)
+    assert plan_s.sizes.block == 288
+    assert np.abs(rg - rs).max() <= 1e-13
