@@ -95,7 +95,8 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
     double2 *const sE0 = smem2t + kT2NS * kT2Data;       // [kT2NS][kT2E0B]
     __shared__ double2 sK[2][N][N];
     __shared__ double2 sIn[S][2][D][N];  // inner factor of the other inner digit: [s][kap][d][value]
-    // class-weight constants [s][kap][d]: ch1, sh1, ch2, sh2, Re P, Im P, Re P^2, Im P^2 (see the moments)
+    // class-weight constants [s][kap][d] (see the moments): Re P ch1, Re P sh1, Im P ch1, Im P sh1, ch2, sh2,
+    // Re P^2, Im P^2 with ch_j = (R^j + R^-j) / 2, sh_j = (R^j - R^-j) / 2
     __shared__ __align__(16) double sC[S][2][D][8];
     // per tile (double buffered by tile parity, built by the load warp): Ehi (outer groups >= 1) x inner
     // factor of the digit value, and sub-step 0's 'last' when it is a tile digit
@@ -129,10 +130,10 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
         const int s = tid / (2 * D), kap = (tid / D) % 2, d = tid % D;
         const double2 *b = bt.b[s][kap][d];
         const double r1 = hypot(b[1].x, b[1].y), r1i = hypot(b[3].x, b[3].y);
+        const double ch1 = 0.5 * (r1 + r1i), sh1 = 0.5 * (r1 - r1i), pr = b[1].x / r1, pi = b[1].y / r1;
         double *c = sC[s][kap][d];
-        c[0] = 0.5 * (r1 + r1i), c[1] = 0.5 * (r1 - r1i);
-        c[2] = 0.5 * (b[2].x + b[6].x), c[3] = 0.5 * (b[2].x - b[6].x);
-        c[4] = b[1].x / r1, c[5] = b[1].y / r1;
+        c[0] = pr * ch1, c[1] = pr * sh1, c[2] = pi * ch1, c[3] = pi * sh1;
+        c[4] = 0.5 * (b[2].x + b[6].x), c[5] = 0.5 * (b[2].x - b[6].x);
         c[6] = b[0].x, c[7] = b[0].y;
     }
     if (tid == 0) {
@@ -178,8 +179,8 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                     // s = (c, 0, -c): with eta of the class weights = er + i ei, beta(a, b) = R^(s_a - s_b)
                     // P^(s_a + s_b) (R = e^(-delta er) real, |P| = 1), so the old-state pairs (0,2)/(2,0) have
                     // real weights R^(+-2), (0,0)/(2,2) conjugate weights P^(+-2), (0,1)/(1,0) and (1,2)/(2,1)
-                    // weights P^(+-1) R^(+-1), and (1,1) weight 1 (sC: ch1, sh1, ch2, sh2, P, P^2 per class):
-                    // 24 instead of 36 FP64 operations per class moment; one pair group live at a time
+                    // weights P^(+-1) R^(+-1), and (1,1) weight 1 (sC per class, below): 16 instead of 36 FP64
+                    // operations per class moment; one pair group live at a time
                     const double2 xc = slot(4);
                     double2 S0v = xc, mp[D], mr[RO ? D : 1];
 #pragma unroll
@@ -198,8 +199,8 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                         const double2 x = slot(2), y = slot(6), pp = cadd(x, y), qq = csub(x, y);
                         S0v = cadd(S0v, pp);
                         each([&](const double *c, double2 &m) {
-                            m.x = fma(c[2], pp.x, fma(c[3], qq.x, m.x));
-                            m.y = fma(c[2], pp.y, fma(c[3], qq.y, m.y));
+                            m.x = fma(c[4], pp.x, fma(c[5], qq.x, m.x));
+                            m.y = fma(c[4], pp.y, fma(c[5], qq.y, m.y));
                         });
                     }
                     {  // (0,0) / (2,2): P^2 x + conj(P^2) y = Re P^2 (x + y) + i Im P^2 (x - y)
@@ -210,16 +211,16 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                             m.y = fma(c[6], pp.y, fma(c[7], qq.x, m.y));
                         });
                     }
-                    {  // (0,1)/(1,0) -> A, (1,2)/(2,1) -> B (ch1 (x + y) + sh1 (x - y)); P A + conj(P) B
+                    {  // (0,1)/(1,0) -> A, (1,2)/(2,1) -> B, A = ch1 (x + y) + sh1 (x - y); P A + conj(P) B
+                       // = Re P (A + B) + i Im P (A - B): with the per-fibre sums and differences of the two
+                       // pairs and c[0..3] = Re P ch1, Re P sh1, Im P ch1, Im P sh1 it is 8 FMA per class
                         const double2 x1 = slot(1), y1 = slot(3), x5 = slot(5), y5 = slot(7);
                         const double2 p1 = cadd(x1, y1), q1 = csub(x1, y1), p5 = cadd(x5, y5), q5 = csub(x5, y5);
-                        S0v = cadd(S0v, cadd(p1, p5));
+                        const double2 P15 = cadd(p1, p5), Q15 = cadd(q1, q5), Pd = csub(p1, p5), Qd = csub(q1, q5);
+                        S0v = cadd(S0v, P15);
                         each([&](const double *c, double2 &m) {
-                            const double2 A = make_double2(fma(c[0], p1.x, c[1] * q1.x), fma(c[0], p1.y, c[1] * q1.y));
-                            const double2 B = make_double2(fma(c[0], p5.x, c[1] * q5.x), fma(c[0], p5.y, c[1] * q5.y));
-                            const double2 u = cadd(A, B), v = csub(A, B);
-                            m.x = fma(c[4], u.x, fma(-c[5], v.y, m.x));
-                            m.y = fma(c[4], u.y, fma(c[5], v.x, m.y));
+                            m.x = fma(c[0], P15.x, fma(c[1], Q15.x, fma(-c[2], Pd.y, fma(-c[3], Qd.y, m.x))));
+                            m.y = fma(c[0], P15.y, fma(c[1], Q15.y, fma(c[2], Pd.x, fma(c[3], Qd.x, m.y))));
                         });
                     }
                     // class moment x its class factor E0 (outer group 0, this fibre) x EI (tile x inner digit w)
