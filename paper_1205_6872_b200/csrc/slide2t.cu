@@ -32,7 +32,7 @@ constexpr int kT2N = 9, kT2F = 27;                  // N, outer fibres per unit
 constexpr int kT2GW = kT2N, kT2Groups = 2;          // warps per consumer group, groups (alternate units)
 constexpr int kT2Consumers = kT2Groups * kT2GW;     // 18
 constexpr int kT2Block = 32 * (kT2Consumers + 2);   // + store warp + load warp
-constexpr int kT2NS = 4;                            // ring depth
+constexpr int kT2NS = 5;                            // ring depth
 constexpr int kT2Data = 2192;                       // 27 x 81 = 2187 entries, padded to a 128-B multiple
 constexpr int kT2D = 4;                             // classes (lattice s, M = 3)
 constexpr int kT2E0B = 2 * 2 * kT2D * kT2F + 14;    // unit block: factors [s][kap][d][27] + 27 int2 ('last')
