@@ -30,6 +30,9 @@ for flags in (0, Q.QP_FLAG_NO_TMA, Q.QP_FLAG_GENERIC_MOMENTS):
 for flags in (0, Q.QP_FLAG_GENERIC_MOMENTS):
     for L in (8, 9):
         run(W.random_problem(7, 2, L, 2 * L + 6), flags=flags)
+# k_fused2t (M = 3, s = (1, 0, -1): TMA units, all four views at L = 5) and the same through k_fused2s
+for flags in (0, Q.QP_FLAG_NO_TMA):
+    run(W.random_problem(9, 3, 5, 18), flags=flags | NP)
 # k_small: one CTA, ARDM and tables in shared memory (M = 2, 3, 4)
 for w in (W.CONFIGS[1].with_(n_steps=14), W.random_problem(3, 3, 3, 9), W.random_problem(4, 4, 2, 7),
           W.random_problem(5, 2, 6, 15, lattice_s=False)):

@@ -250,3 +250,5 @@ def test_fused2t_every_start_slot(L, kind):
     rs, plan_s, _ = gpu_run(w, flags=Q.QP_FLAG_NO_TMA)
     assert plan_s.sizes.block == 288
     assert np.abs(rg - rs).max() <= 1e-13
+    r2, _, _ = gpu_run(w)  # fixed grid, fixed unit -> CTA assignment and reduction order: bit-identical
+    assert np.array_equal(rg, r2)
