@@ -187,28 +187,35 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                     for (int d = 0; d < D; ++d) mp[d] = xc;
 #pragma unroll
                     for (int d = 0; d < (RO ? D : 1); ++d) mr[d] = xc;
-                    auto each = [&](auto &&fn) {  // fn(class constants, moment) for every used (kap, d)
+                    // fn(class constants, moment, g) for every used (kap, d).  Classes d and d + 2 have opposite
+                    // Delta s (R -> 1/R, P -> conj P): class d + 2's moment uses class d's constants with
+                    // the signs of sh_j and Im P flipped (g = -1 on c[1], c[2], c[5], c[7])
+                    auto each = [&](auto &&fn) {
 #pragma unroll
-                        for (int d = 0; d < D; ++d) fn(&sC[s][0][d][0], mp[d]);
+                        for (int d = 0; d < D / 2; ++d) {
+                            const double *c = &sC[s][0][d][0];
+                            fn(c, mp[d], 1.0);
+                            fn(c, mp[d + D / 2], -1.0);
+                        }
                         if constexpr (RO)
 #pragma unroll
                             for (int d = 0; d < D; ++d)
-                                if (upper_class(d)) fn(&sC[s][1][d][0], mr[d]);
+                                if (upper_class(d)) fn(&sC[s][1][d][0], mr[d], 1.0);
                     };
                     {  // (0,2) / (2,0): real weights ch2 (x + y) + sh2 (x - y)
                         const double2 x = slot(2), y = slot(6), pp = cadd(x, y), qq = csub(x, y);
                         S0v = cadd(S0v, pp);
-                        each([&](const double *c, double2 &m) {
-                            m.x = fma(c[4], pp.x, fma(c[5], qq.x, m.x));
-                            m.y = fma(c[4], pp.y, fma(c[5], qq.y, m.y));
+                        each([&](const double *c, double2 &m, double g) {
+                            m.x = fma(c[4], pp.x, fma(g * c[5], qq.x, m.x));
+                            m.y = fma(c[4], pp.y, fma(g * c[5], qq.y, m.y));
                         });
                     }
                     {  // (0,0) / (2,2): P^2 x + conj(P^2) y = Re P^2 (x + y) + i Im P^2 (x - y)
                         const double2 x = slot(0), y = slot(8), pp = cadd(x, y), qq = csub(x, y);
                         S0v = cadd(S0v, pp);
-                        each([&](const double *c, double2 &m) {
-                            m.x = fma(c[6], pp.x, fma(-c[7], qq.y, m.x));
-                            m.y = fma(c[6], pp.y, fma(c[7], qq.x, m.y));
+                        each([&](const double *c, double2 &m, double g) {
+                            m.x = fma(c[6], pp.x, fma(-g * c[7], qq.y, m.x));
+                            m.y = fma(c[6], pp.y, fma(g * c[7], qq.x, m.y));
                         });
                     }
                     {  // (0,1)/(1,0) -> A, (1,2)/(2,1) -> B, A = ch1 (x + y) + sh1 (x - y); P A + conj(P) B
@@ -218,9 +225,9 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                         const double2 p1 = cadd(x1, y1), q1 = csub(x1, y1), p5 = cadd(x5, y5), q5 = csub(x5, y5);
                         const double2 P15 = cadd(p1, p5), Q15 = cadd(q1, q5), Pd = csub(p1, p5), Qd = csub(q1, q5);
                         S0v = cadd(S0v, P15);
-                        each([&](const double *c, double2 &m) {
-                            m.x = fma(c[0], P15.x, fma(c[1], Q15.x, fma(-c[2], Pd.y, fma(-c[3], Qd.y, m.x))));
-                            m.y = fma(c[0], P15.y, fma(c[1], Q15.y, fma(c[2], Pd.x, fma(c[3], Qd.x, m.y))));
+                        each([&](const double *c, double2 &m, double g) {
+                            m.x = fma(c[0], P15.x, fma(g * c[1], Q15.x, fma(-g * c[2], Pd.y, fma(-c[3], Qd.y, m.x))));
+                            m.y = fma(c[0], P15.y, fma(g * c[1], Q15.y, fma(g * c[2], Pd.x, fma(c[3], Qd.x, m.y))));
                         });
                     }
                     // class moment x its class factor E0 (outer group 0, this fibre) x EI (tile x inner digit w)
