@@ -452,22 +452,31 @@ __global__ void __maxnreg__(168) k_fused4(const __grid_constant__ FusedArgs a) {
     if constexpr (RO) {
         // one fixed-order grid reduction of the four steps' per-thread accumulators (the producer warps
         // contribute 0); the stages are free now and hold the scratch
-        double2 tt[S * N];
+        // per step two values: (Re rho_00, Re rho_11) and rho_01 (rho_10 = conj rho_01)
+        double2 tt[2 * S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (warp < kF4Consumers) {
                 double p[4];
                 tmem_wait_st();
                 tmem_ld_d4(tacc + 8 * s, p);
-                tt[s * N + 0] = make_double2(p[0], 0.0), tt[s * N + 1] = make_double2(p[2], p[3]);
-                tt[s * N + 2] = make_double2(p[2], -p[3]), tt[s * N + 3] = make_double2(p[1], 0.0);
+                tt[2 * s] = make_double2(p[0], p[1]), tt[2 * s + 1] = make_double2(p[2], p[3]);
             } else {
-                tt[s * N + 0] = tt[s * N + 1] = tt[s * N + 2] = tt[s * N + 3] = make_double2(0.0, 0.0);
+                tt[2 * s] = tt[2 * s + 1] = make_double2(0.0, 0.0);
             }
         }
-        grid_sum_multi<S * N, kF4Block>(tt, stage, a.partials, a.counter, [&](int v, double2 x) {
-            double2 *r = a.rho[v / N];
-            if (r != nullptr) r[v % N] = a.rho_accumulate ? cadd(r[v % N], x) : x;
+        grid_sum_multi<2 * S, kF4Block>(tt, stage, a.partials, a.counter, [&](int v, double2 x) {
+            double2 *r = a.rho[v / 2];
+            if (r == nullptr) return;
+            const bool acc = a.rho_accumulate != 0;
+            if (v & 1) {
+                r[1] = acc ? cadd(r[1], x) : x;
+                const double2 xc = make_double2(x.x, -x.y);
+                r[2] = acc ? cadd(r[2], xc) : xc;
+            } else {
+                r[0] = acc ? make_double2(r[0].x + x.x, r[0].y) : make_double2(x.x, 0.0);
+                r[3] = acc ? make_double2(r[3].x + x.y, r[3].y) : make_double2(x.y, 0.0);
+            }
         });
         tmem_fence_before();
         __syncthreads();
