@@ -18,8 +18,8 @@
 //   consumers   : two groups of 9 warps take alternate units; warp w: sub-step 0 the fibres along d0
 //                 with d1 = w, group barrier (named), sub-step 1 along d1 with d0 = w, both in place in
 //                 the stage; fence the async proxy, arrive on done[b];
-//   store warp  : unit j: wait done[b], one cp.async.bulk.tensor store; once the store of unit j - 1 has
-//                 read its stage, arrive on that stage's empty barrier.
+//   store warp  : unit j: wait done[b], one cp.async.bulk.tensor store; once it has read the stage,
+//                 arrive on the stage's empty barrier.
 // Used for s = (c, 0, -c) (the class moments use the conjugate symmetry of the weights, 4 old-state
 // pairs + the centre instead of 9 complex products).  Lanes 27..31 of the consumer warps idle (a box of 27 fibres tiles every view exactly: no padding
 // traffic).  Readout accumulators in registers, fixed-order CTA reduction at the end (deterministic).
@@ -292,18 +292,18 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
         if (lane == 0) {
             Cursor cur;
             cur.init(a, u_begin * kT2F);
-            int b = 0, ph = 0, bp = 0;
+            // a unit takes a consumer group several microseconds, so the store warp waits for each store to
+            // have read its stage and releases the stage at once (the load warp refills it a unit earlier
+            // than if the release waited for the next unit's store)
+            int b = 0, ph = 0;
             for (long long j = 0; j < R; ++j) {
                 mbar_wait(&bar_done[b], ph);
                 int c[5];
                 cur.coords(c);
                 tma_store_5d_t(&a.tmap, sData + b * kT2Data, c);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                if (j >= 1) {
-                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                    arrive_t(&bar_empty[bp]);
-                }
-                bp = b;
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                arrive_t(&bar_empty[b]);
                 if (++b == NS) b = 0, ph ^= 1;
                 cur.next();
             }
