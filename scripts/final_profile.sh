@@ -16,11 +16,12 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fu
     python bench.py --steps 40 --warmup 4 --reps 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_f4.log 2>&1
 python scripts/ncu_summary.py gpurun_out/prof_f4.ncu-rep gpurun_out/prof_f4.json > /dev/null
 python scripts/ncu_stalls.py gpurun_out/prof_f4.ncu-rep 8 > gpurun_out/stalls_f4.json
-# k_fused2s on cfg4
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused2s -s 4 -c 1 -o gpurun_out/prof_f2s -f \
-    python bench.py --cfg 4 --steps 20 --warmup 4 --reps 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_f2s.log 2>&1
-python scripts/ncu_summary.py gpurun_out/prof_f2s.ncu-rep gpurun_out/prof_f2s.json > /dev/null
-python scripts/ncu_stalls.py gpurun_out/prof_f2s.ncu-rep 8 > gpurun_out/stalls_f2s.json
+# k_fused2t on cfg4
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused2t -s 4 -c 2 -o gpurun_out/prof_f2t -f \
+    python bench.py --cfg 4 --steps 20 --warmup 4 --reps 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_f2t.log 2>&1
+python scripts/ncu_summary.py gpurun_out/prof_f2t.ncu-rep gpurun_out/prof_f2t.json > /dev/null
+python scripts/ncu_stalls.py gpurun_out/prof_f2t.ncu-rep 8 > gpurun_out/stalls_f2t.json
+timeout 300 python scripts/perp.py --cfg 4 > gpurun_out/perp4.txt 2>&1
 timeout 300 python scripts/perp.py > gpurun_out/perp.txt 2>&1
 timeout 300 python scripts/perp.py --final-only > gpurun_out/perp_final_only.txt 2>&1
 tail -c 400 gpurun_out/bench.json; echo; cut -c1-200 gpurun_out/bench_cfgs.jsonl; tail -2 gpurun_out/perp.txt; du -sh gpurun_out
