@@ -11,26 +11,28 @@
 //   VK 1 (p0 = L-1)      : d1 + 9 f + 243 d0
 //   VK 2 (2 <= p0 <= L-2): f + 27 d0 + 243 d1        (27 consecutive fibres of the run of slots < p0)
 //   VK 3 (p0 = 1)        : f%9 + 9 d0 + 81 d1 + 729 (f/9)
-// -- conflict-free 16-B accesses for lane = fibre in every case.  One CTA per SM, 20 warps:
+// -- conflict-free 16-B accesses for consecutive fibres in every case.  One CTA per SM, 18 warps:
 //   load warp   : unit r into stage r % NS once the stage's previous unit has been stored (empty[b]):
 //                 one cp.async.bulk.tensor box + one bulk copy of the unit's outer group-0 factors and
 //                 'last' digits, completing on full[b]; also builds each tile's constants;
-//   consumers   : two groups of 9 warps take alternate units; warp w: sub-step 0 the fibres along d0
-//                 with d1 = w, group barrier (named), sub-step 1 along d1 with d0 = w, both in place in
-//                 the stage; fence the async proxy, arrive on done[b];
+//   consumers   : two groups of 8 warps take alternate units; thread t < 243 of a group (fibre t % 27,
+//                 digit w = t / 27): sub-step 0 the fibre along d0 with d1 = w, group barrier (named),
+//                 sub-step 1 along d1 with d0 = w, both in place in the stage; fence the async proxy,
+//                 arrive on done[b];
 //   store warp  : unit j: wait done[b], one cp.async.bulk.tensor store; once it has read the stage,
 //                 arrive on the stage's empty barrier.
-// Used for s = (c, 0, -c) (the class moments use the conjugate symmetry of the weights, 4 old-state
-// pairs + the centre instead of 9 complex products).  Lanes 27..31 of the consumer warps idle (a box of 27 fibres tiles every view exactly: no padding
-// traffic).  Readout accumulators in registers, fixed-order CTA reduction at the end (deterministic).
+// Used for s = (c, 0, -c) (the class moments use the structure of the weights: old-state pairs instead
+// of 9 complex products).  13 of a group's 256 threads idle (a box of 27 fibres tiles every view
+// exactly: no padding traffic).  Readout accumulators in registers, fixed-order CTA reduction at the
+// end (deterministic).
 #include "common.cuh"
 
 namespace qp {
 
 namespace {
 constexpr int kT2N = 9, kT2F = 27;                  // N, outer fibres per unit
-constexpr int kT2GW = kT2N, kT2Groups = 2;          // warps per consumer group, groups (alternate units)
-constexpr int kT2Consumers = kT2Groups * kT2GW;     // 18
+constexpr int kT2GW = 8, kT2Groups = 2;             // warps per consumer group, groups (alternate units)
+constexpr int kT2Consumers = kT2Groups * kT2GW;     // 16: a group's 256 threads take the 243 fibres of a sub-step
 constexpr int kT2Block = 32 * (kT2Consumers + 2);   // + store warp + load warp
 constexpr int kT2NS = 5;                            // ring depth
 constexpr int kT2Data = 2192;                       // 27 x 81 = 2187 entries, padded to a 128-B multiple
@@ -153,9 +155,10 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
 
     if (warp < kT2Consumers) {
         // =========================================================== consumer groups
-        const int g = warp / kT2GW, w = warp % kT2GW;
-        const int f = lane;
-        const bool valid = f < kT2F;
+        // thread t of group g: fibre f = t % 27 of the unit, inner digit w = t / 27 (t < 243)
+        const int g = warp / kT2GW, t = tid - g * 32 * kT2GW;
+        const int f = t % kT2F, w = t / kT2F;
+        const bool valid = t < kT2F * kT2N;
         const int cf = VK == 0 ? 81 * f : (VK == 1 ? 9 * f : (VK == 2 ? f : (f % 9) + 729 * (f / 9)));
         long long uu = u_begin + g;
         int tau = (int)(uu / CH), ch = (int)(uu % CH), b = g % NS, ph = (g / NS) & 1;
@@ -345,8 +348,8 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if constexpr (RO) {
-        const int w = warp % kT2GW;
-        const bool cons = warp < kT2Consumers && lane < kT2F;
+        const int t = tid - (warp / kT2GW) * 32 * kT2GW, w = t / kT2F;
+        const bool cons = warp < kT2Consumers && t < kT2F * kT2N;
 #pragma unroll
         for (int s = 0; s < S; ++s)
             if (a.rho[s] != nullptr) {

@@ -245,7 +245,7 @@ def test_fused2t_every_start_slot(L, kind):
     w = W.random_problem(900 + L, 3, L, n, kind=kind)
     assert tuple(w.s) == (1.0, 0.0, -1.0)
     rg, plan, _ = gpu_run(w)
-    assert plan.sizes.fuse_steps == 2 and plan.sizes.block == 640  # the k_fused2t launch configuration
+    assert plan.sizes.fuse_steps == 2 and plan.sizes.block == 576  # the k_fused2t launch configuration
     check(rg, O.run(P(w)))
     rs, plan_s, _ = gpu_run(w, flags=Q.QP_FLAG_NO_TMA)
     assert plan_s.sizes.block == 288
