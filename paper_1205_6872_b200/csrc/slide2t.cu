@@ -25,7 +25,7 @@
 // of 9 complex products).  13 of a group's 256 threads idle (a box of 27 fibres tiles every view
 // exactly: no padding traffic).  Readout accumulators in registers, fixed-order CTA reduction at the
 // end (deterministic).
-#include "common.cuh"
+#include "tmem.cuh"
 
 namespace qp {
 
@@ -104,6 +104,7 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
     // factor of the digit value, and sub-step 0's 'last' when it is a tile digit
     __shared__ double2 sEI[2][S][2][D][N];
     __shared__ int sLast[2];
+    __shared__ unsigned tmem_base;
     __shared__ __align__(8) unsigned long long bar_full[kT2NS], bar_done[kT2NS], bar_empty[kT2NS], bar_ei[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     auto upper_class = [](int d) {
@@ -143,15 +144,25 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
         for (int b = 0; b < 2; ++b) mbar_init(&bar_ei[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // readout sums in tensor memory (frees ~26 registers of the 96): consumer warp w owns 64 columns of
+    // its lane quarter (warps w, w + 4, w + 8, w + 12 share the lanes 32 (w % 4) .. + 31); blocks of 8
+    // columns (4 doubles): A = Re rho_00, Re rho_11, Re rho_22 (sub-step 0); B = rho_01, rho_02; C = rho_12
+    // (sub-step 0); D = the plain sum, class-(b - a = 1) moment; E = class-(b - a = 2) moment (sub-step 1)
+    if constexpr (RO)
+        if (warp == 0) tmem_alloc(&tmem_base, 256);
     // programmatic dependent launch: the setup above overlapped the previous launch's tail
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    tmem_fence_before();
     __syncthreads();
-
-    double2 acc0[RO ? NU : 1], accS1 = make_double2(0.0, 0.0), accM1[RO ? D : 1];
+    tmem_fence_after();
+    const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 64u * (unsigned)((warp >> 2) & 3);
+    if constexpr (RO)
+        if (warp < kT2Consumers) {
+            const double z[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int n = 0; n < (RO ? NU : 1); ++n) acc0[n] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int n = 0; n < (RO ? D : 1); ++n) accM1[n] = make_double2(0.0, 0.0);
+            for (int i = 0; i < 5; ++i) tmem_st_d4(tacc + 8 * i, z);
+            tmem_wait_st();
+        }
 
     if (warp < kT2Consumers) {
         // =========================================================== consumer groups
@@ -176,6 +187,12 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
             const int lastf = valid ? reinterpret_cast<const int2 *>(e0b + S * 2 * D * kT2F)[f].y : 0;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
+                // this fibre's readout terms (flushed into tensor memory after the sub-step)
+                double2 acc0[RO ? NU : 1], accS1 = make_double2(0.0, 0.0), accM1[RO ? D : 1];
+#pragma unroll
+                for (int n = 0; n < (RO ? NU : 1); ++n) acc0[n] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int n = 0; n < (RO ? D : 1); ++n) accM1[n] = make_double2(0.0, 0.0);
                 if (valid) {
                     auto slot = [&](int v) -> double2 & { return s == 0 ? st[S0 * v + S1 * w] : st[S0 * w + S1 * v]; };
                     const int last = s == 0 ? (lastf >= 0 ? lastf : last_t) : w;
@@ -280,6 +297,27 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                             if (class_of(M, LAT, nw / M, nw % M) == d + 1) slot(nw) = cmul(sK[0][nw][last], m);
                     }
                 }
+                if constexpr (RO) {  // every lane (tcgen05 is warp-collective; idle threads add zeros)
+                    tmem_wait_st();  // this thread's previous store to the columns has landed
+                    if (s == 0) {
+                        unsigned ra[8], rb[8], rc[8];
+                        tmem_ld8_nowait(tacc, ra), tmem_ld8_nowait(tacc + 8, rb), tmem_ld8_nowait(tacc + 16, rc);
+                        tmem_wait_ld();
+                        double2 x0, x1, y0, y1, z0, z1;
+                        tmem_unpack_c2(ra, x0, x1), tmem_unpack_c2(rb, y0, y1), tmem_unpack_c2(rc, z0, z1);
+                        tmem_st_c2(tacc, make_double2(x0.x + acc0[0].x, x0.y + acc0[3].x), make_double2(x1.x + acc0[5].x, 0.0));
+                        tmem_st_c2(tacc + 8, cadd(y0, acc0[1]), cadd(y1, acc0[2]));
+                        tmem_st_c2(tacc + 16, cadd(z0, acc0[4]), z1);
+                    } else {
+                        unsigned rd[8], re[8];
+                        tmem_ld8_nowait(tacc + 24, rd), tmem_ld8_nowait(tacc + 32, re);
+                        tmem_wait_ld();
+                        double2 x0, x1, y0, y1;
+                        tmem_unpack_c2(rd, x0, x1), tmem_unpack_c2(re, y0, y1);
+                        tmem_st_c2(tacc + 24, cadd(x0, accS1), cadd(x1, accM1[2]));
+                        tmem_st_c2(tacc + 32, cadd(y0, accM1[3]), y1);
+                    }
+                }
                 if (s == 0) group_sync_t(1 + g);  // sub-step 0 of the whole unit is in the stage
             }
             fence_proxy_async();  // this thread's stage writes -> visible to the TMA store
@@ -350,6 +388,22 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
     if constexpr (RO) {
         const int t = tid - (warp / kT2GW) * 32 * kT2GW, w = t / kT2F;
         const bool cons = warp < kT2Consumers && t < kT2F * kT2N;
+        double2 acc0[NU], accS1, accM1[D];
+        {
+            double2 q[10];
+            if (warp < kT2Consumers) {
+                tmem_wait_st();
+#pragma unroll
+                for (int i = 0; i < 5; ++i) tmem_ld_c2(tacc + 8 * i, q[2 * i], q[2 * i + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 10; ++i) q[i] = make_double2(0.0, 0.0);
+            }
+            acc0[0] = make_double2(q[0].x, 0.0), acc0[3] = make_double2(q[0].y, 0.0), acc0[5] = make_double2(q[1].x, 0.0);
+            acc0[1] = q[2], acc0[2] = q[3], acc0[4] = q[4];
+            accS1 = q[6], accM1[2] = q[7], accM1[3] = q[8];
+            accM1[0] = accM1[1] = make_double2(0.0, 0.0);
+        }
 #pragma unroll
         for (int s = 0; s < S; ++s)
             if (a.rho[s] != nullptr) {
@@ -369,6 +423,12 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                 reduce_finalize<N, kT2Block>(full, a.partials + (size_t)s * kPartialsMax * N, a.rho[s], a.counter + s,
                                              a.rho_accumulate != 0);
             }
+        tmem_fence_before();
+        __syncthreads();
+        if (warp == 0) {
+            tmem_fence_after();
+            tmem_dealloc(tmem_base, 256);
+        }
     }
 }
 
