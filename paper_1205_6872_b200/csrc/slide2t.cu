@@ -146,8 +146,11 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
     }
     // readout sums in tensor memory (frees ~26 registers of the 96): consumer warp w owns 64 columns of
     // its lane quarter (warps w, w + 4, w + 8, w + 12 share the lanes 32 (w % 4) .. + 31); blocks of 8
-    // columns (4 doubles): A = Re rho_00, Re rho_11, Re rho_22 (sub-step 0); B = rho_01, rho_02; C = rho_12
-    // (sub-step 0); D = the plain sum, class-(b - a = 1) moment; E = class-(b - a = 2) moment (sub-step 1)
+    // columns (4 doubles) at tacc + 8 i: 0 = Re rho_00, Re rho_11, Re rho_22 (sub-step 0); 1 = the plain sum
+    // (sub-step 1); the class-moment terms are summed per tile WITHOUT the tile's inner factor EI (a
+    // common factor of the tile for the thread's digit w) in 2 = rho_01, rho_02, 3 = rho_12 (sub-step 0),
+    // class-(b - a = 1) moment (sub-step 1), 4 = class-(b - a = 2) moment (sub-step 1), and folded (x EI)
+    // into 5, 6, 7 (same order) when the tile changes
     if constexpr (RO)
         if (warp == 0) tmem_alloc(&tmem_base, 256);
     // programmatic dependent launch: the setup above overlapped the previous launch's tail
@@ -160,7 +163,7 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
         if (warp < kT2Consumers) {
             const double z[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int i = 0; i < 5; ++i) tmem_st_d4(tacc + 8 * i, z);
+            for (int i = 0; i < 8; ++i) tmem_st_d4(tacc + 8 * i, z);
             tmem_wait_st();
         }
 
@@ -174,8 +177,31 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
         long long uu = u_begin + g;
         int tau = (int)(uu / CH), ch = (int)(uu % CH), b = g % NS, ph = (g / NS) & 1;
         int cur_tile = -1, last_t = 0, tp = 0;
+        // the tile sums of blocks 2..4 x the tile's EI into blocks 5..7, blocks 2..4 zeroed (warp-collective)
+        auto fold = [&](int tpo) {
+            if constexpr (RO) {
+                const int wc = w < N ? w : N - 1;  // (idle threads: zero sums)
+                const double2 e02 = sEI[tpo][0][1][2][wc], e03 = sEI[tpo][0][1][3][wc];
+                const double2 e12 = sEI[tpo][1][1][2][wc], e13 = sEI[tpo][1][1][3][wc];
+                tmem_wait_st();
+                unsigned r[6][8];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) tmem_ld8_nowait(tacc + 16 + 8 * i, r[i]), tmem_ld8_nowait(tacc + 40 + 8 * i, r[3 + i]);
+                tmem_wait_ld();
+                double2 x[6][2];
+#pragma unroll
+                for (int i = 0; i < 6; ++i) tmem_unpack_c2(r[i], x[i][0], x[i][1]);
+                tmem_st_c2(tacc + 40, cfma(e02, x[0][0], x[3][0]), cfma(e03, x[0][1], x[3][1]));
+                tmem_st_c2(tacc + 48, cfma(e02, x[1][0], x[4][0]), cfma(e12, x[1][1], x[4][1]));
+                tmem_st_c2(tacc + 56, cfma(e13, x[2][0], x[5][0]), x[5][1]);
+                const double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) tmem_st_c2(tacc + 16 + 8 * i, z, z);
+            }
+        };
         for (long long j = g; j < R; j += kT2Groups) {
             if (tau != cur_tile) {
+                if (cur_tile >= 0) fold(tp);
                 cur_tile = tau;
                 tp = (tau - tau0) & 1;
                 mbar_wait(&bar_ei[tp], ((tau - tau0) >> 1) & 1);
@@ -250,9 +276,11 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                             m.y = fma(c[0], P15.y, fma(g * c[1], Q15.y, fma(g * c[2], Pd.x, fma(c[3], Qd.x, m.y))));
                         });
                     }
-                    // class moment x its class factor E0 (outer group 0, this fibre) x EI (tile x inner digit w)
+                    // class moment x its class factor E0 (outer group 0, this fibre) x EI (tile x inner digit w);
+                    // the readout terms leave EI out (applied per tile by fold)
                     auto moment = [&](int kap, int d) {
                         const double2 mm = kap == 0 ? mp[d] : mr[RO ? d : 0];
+                        if (kap == 1) return cmul(e0b[((s * 2 + kap) * D + d) * kT2F + f], mm);
                         return cmul(cmul(e0b[((s * 2 + kap) * D + d) * kT2F + f], sEI[tp][s][kap][d][w]), mm);
                     };
                     if constexpr (RO) {  // readout first (upper triangle only: rho_ba = conj rho_ab)
@@ -301,21 +329,22 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                     tmem_wait_st();  // this thread's previous store to the columns has landed
                     if (s == 0) {
                         unsigned ra[8], rb[8], rc[8];
-                        tmem_ld8_nowait(tacc, ra), tmem_ld8_nowait(tacc + 8, rb), tmem_ld8_nowait(tacc + 16, rc);
+                        tmem_ld8_nowait(tacc, ra), tmem_ld8_nowait(tacc + 16, rb), tmem_ld8_nowait(tacc + 24, rc);
                         tmem_wait_ld();
                         double2 x0, x1, y0, y1, z0, z1;
                         tmem_unpack_c2(ra, x0, x1), tmem_unpack_c2(rb, y0, y1), tmem_unpack_c2(rc, z0, z1);
                         tmem_st_c2(tacc, make_double2(x0.x + acc0[0].x, x0.y + acc0[3].x), make_double2(x1.x + acc0[5].x, 0.0));
-                        tmem_st_c2(tacc + 8, cadd(y0, acc0[1]), cadd(y1, acc0[2]));
-                        tmem_st_c2(tacc + 16, cadd(z0, acc0[4]), z1);
+                        tmem_st_c2(tacc + 16, cadd(y0, acc0[1]), cadd(y1, acc0[2]));
+                        tmem_st_c2(tacc + 24, cadd(z0, acc0[4]), z1);
                     } else {
-                        unsigned rd[8], re[8];
-                        tmem_ld8_nowait(tacc + 24, rd), tmem_ld8_nowait(tacc + 32, re);
+                        unsigned ra[8], rc[8], re[8];
+                        tmem_ld8_nowait(tacc + 8, ra), tmem_ld8_nowait(tacc + 24, rc), tmem_ld8_nowait(tacc + 32, re);
                         tmem_wait_ld();
-                        double2 x0, x1, y0, y1;
-                        tmem_unpack_c2(rd, x0, x1), tmem_unpack_c2(re, y0, y1);
-                        tmem_st_c2(tacc + 24, cadd(x0, accS1), cadd(x1, accM1[2]));
-                        tmem_st_c2(tacc + 32, cadd(y0, accM1[3]), y1);
+                        double2 x0, x1, y0, y1, z0, z1;
+                        tmem_unpack_c2(ra, x0, x1), tmem_unpack_c2(rc, y0, y1), tmem_unpack_c2(re, z0, z1);
+                        tmem_st_c2(tacc + 8, cadd(x0, accS1), x1);
+                        tmem_st_c2(tacc + 24, y0, cadd(y1, accM1[2]));
+                        tmem_st_c2(tacc + 32, cadd(z0, accM1[3]), z1);
                     }
                 }
                 if (s == 0) group_sync_t(1 + g);  // sub-step 0 of the whole unit is in the stage
@@ -328,6 +357,7 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
                 if (++ch == CH) ch = 0, ++tau;
             }
         }
+        if (cur_tile >= 0) fold(tp);
     } else if (warp == kT2Consumers) {
         // =========================================================== store warp
         if (lane == 0) {
@@ -390,18 +420,18 @@ __global__ void __maxnreg__(96) k_fused2t(const __grid_constant__ FusedArgs a, c
         const bool cons = warp < kT2Consumers && t < kT2F * kT2N;
         double2 acc0[NU], accS1, accM1[D];
         {
-            double2 q[10];
+            double2 q[16];
             if (warp < kT2Consumers) {
                 tmem_wait_st();
 #pragma unroll
-                for (int i = 0; i < 5; ++i) tmem_ld_c2(tacc + 8 * i, q[2 * i], q[2 * i + 1]);
+                for (int i = 0; i < 8; ++i) tmem_ld_c2(tacc + 8 * i, q[2 * i], q[2 * i + 1]);
             } else {
 #pragma unroll
-                for (int i = 0; i < 10; ++i) q[i] = make_double2(0.0, 0.0);
+                for (int i = 0; i < 16; ++i) q[i] = make_double2(0.0, 0.0);
             }
             acc0[0] = make_double2(q[0].x, 0.0), acc0[3] = make_double2(q[0].y, 0.0), acc0[5] = make_double2(q[1].x, 0.0);
-            acc0[1] = q[2], acc0[2] = q[3], acc0[4] = q[4];
-            accS1 = q[6], accM1[2] = q[7], accM1[3] = q[8];
+            accS1 = q[2];
+            acc0[1] = q[10], acc0[2] = q[11], acc0[4] = q[12], accM1[2] = q[13], accM1[3] = q[14];
             accM1[0] = accM1[1] = make_double2(0.0, 0.0);
         }
 #pragma unroll
