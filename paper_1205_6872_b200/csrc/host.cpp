@@ -775,9 +775,8 @@ static bool encode_f4_tmaps(const qp_plan::LaunchSet &ls, double2 *A) {
 
 // k_fused2t's TMA view of the ARDM for launch set ls (slide2t.cu): a 5-D tensor of FP64 whose box is one
 // unit of 27 outer fibres x the 81 inner entries (d0 = slot p0, d1 = slot p0 + 1); the same map loads
-// and stores.  VK 0 (p0 = 0): [d0][d1][slots 2..L-1]; VK 1 (p0 = L-1): [d1 = slot 0][slots 1..L-2][d0];
-// VK 2 (2 <= p0 <= L-2): [slots 0..p0-1][d0][d1][slots p0+2..]; VK 3 (p0 = 1): the same with a box of
-// 9 x 3 fibres.
+// and stores.  VK 0 (p0 = 0): [d0 d1][slots 2..L-1]; VK 1 (p0 = L-1): [d1 = slot 0, slot 1][slots 2..L-2][d0];
+// VK 2 (2 <= p0 <= L-2): [slots 0..p0-1][d0][d1][slots p0+2..]; VK 3 (p0 = 1): [slot 0, d0][d1][slots 3..].
 static bool encode_f2t_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, double2 *A) {
     if (ls.tma_A == A) return true;
     EncodeTiledFn enc = encode_tiled();
@@ -789,15 +788,23 @@ static bool encode_f2t_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doub
     auto set = [&](std::initializer_list<cuuint64_t> d, std::initializer_list<cuuint64_t> st, std::initializer_list<cuuint32_t> b) {
         std::copy(d.begin(), d.end(), gd), std::copy(st.begin(), st.end(), gs), std::copy(b.begin(), b.end(), bx);
     };
+    // (the two lowest slots are merged into one box dimension of 162 doubles where both lie in the box
+    // whole: 27 rows of 1296 B per unit instead of 243 rows of 144 B)
     switch (ls.f2t) {
-    case 0: set({18, 9, (cuuint64_t)ipow(9, L - 2), 1, 1}, {16 * 9, 16 * 81, big, big}, {18, 9, 27, 1, 1}); break;
-    case 1: set({18, (cuuint64_t)ipow(9, L - 2), 9, 1, 1}, {16 * 9, 16ull * (cuuint64_t)ipow(9, L - 1), big, big}, {18, 27, 9, 1, 1}); break;
-    case 2:
+    case 0:  // [d0 d1 (slots 0, 1)][slots 2..L-1]
+        set({162, (cuuint64_t)ipow(9, L - 2), 1, 1, 1}, {16 * 81, big, big, big}, {162, 27, 1, 1, 1});
+        break;
+    case 1:  // [d1 = slot 0, slot 1][slots 2..L-2][d0 = slot L-1]
+        set({162, (cuuint64_t)ipow(9, L - 3), 9, 1, 1}, {16 * 81, 16ull * (cuuint64_t)ipow(9, L - 1), big, big}, {162, 3, 9, 1, 1});
+        break;
+    case 2:  // [slots 0..p0-1][d0][d1][slots p0+2..L-1]
         set({2ull * (cuuint64_t)ipow(9, p0), 9, 9, (cuuint64_t)ipow(9, L - 2 - p0), 1},
             {16ull * (cuuint64_t)ipow(9, p0), 16ull * (cuuint64_t)ipow(9, p0 + 1), 16ull * (cuuint64_t)ipow(9, p0 + 2), big},
             {54, 9, 9, 1, 1});
         break;
-    default: set({18, 9, 9, (cuuint64_t)ipow(9, L - 3), 1}, {16 * 9, 16 * 81, 16 * 729, big}, {18, 9, 9, 3, 1}); break;
+    default:  // p0 = 1: [slot 0, d0 = slot 1][d1 = slot 2][slots 3..L-1]
+        set({162, 9, (cuuint64_t)ipow(9, L - 3), 1, 1}, {16 * 81, 16 * 729, big, big}, {162, 9, 3, 1, 1});
+        break;
     }
     const cuuint32_t es[5] = {1, 1, 1, 1, 1};
     if (enc(&ls.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)A, gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -817,10 +824,12 @@ static qp_status set_tma(const qp_plan &P, const qp_plan::LaunchSet &ls, qp::Fus
         a.f4_layout = ls.f2t;
         // unit G (first outer fibre) = cB nA + cA: run A (VK 2, 3) as doubles in box dimension 0, the rest in
         // dimension cdimB; VK 0, 1: one coordinate G
-        a.tma_nA = ls.f2t == 2 ? ipow(P.N, ls.p0) : (ls.f2t == 3 ? P.N : 0);
+        // (VK 1, 3: the unit's 27 fibres are all 9 values of the lowest outer slot x 3 of the next ones: the
+        // merged box dimension 0 starts at 0, dimension cdimB at G / 9)
+        a.tma_nA = ls.f2t == 2 ? ipow(P.N, ls.p0) : (ls.f2t == 0 ? 0 : P.N);
         a.tma_c0m = 2;
-        a.f4_cdimA[0] = ls.f2t >= 2 ? 0 : -1;
-        a.f4_cdimB[0] = ls.f2t == 0 ? 2 : (ls.f2t == 1 ? 1 : 3);
+        a.f4_cdimA[0] = ls.f2t == 0 ? -1 : 0;
+        a.f4_cdimB[0] = ls.f2t == 2 ? 3 : (ls.f2t == 3 ? 2 : 1);
         a.E0r = (const double2 *)(w + ls.off_E0r);
         return QP_OK;
     }
