@@ -102,6 +102,9 @@ def kernel_name(sz) -> str:
     if sz.persistent:
         return "k_small: every slide step of the call in one single-CTA launch, ARDM + tables in shared memory"
     if sz.M == 3 and sz.fuse_steps == 2:
+        if sz.block == 576:  # (qp_sizes.block after qp_init)
+            return ("k_fused2t: 2 time steps per HBM pass, TMA load + TMA store of 27-fibre units (5-stage ring, "
+                    "load and store warps, 2 x 8 consumer warps, readout sums in TMEM), one CTA per SM")
         return "k_fused2s: 2 time steps per HBM pass, 32-fibre units staged in shared memory (cp.async)"
     return {4: "k_fused4: 4 time steps per HBM pass, TMA load + TMA store of 8-fibre rounds "
                "(6-stage ring, load and store warps, 8 consumer warps, readout sums in TMEM), one CTA per SM",
@@ -240,6 +243,7 @@ def main():
         nt_fit = {"ms_per_step": float(b), "intercept_ms": float(a), "r2": r2, "points": int(len(xs)),
                   "steps_at": cuts[1:], "note": "wall time linear in the number of time steps (P:455-466)"}
     rho = plan.read_rho(work, stream)
+    sz = plan.sizes  # after qp_init: the launch configuration the timed region ran
     tr_err = float(np.abs(np.einsum("kii->k", rho) - 1).max())
     del ardm, work
     torch.cuda.empty_cache()
