@@ -1,5 +1,5 @@
 // slide2t.cu -- k_fused2t: two consecutive slide steps k, k+1 (k >= L) of the iterative tensor
-// propagator for M = 3 (N = 9, lattice s) in ONE pass over HBM, in place on the ring-buffer ARDM, with
+// propagator for M = 3 (N = 9, s = (c, 0, -c)) in ONE pass over HBM, in place on the ring-buffer ARDM, with
 // the rho(t_k) readout of both steps fused (the algebra and the step
 // fusion are those of slide_r.cu / slide2.cu).  HBM traffic per step: 32/2 = 16 B per ARDM entry.
 // The TMA-staged, warp-specialised form of k_fused2s for unsharded launch sets.
@@ -10,7 +10,8 @@
 //   VK 0 (p0 = 0)        : d0 + 9 d1 + 81 f          (the unit is one contiguous 35 KB block)
 //   VK 1 (p0 = L-1)      : d1 + 9 f + 243 d0
 //   VK 2 (2 <= p0 <= L-2): f + 27 d0 + 243 d1        (27 consecutive fibres of the run of slots < p0)
-//   VK 3 (p0 = 1)        : f%9 + 9 d0 + 81 d1 + 729 (f/9)
+//   VK 3 (p0 = 1)        : f%9 + 9 d0 + 81 d1 + 729 (f/9)   (one contiguous block)
+// (VK 0, 1, 3 merge the two lowest slots into one box dimension: 27 rows of 1296 B per unit.)
 // -- conflict-free 16-B accesses for consecutive fibres in every case.  One CTA per SM, 18 warps:
 //   load warp   : unit r into stage r % NS once the stage's previous unit has been stored (empty[b]):
 //                 one cp.async.bulk.tensor box + one bulk copy of the unit's outer group-0 factors and
@@ -23,8 +24,9 @@
 //                 arrive on the stage's empty barrier.
 // Used for s = (c, 0, -c) (the class moments use the structure of the weights: old-state pairs instead
 // of 9 complex products).  13 of a group's 256 threads idle (a box of 27 fibres tiles every view
-// exactly: no padding traffic).  Readout accumulators in registers, fixed-order CTA reduction at the
-// end (deterministic).
+// exactly: no padding traffic).  Readout: each thread's per-fibre terms go into tensor memory after
+// every sub-step (tcgen05.ld / st), the class-moment terms summed per tile without the tile's inner
+// factor (applied once per tile); fixed-order CTA and grid reductions at the end (deterministic).
 #include "tmem.cuh"
 
 namespace qp {
