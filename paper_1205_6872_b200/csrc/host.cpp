@@ -371,6 +371,7 @@ struct qp_plan {
         mutable CUtensorMap tmapS{};
         // k_fused2t (M = 3 lattice, S = 2, unsharded): view kind (slide2t.cu), -1 none
         int f2t = -1;
+        int f2t_p0 = 0, f2t_L = 0;     // position of inner digit 0 in the (local) layout, its digit count
     };
     int group_w = 1;                   // digits per outer digit group (g >= 1) of the factor tables
     int Smax = 1;
@@ -781,7 +782,7 @@ static bool encode_f2t_tmap(const qp_plan &P, const qp_plan::LaunchSet &ls, doub
     if (ls.tma_A == A) return true;
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return false;
-    const int L = P.L, p0 = ls.p0;
+    const int L = ls.f2t_L, p0 = ls.f2t_p0;  // the local layout (a shard block lacks the shard slots)
     const cuuint64_t big = 16ull * (cuuint64_t)ipow(9, L);
     cuuint64_t gd[5], gs[4];
     cuuint32_t bx[5];
@@ -826,7 +827,7 @@ static qp_status set_tma(const qp_plan &P, const qp_plan::LaunchSet &ls, qp::Fus
         // dimension cdimB; VK 0, 1: one coordinate G
         // (VK 1, 3: the unit's 27 fibres are all 9 values of the lowest outer slot x 3 of the next ones: the
         // merged box dimension 0 starts at 0, dimension cdimB at G / 9)
-        a.tma_nA = ls.f2t == 2 ? ipow(P.N, ls.p0) : (ls.f2t == 0 ? 0 : P.N);
+        a.tma_nA = ls.f2t == 2 ? ipow(P.N, ls.f2t_p0) : (ls.f2t == 0 ? 0 : P.N);
         a.tma_c0m = 2;
         a.f4_cdimA[0] = ls.f2t == 0 ? -1 : 0;
         a.f4_cdimB[0] = ls.f2t == 2 ? 3 : (ls.f2t == 3 ? 2 : 1);
@@ -1031,9 +1032,14 @@ void build_launch_set(const qp_plan &P, int p0, int S, const std::vector<int> &r
         }
     }
     ls.f2t = -1;
-    if (f2s && P.sym3 && removed.empty() && !(P.flags & QP_FLAG_NO_TMA) && L >= 4 && T % 27 == 0 && T / 27 >= 3) {
-        // k_fused2t: one block per 27-fibre unit of a tile: factors [s][kap][d][f] + the 27 lofs (int2)
-        ls.f2t = p0 == 0 ? 0 : (p0 == L - 1 ? 1 : (p0 == 1 ? 3 : 2));
+    const int Lloc = L - (int)removed.size();
+    if (f2s && P.sym3 && !(P.flags & QP_FLAG_NO_TMA) && Lloc >= 4 && T % 27 == 0 && T / 27 >= 3) {
+        // k_fused2t: one block per 27-fibre unit of a tile: factors [s][kap][d][f] + the 27 lofs (int2).
+        // The view follows from the local positions of the inner digits (a shard block's layout has the
+        // shard slots removed; the inner slots are never shard slots)
+        const int l0 = pos[inner[0]], l1 = pos[inner[1]];
+        ls.f2t = (l0 == 0 && l1 == 1) ? 0 : ((l0 == Lloc - 1 && l1 == 0) ? 1 : (l0 == 1 ? 3 : 2));
+        ls.f2t_p0 = l0, ls.f2t_L = Lloc;
         const int F = qp::fused2t_unit_fibres(), R = T / F, Q = S * 2 * D;
         const size_t blk = (size_t)qp::fused2t_e0_block();
         ls.E0r.assign((size_t)R * blk, make_double2(0.0, 0.0));

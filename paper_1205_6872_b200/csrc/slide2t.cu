@@ -2,7 +2,8 @@
 // propagator for M = 3 (N = 9, s = (c, 0, -c)) in ONE pass over HBM, in place on the ring-buffer ARDM, with
 // the rho(t_k) readout of both steps fused (the algebra and the step
 // fusion are those of slide_r.cu / slide2.cu).  HBM traffic per step: 32/2 = 16 B per ARDM entry.
-// The TMA-staged, warp-specialised form of k_fused2s for unsharded launch sets.
+// The TMA-staged, warp-specialised form of k_fused2s (unsharded launch sets and shard blocks: the
+// tensor map is over the block's local layout).
 //
 // A unit is 27 consecutive outer fibres x the 81 entries of the inner digits (d0, d1) = ring slots
 // (p0, p0+1): one TMA box (35 KB) of a tensor map over the ARDM whose shape depends on where ring slot

@@ -41,7 +41,9 @@ def single(w, out_steps=None, **kw):
 @pytest.mark.parametrize("G,M,L,n,lat", [(2, 2, 5, 23, True), (4, 2, 6, 30, True), (8, 2, 6, 25, True),
                                           (3, 2, 7, 20, True), (2, 3, 4, 14, True), (3, 3, 5, 12, False),
                                           (2, 2, 4, 3, True), (2, 2, 9, 40, False), (8, 2, 8, 41, True),
-                                          (4, 2, 11, 40, True), (8, 3, 5, 17, True)])
+                                          (4, 2, 11, 40, True), (8, 3, 5, 17, True),
+                                          # M = 3, s = (1, 0, -1), >= 4 local slots: shard blocks on k_fused2t
+                                          (2, 3, 7, 30, True), (3, 3, 6, 26, True)])
 def test_sharded_matches_single_gpu(G, M, L, n, lat):
     w = W.random_problem(500 + G * 10 + L, M, L, n, kind=W.J_DEBYE, lattice_s=lat)
     ranks = [SH.ShardRank(w, G, r) for r in range(G)]
